@@ -1,0 +1,116 @@
+/*
+ * attnqat_b200 -- C ABI of the B200 (sm_100a) NVFP4 Attn-QAT attention path.
+ *
+ * This is the drop-in boundary for the reference package's operator API
+ * (/root/reference/pkg/src/attnqat). Plain pointers, sizes and a CUDA stream
+ * (passed as void*); no torch types. Every function is stream-ordered, never
+ * synchronises the host, never allocates device memory (callers pass
+ * workspaces sized by the *_workspace_bytes queries) and returns an AqStatus.
+ *
+ * dtype codes: 0 = float32, 1 = bfloat16, 2 = float16.
+ * Tensors are [heads][n][d] contiguous per head (head stride / row stride
+ * given explicitly where noted). `heads` is the flattened batch*heads count.
+ */
+#ifndef ATTNQAT_B200_H_
+#define ATTNQAT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes map 1:1 onto the reference exception classes
+ * (attnqat/errors.py:4-41). */
+typedef enum {
+  AQ_OK = 0,
+  AQ_E_SHAPE = 1,          /* ShapeError     errors.py:12-13 */
+  AQ_E_TILE = 2,           /* TileError      errors.py:16-17 */
+  AQ_E_INVALID = 3,        /* InvalidValue   errors.py:8-9   */
+  AQ_E_MISSING_OPRIME = 4, /* MissingOPrime  errors.py:30-31 */
+  AQ_E_CUDA = 5,           /* CUDA launch / runtime failure   */
+  AQ_E_UNSUPPORTED = 6     /* head dim other than 64 / 128    */
+} AqStatus;
+
+/* Backward variants (attnqat/flash.py:83-95, BwdVariant). */
+typedef enum {
+  AQ_BWD_CORRECT = 0,         /* D = rowsum(dO . O'), P^F in dV */
+  AQ_BWD_LOW_PREC_O = 1,      /* D = rowsum(dO . O),  P^F in dV */
+  AQ_BWD_NO_FAKE_QUANT_P = 2, /* D = rowsum(dO . O'), P   in dV */
+  AQ_BWD_NAIVE_BF16 = 3       /* D = rowsum(dO . O),  P   in dV */
+} AqBwdVariant;
+
+int aq_abi_version(void);
+const char* aq_status_string(int status);
+
+/* ---- NVFP4 codec --------------------------------------------------------
+ * Replaces attnqat.codec.quantize / fake_quantize (codec.py:302-340).
+ * Blocks of 16 along the contiguous axis of x [heads][n][cols]
+ * (row stride ld, head stride hs, in elements). Outputs in the reference
+ * layout: codes [heads*n][cols/2] (low nibble = lower index), scales
+ * [heads*n][cols/16] E4M3 codes; fq (optional) = dequantized values in
+ * fq_dtype. nonfinite (optional, device int) is OR-ed with 1 when an input
+ * is NaN/Inf (the reference raises InvalidValue, codec.py:313-314). */
+int aq_quantize_rows(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld,
+                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite,
+                     void* stream);
+
+/* Replaces quantize_padded(V.T) / fake_quantize_cols (codec.py:359-381):
+ * blocks of 16 along the token axis of x [heads][n][cols]; the token tail is
+ * zero-padded to n16 = ceil(n/16)*16. codes [heads][cols][n16/2], scales
+ * [heads][cols][n16/16]; fq (optional) [heads][n][cols]. */
+int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld,
+                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite,
+                     void* stream);
+
+/* Replaces attnqat.codec.dequantize (codec.py:327-333). rows x cols. */
+int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
+                  int out_dtype, void* stream);
+
+/* ---- fused attention ----------------------------------------------------- */
+typedef struct {
+  const void* q; const void* k; const void* v; /* [heads][n_q|n_k][d], dtype in_dtype */
+  int in_dtype;
+  int64_t heads, n_q, n_k, d;
+  int causal;        /* right-aligned causal mask (oracle.py:62-75) */
+  int train;         /* 1: flash_forward_training (emit O_hp), 0: flash_forward_inference */
+  void* o;           /* [heads][n_q][d], o_dtype */
+  int o_dtype;
+  void* o_hp;        /* [heads][n_q][d] O' (train only; may be NULL) */
+  int o_hp_dtype;
+  float* lse;        /* [heads][n_q] natural-log LSE L (flash.py:217) */
+  void* workspace;   /* aq_attn_fwd_workspace_bytes(); keep it for the backward */
+  int keep_for_bwd;  /* also stage the bf16 operands the backward reuses */
+} AqFwdArgs;
+
+int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train,
+                                    int keep_for_bwd);
+/* Replaces flash_forward_training / flash_forward_inference (flash.py:176-314). */
+int aq_attn_fwd(const AqFwdArgs* args, void* stream);
+
+typedef struct {
+  const void* q; const void* k; const void* v; /* original operands, in_dtype */
+  int in_dtype;
+  const void* d_o;   /* [heads][n_q][d], do_dtype */
+  int do_dtype;
+  const void* o;     /* forward O  (LOW_PREC_O / NAIVE); dtype o_dtype */
+  const void* o_hp;  /* forward O' (CORRECT / NO_FAKE_QUANT_P); dtype o_dtype */
+  int o_dtype;
+  const float* lse;  /* [heads][n_q] */
+  int64_t heads, n_q, n_k, d;
+  int causal;
+  int variant;       /* AqBwdVariant */
+  void* dq; void* dk; void* dv; /* [heads][n][d], g_dtype */
+  int g_dtype;
+  void* workspace;   /* aq_attn_bwd_workspace_bytes() */
+  const void* fwd_workspace; /* forward workspace with keep_for_bwd=1, or NULL to re-quantize */
+} AqBwdArgs;
+
+int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d);
+/* Replaces flash_backward (flash.py:317-390). */
+int aq_attn_bwd(const AqBwdArgs* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTNQAT_B200_H_ */

@@ -1,0 +1,17 @@
+"""B200-native (sm_100a) NVFP4 Attn-QAT attention: drop-in for the reference
+``attnqat`` operator API (quantize / dequantize / fake_quantize /
+fake_quantize_cols, flash_forward_training / flash_forward_inference /
+flash_backward) plus a torch.autograd.Function for batched CUDA tensors.
+All compute runs in ``libattnqat_b200.so`` (hand-written sm_100a CUDA through
+a C ABI); there is no CPU fallback.
+"""
+
+from .autograd import AttnQATFunction, attn_qat
+from .codec import (MXFP4, NVFP4, BlockSpec, QuantTensor, ScaleFormat, dequantize, fake_quantize,
+                    fake_quantize_cols, fake_quantize_padded, quantize, quantize_cols, quantize_padded)
+from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, ShapeError, StabilityError,
+                     TileError)
+from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward,
+                    flash_backward, flash_forward_inference, flash_forward_training)
+
+__version__ = "0.1.0"

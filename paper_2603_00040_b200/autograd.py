@@ -1,0 +1,37 @@
+"""``torch.autograd.Function`` for NVFP4 Attn-QAT attention on [..., N, d] CUDA tensors.
+
+Forward = flash_forward_training (O is the FP4-path output that flows to the
+next layer; O' and L are saved). Backward = flash_backward with the chosen
+BwdVariant: D = rowsum(dO . O'), P recomputed at forward precision and
+re-quantized for dV, straight-through gradients for Q/K/V (flash.py:317-390).
+The quantized operands staged by the forward are kept in a workspace and
+reused by the backward instead of re-quantizing.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .flash import BwdVariant, attn_backward, attn_forward
+
+
+class AttnQATFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT):
+        o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True)
+        ctx.save_for_backward(q, k, v, o, o_hp, lse, ws)
+        ctx.causal = causal
+        ctx.variant = variant
+        return o
+
+    @staticmethod
+    def backward(ctx, d_o):
+        q, k, v, o, o_hp, lse, ws = ctx.saved_tensors
+        dq, dk, dv = attn_backward(q, k, v, d_o.contiguous(), o, o_hp, lse, causal=ctx.causal,
+                                   variant=ctx.variant, grad_dtype=q.dtype, fwd_workspace=ws)
+        return dq, dk, dv, None, None
+
+
+def attn_qat(q, k, v, causal=False, variant=BwdVariant.CORRECT):
+    """NVFP4 QAT attention: O = softmax_fq(Q^F K^F^T / sqrt(d)) V^F with the Attn-QAT backward."""
+    return AttnQATFunction.apply(q, k, v, causal, variant)

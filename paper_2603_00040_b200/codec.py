@@ -1,0 +1,212 @@
+"""NVFP4 codec on the GPU, mirroring ``attnqat.codec`` (codec.py:145-381).
+
+Same names, argument meaning and errors as the reference; the arithmetic runs
+in the sm_100a quantizer kernels (csrc/quantize.cu) through the C ABI.
+Inputs may be NumPy arrays (uploaded; results come back as NumPy) or torch
+tensors (results stay on the GPU). float64 inputs are rounded to float32 on
+upload -- the kernels quantize fp32 / bf16 / fp16 values (bit-exact versus the
+reference for every value representable in those formats).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidValue, ShapeError
+
+FP4_MAX = 6.0
+E4M3_MAX = 448.0
+
+
+class ScaleFormat(Enum):
+    E4M3 = 0
+    E8M0 = 1
+
+
+@dataclass(frozen=True)
+class BlockSpec:
+    """Block size and scale format (codec.py:150-163)."""
+
+    block_size: int
+    scale_format: ScaleFormat
+
+    def __post_init__(self):
+        if (self.block_size, self.scale_format) not in {(16, ScaleFormat.E4M3), (32, ScaleFormat.E8M0)}:
+            raise InvalidValue(f"unsupported block spec ({self.block_size}, {self.scale_format})")
+
+
+NVFP4 = BlockSpec(16, ScaleFormat.E4M3)
+MXFP4 = BlockSpec(32, ScaleFormat.E8M0)
+
+
+def _require_nvfp4(spec):
+    if spec != NVFP4:
+        raise InvalidValue("the B200 path implements NVFP4 (16-element blocks, E4M3 scales) only")
+
+
+@dataclass
+class QuantTensor:
+    """Packed FP4 codes (rows, cols/2) + row-major scale grid (rows, cols/16) (codec.py:260-299)."""
+
+    rows: int
+    cols: int
+    spec: BlockSpec
+    codes: object
+    scales: object
+
+    @property
+    def block_grid(self):
+        return (self.rows, self.cols // self.spec.block_size)
+
+    def row_slice(self, start, stop):
+        return QuantTensor(stop - start, self.cols, self.spec, self.codes[start:stop], self.scales[start:stop])
+
+    def col_slice(self, start, stop):
+        bs = self.spec.block_size
+        if start % bs or stop % bs:
+            raise ShapeError("column slices must align to block boundaries")
+        return QuantTensor(self.rows, stop - start, self.spec, self.codes[:, start // 2:stop // 2],
+                           self.scales[:, start // bs:stop // bs])
+
+
+def to_device(x, allow_f64=True):
+    """(cuda tensor, came_from_numpy). float64 is rounded to float32."""
+    _lib.require_cuda()
+    if isinstance(x, torch.Tensor):
+        t, was_np = x, False
+    else:
+        t, was_np = torch.from_numpy(np.ascontiguousarray(np.asarray(x))), True
+    if not t.is_floating_point():
+        t = t.to(torch.float32)
+    if t.dtype == torch.float64:
+        t = t.to(torch.float32)
+    return t.to("cuda").contiguous(), was_np
+
+
+def _out(t, as_numpy, np_dtype=None):
+    if not as_numpy:
+        return t
+    a = t.cpu().numpy()
+    return a.astype(np_dtype) if np_dtype is not None else a
+
+
+def _nonfinite_check(flag):
+    if int(flag.item()):
+        raise InvalidValue("quantize requires finite input")
+
+
+def quantize(x, spec=NVFP4) -> QuantTensor:
+    """Block-row-wise NVFP4 quantization (codec.py:302-324)."""
+    _require_nvfp4(spec)
+    t, was_np = to_device(x)
+    if t.dim() != 2:
+        raise ShapeError("quantize expects a 2-D tensor")
+    rows, cols = t.shape
+    if cols % spec.block_size:
+        raise ShapeError(f"cols ({cols}) must be a multiple of block_size ({spec.block_size});"
+                         " padding is the caller's responsibility")
+    codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=t.device)
+    scales = torch.empty((rows, cols // 16), dtype=torch.uint8, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_quantize_rows(
+        _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, rows, cols, cols, rows * cols,
+        _lib.ptr(codes), _lib.ptr(scales), None, 0, _lib.ptr(flag), _lib.stream_ptr()))
+    _nonfinite_check(flag)
+    return QuantTensor(rows, cols, spec, _out(codes, was_np), _out(scales, was_np))
+
+
+_NP2T = {np.float32: torch.float32, np.float64: torch.float32, np.float16: torch.float16}
+
+
+def dequantize(qt: QuantTensor, dtype=np.float32):
+    """code x scale, exact (codec.py:327-333)."""
+    was_np = not isinstance(qt.codes, torch.Tensor)
+    codes = torch.as_tensor(np.ascontiguousarray(qt.codes) if was_np else qt.codes).to("cuda").contiguous()
+    scales = torch.as_tensor(np.ascontiguousarray(qt.scales) if was_np else qt.scales).to("cuda").contiguous()
+    tdt = dtype if isinstance(dtype, torch.dtype) else _NP2T.get(np.dtype(dtype).type, torch.float32)
+    out = torch.empty((qt.rows, qt.cols), dtype=tdt, device="cuda")
+    _lib.check(_lib.load().aq_dequantize(_lib.ptr(codes), _lib.ptr(scales), qt.rows, qt.cols,
+                                         _lib.ptr(out), _lib.DT_CODE[tdt], _lib.stream_ptr()))
+    return _out(out, was_np, None if isinstance(dtype, torch.dtype) else dtype)
+
+
+def fake_quantize(x, spec=NVFP4):
+    """Quantize-then-dequantize, shape and dtype preserved (codec.py:336-340)."""
+    _require_nvfp4(spec)
+    t, was_np = to_device(x)
+    if t.dim() != 2:
+        raise ShapeError("quantize expects a 2-D tensor")
+    rows, cols = t.shape
+    if cols % spec.block_size:
+        raise ShapeError(f"cols ({cols}) must be a multiple of block_size ({spec.block_size})")
+    out = torch.empty_like(t)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_quantize_rows(
+        _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, rows, cols, cols, rows * cols,
+        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _lib.ptr(flag), _lib.stream_ptr()))
+    _nonfinite_check(flag)
+    np_dt = np.asarray(x).dtype if was_np else None
+    return _out(out, was_np, np_dt)
+
+
+def pad_cols(x, block_size):
+    """Zero-pad the column axis to a block multiple (codec.py:343-356)."""
+    cols = x.shape[1]
+    rem = cols % block_size
+    if rem == 0:
+        return x
+    if isinstance(x, torch.Tensor):
+        return torch.nn.functional.pad(x, (0, block_size - rem))
+    out = np.zeros((x.shape[0], cols + block_size - rem), dtype=np.asarray(x).dtype)
+    out[:, :cols] = x
+    return out
+
+
+def quantize_padded(x, spec=NVFP4):
+    """codec.py:359-361."""
+    return quantize(pad_cols(x, spec.block_size), spec)
+
+
+def fake_quantize_padded(x, spec=NVFP4):
+    """codec.py:364-370."""
+    n = x.shape[1]
+    out = fake_quantize(pad_cols(x, spec.block_size), spec)
+    return out[:, :n] if out.shape[1] != n else out
+
+
+def fake_quantize_cols(x, spec=NVFP4):
+    """Blocks along the token (row) axis, ragged tail zero-padded (codec.py:373-381)."""
+    _require_nvfp4(spec)
+    t, was_np = to_device(x)
+    if t.dim() != 2:
+        raise ShapeError("quantize expects a 2-D tensor")
+    n, cols = t.shape
+    out = torch.empty_like(t)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_quantize_cols(
+        _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, n, cols, cols, n * cols,
+        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _lib.ptr(flag), _lib.stream_ptr()))
+    _nonfinite_check(flag)
+    np_dt = np.asarray(x).dtype if was_np else None
+    return _out(out, was_np, np_dt)
+
+
+def quantize_cols(x, spec=NVFP4) -> QuantTensor:
+    """QuantTensor of x^T with the token axis zero-padded: quantize_padded(x.T) (flash.py:267)."""
+    _require_nvfp4(spec)
+    t, was_np = to_device(x)
+    n, cols = t.shape
+    n16 = -(-n // 16) * 16
+    codes = torch.empty((cols, n16 // 2), dtype=torch.uint8, device=t.device)
+    scales = torch.empty((cols, n16 // 16), dtype=torch.uint8, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_quantize_cols(
+        _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, n, cols, cols, n * cols,
+        _lib.ptr(codes), _lib.ptr(scales), None, 0, _lib.ptr(flag), _lib.stream_ptr()))
+    _nonfinite_check(flag)
+    return QuantTensor(cols, n16, spec, _out(codes, was_np), _out(scales, was_np))

@@ -1,0 +1,300 @@
+// C-ABI entry points (include/attnqat_b200.h). Validates arguments the way the
+// reference does (ShapeError / TileError / MissingOPrime), carves the
+// caller-owned workspace, and launches the quantizers + attention kernels on
+// the caller's stream. No host synchronisation, no device allocation.
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/attnqat_b200.h"
+#include "attn.h"
+#include "layouts.cuh"
+
+using namespace aq;
+
+namespace {
+
+constexpr int kAbiVersion = 1;
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+struct FwdWs {
+  int64_t q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, v_h16, q_hb, k_hb, v_hb, total;
+};
+
+FwdWs fwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int keep) {
+  const int64_t qt = ceil_div(n_q, TILE), kt = ceil_div(n_k, TILE);
+  FwdWs w{};
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.q_codes = take(heads * qt * fp4_tile_bytes(static_cast<int>(d)));
+  w.q_sf = take(heads * qt * sf_tile_bytes_qk(static_cast<int>(d)));
+  w.k_codes = take(heads * kt * fp4_tile_bytes(static_cast<int>(d)));
+  w.k_sf = take(heads * kt * sf_tile_bytes_qk(static_cast<int>(d)));
+  w.v_codes = take(heads * kt * fp4_tile_bytes(static_cast<int>(d)));
+  w.v_sf = take(heads * kt * kSfTileBytesV);
+  // fp16 V^F tiles feed the O' MMA; a kept workspace always carries them so the
+  // layout does not depend on the forward mode
+  w.v_h16 = (train || keep) ? take(heads * kt * h_tile_bytes(static_cast<int>(d))) : -1;
+  w.q_hb = keep ? take(heads * qt * h_tile_bytes(static_cast<int>(d))) : -1;
+  w.k_hb = keep ? take(heads * kt * h_tile_bytes(static_cast<int>(d))) : -1;
+  w.v_hb = keep ? take(heads * kt * h_tile_bytes(static_cast<int>(d))) : -1;
+  w.total = off;
+  return w;
+}
+
+struct BwdWs {
+  int64_t fwd, do_h, delta, dq_acc, total;
+};
+
+BwdWs bwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
+  BwdWs w{};
+  const FwdWs f = fwd_ws(heads, n_q, n_k, d, 0, 1);
+  const int64_t qt = ceil_div(n_q, TILE);
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.fwd = take(f.total);  // re-quantized operands when no forward workspace is given
+  w.do_h = take(heads * qt * h_tile_bytes(static_cast<int>(d)));
+  w.delta = take(heads * qt * TILE * 4);
+  w.dq_acc = take(heads * n_q * d * 4);
+  w.total = off;
+  return w;
+}
+
+bool dtype_ok(int dt) { return dt == 0 || dt == 1 || dt == 2; }
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? AQ_OK : AQ_E_CUDA; }
+
+// Stage Q/K/V into the attention layouts (K1/K2 in tiled mode).
+int stage_operands(const void* q, const void* k, const void* v, int in_dt, int64_t heads, int64_t n_q, int64_t n_k,
+                   int64_t d, uint8_t* ws, const FwdWs& w, cudaStream_t st) {
+  RowsArgs a{};
+  a.x_dt = in_dt;
+  a.heads = heads;
+  a.cols = d;
+  a.ld = d;
+  // Q
+  a.x = q;
+  a.n = n_q;
+  a.hs = n_q * d;
+  a.codes_t = ws + w.q_codes;
+  a.sf_t = ws + w.q_sf;
+  a.fqh_t = w.q_hb >= 0 ? ws + w.q_hb : nullptr;
+  a.fqh_dt = 1;
+  cudaError_t e = launch_quantize_rows(a, st);
+  if (e != cudaSuccess) return AQ_E_CUDA;
+  // K
+  a.x = k;
+  a.n = n_k;
+  a.hs = n_k * d;
+  a.codes_t = ws + w.k_codes;
+  a.sf_t = ws + w.k_sf;
+  a.fqh_t = w.k_hb >= 0 ? ws + w.k_hb : nullptr;
+  e = launch_quantize_rows(a, st);
+  if (e != cudaSuccess) return AQ_E_CUDA;
+  // V (blocks along tokens): fp16 tiles for the O' MMA, bf16 tiles for the backward
+  a.x = v;
+  a.codes_t = ws + w.v_codes;
+  a.sf_t = ws + w.v_sf;
+  a.fqh_t = w.v_h16 >= 0 ? ws + w.v_h16 : nullptr;
+  a.fqh_dt = 2;
+  e = launch_quantize_cols(a, st);
+  if (e != cudaSuccess) return AQ_E_CUDA;
+  if (w.v_hb >= 0) {
+    RowsArgs b = a;
+    b.codes_t = nullptr;
+    b.sf_t = nullptr;
+    b.fqh_t = ws + w.v_hb;
+    b.fqh_dt = 1;
+    e = launch_quantize_cols(b, st);
+    if (e != cudaSuccess) return AQ_E_CUDA;
+  }
+  return AQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int aq_abi_version(void) { return kAbiVersion; }
+
+const char* aq_status_string(int s) {
+  switch (s) {
+    case AQ_OK: return "ok";
+    case AQ_E_SHAPE: return "shape error";
+    case AQ_E_TILE: return "tile error";
+    case AQ_E_INVALID: return "invalid value";
+    case AQ_E_MISSING_OPRIME: return "missing O_prime";
+    case AQ_E_CUDA: return "CUDA error";
+    case AQ_E_UNSUPPORTED: return "unsupported configuration";
+    default: return "unknown status";
+  }
+}
+
+int aq_quantize_rows(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld, int64_t hs,
+                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite, void* stream) {
+  if (!x || !dtype_ok(x_dtype) || (fq && !dtype_ok(fq_dtype))) return AQ_E_INVALID;
+  if (heads < 0 || n < 0 || cols <= 0 || cols % 16 || ld < cols) return AQ_E_SHAPE;
+  if (heads == 0 || n == 0) return AQ_OK;
+  RowsArgs a{};
+  a.x = x;
+  a.x_dt = x_dtype;
+  a.heads = heads;
+  a.n = n;
+  a.cols = cols;
+  a.ld = ld;
+  a.hs = hs;
+  a.codes_ref = codes;
+  a.scales_ref = scales;
+  a.fq = fq;
+  a.fq_dt = fq_dtype;
+  a.nonfinite = nonfinite;
+  return cuda_status(launch_quantize_rows(a, static_cast<cudaStream_t>(stream)));
+}
+
+int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld, int64_t hs,
+                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite, void* stream) {
+  if (!x || !dtype_ok(x_dtype) || (fq && !dtype_ok(fq_dtype))) return AQ_E_INVALID;
+  if (heads < 0 || n < 0 || cols <= 0 || ld < cols) return AQ_E_SHAPE;
+  if (heads == 0 || n == 0) return AQ_OK;
+  RowsArgs a{};
+  a.x = x;
+  a.x_dt = x_dtype;
+  a.heads = heads;
+  a.n = n;
+  a.cols = cols;
+  a.ld = ld;
+  a.hs = hs;
+  a.codes_ref = codes;
+  a.scales_ref = scales;
+  a.fq = fq;
+  a.fq_dt = fq_dtype;
+  a.nonfinite = nonfinite;
+  return cuda_status(launch_quantize_cols(a, static_cast<cudaStream_t>(stream)));
+}
+
+int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out, int out_dtype,
+                  void* stream) {
+  if (!codes || !scales || !out || !dtype_ok(out_dtype)) return AQ_E_INVALID;
+  if (rows < 0 || cols <= 0 || cols % 16) return AQ_E_SHAPE;
+  if (rows == 0) return AQ_OK;
+  return cuda_status(launch_dequantize(codes, scales, rows, cols, out, out_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int keep) {
+  if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128)) return 0;
+  return fwd_ws(heads, n_q, n_k, d, train, keep).total;
+}
+
+int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
+  if (!a || !a->q || !a->k || !a->v || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->o_dtype) || (a->o_hp && !dtype_ok(a->o_hp_dtype))) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d % 16) return AQ_E_SHAPE;  // flash.py:187-188
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;  // oracle.py:62-66
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, a->keep_for_bwd);
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws, w, st);
+  if (s != AQ_OK) return s;
+  FwdParams p{};
+  p.q_codes = ws + w.q_codes;
+  p.q_sf = ws + w.q_sf;
+  p.k_codes = ws + w.k_codes;
+  p.k_sf = ws + w.k_sf;
+  p.v_codes = ws + w.v_codes;
+  p.v_sf = ws + w.v_sf;
+  p.v_h = a->train ? ws + w.v_h16 : nullptr;
+  p.o = a->o;
+  p.o_dt = a->o_dtype;
+  p.o_hp = a->train ? a->o_hp : nullptr;
+  p.o_hp_dt = a->o_hp_dtype;
+  p.lse = a->lse;
+  p.heads = a->heads;
+  p.n_q = a->n_q;
+  p.n_k = a->n_k;
+  p.d = static_cast<int>(a->d);
+  p.causal = a->causal;
+  p.train = a->train;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  return cuda_status(launch_attn_fwd(p, st));
+}
+
+int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
+  if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128)) return 0;
+  return bwd_ws(heads, n_q, n_k, d).total;
+}
+
+int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
+  if (!a || !a->q || !a->k || !a->v || !a->d_o || !a->lse || !a->dq || !a->dk || !a->dv || !a->workspace)
+    return AQ_E_INVALID;
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->do_dtype) || !dtype_ok(a->o_dtype) || !dtype_ok(a->g_dtype))
+    return AQ_E_INVALID;
+  if (a->variant < 0 || a->variant > 3) return AQ_E_INVALID;
+  const bool uses_op = a->variant == AQ_BWD_CORRECT || a->variant == AQ_BWD_NO_FAKE_QUANT_P;  // flash.py:89-91
+  const void* o_ref = uses_op ? a->o_hp : a->o;
+  if (uses_op && !a->o_hp) return AQ_E_MISSING_OPRIME;  // flash.py:333-337
+  if (!o_ref) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d % 16) return AQ_E_SHAPE;
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const BwdWs bw = bwd_ws(a->heads, a->n_q, a->n_k, a->d);
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  const FwdWs fw = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 1);
+  const uint8_t* ops;
+  FwdWs w;
+  if (a->fwd_workspace) {
+    ops = static_cast<const uint8_t*>(a->fwd_workspace);
+    w = fw;
+  } else {
+    // re-fake-quantize Q, K, V from the originals (flash.py:344-349)
+    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws + bw.fwd, fw, st);
+    if (s != AQ_OK) return s;
+    ops = ws + bw.fwd;
+    w = fw;
+  }
+  float* delta = reinterpret_cast<float*>(ws + bw.delta);
+  float* dq_acc = reinterpret_cast<float*>(ws + bw.dq_acc);
+  cudaError_t e = launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, static_cast<int>(a->d),
+                                 delta, ws + bw.do_h, dq_acc, st);
+  if (e != cudaSuccess) return AQ_E_CUDA;
+  BwdParams p{};
+  p.q_codes = ops + w.q_codes;
+  p.q_sf = ops + w.q_sf;
+  p.k_codes = ops + w.k_codes;
+  p.k_sf = ops + w.k_sf;
+  p.q_h = ops + w.q_hb;
+  p.k_h = ops + w.k_hb;
+  p.v_h = ops + w.v_hb;
+  p.do_h = ws + bw.do_h;
+  p.lse = a->lse;
+  p.delta = delta;
+  p.dq_acc = dq_acc;
+  p.dk = a->dk;
+  p.dv = a->dv;
+  p.g_dt = a->g_dtype;
+  p.heads = a->heads;
+  p.n_q = a->n_q;
+  p.n_k = a->n_k;
+  p.d = static_cast<int>(a->d);
+  p.causal = a->causal;
+  p.fq_p = (a->variant == AQ_BWD_CORRECT || a->variant == AQ_BWD_LOW_PREC_O) ? 1 : 0;  // flash.py:93-95
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  p.inv_sqrt_d = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a->d)));
+  e = launch_attn_bwd(p, st);
+  if (e != cudaSuccess) return AQ_E_CUDA;
+  return cuda_status(launch_dq_convert(dq_acc, a->dq, a->g_dtype, a->heads * a->n_q * a->d, st));
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Internal kernel parameter blocks and launchers (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aq {
+
+struct RowsArgs {
+  const void* x;
+  int x_dt;
+  int64_t heads, n, cols, ld, hs;
+  uint8_t* codes_ref;
+  uint8_t* scales_ref;
+  void* fq;
+  int fq_dt;
+  uint8_t* codes_t;
+  uint8_t* sf_t;
+  void* fqh_t;
+  int fqh_dt;
+  int* nonfinite;
+};
+
+struct FwdParams {
+  const uint8_t* q_codes;
+  const uint8_t* q_sf;
+  const uint8_t* k_codes;
+  const uint8_t* k_sf;
+  const uint8_t* v_codes;  // V^T tiles
+  const uint8_t* v_sf;
+  const uint8_t* v_h;      // fp16 T8x8 tiles of V^F (train)
+  void* o;
+  int o_dt;
+  void* o_hp;
+  int o_hp_dt;
+  float* lse;
+  int64_t heads, n_q, n_k;
+  int d;
+  int causal;
+  int train;
+  float scale_log2;
+};
+
+struct BwdParams {
+  const uint8_t* q_codes;
+  const uint8_t* q_sf;
+  const uint8_t* k_codes;
+  const uint8_t* k_sf;
+  const uint8_t* q_h;    // bf16 T8x8 Q^F tiles
+  const uint8_t* k_h;    // bf16 T8x8 K^F tiles
+  const uint8_t* v_h;    // bf16 T8x8 V^F tiles
+  const uint8_t* do_h;   // bf16 T8x8 dO tiles
+  const float* lse;      // [heads][n_q]
+  const float* delta;    // [heads][nq_pad] D = rowsum(dO . O_ref)
+  float* dq_acc;         // [heads][n_q][d] fp32, zero-initialised
+  void* dk;
+  void* dv;
+  int g_dt;
+  int64_t heads, n_q, n_k;
+  int d;
+  int causal;
+  int fq_p;              // quantize the recomputed P for dV
+  float scale_log2;      // log2(e)/sqrt(d)
+  float inv_sqrt_d;
+};
+
+cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st);
+cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st);
+cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
+                              int out_dt, cudaStream_t st);
+cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
+cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
+                           int d, float* delta, uint8_t* do_h, float* dq_acc, cudaStream_t st);
+cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int g_dt, int64_t count, cudaStream_t st);
+
+}  // namespace aq

@@ -1,0 +1,264 @@
+"""Fused NVFP4 Attn-QAT attention, mirroring ``attnqat.flash`` (flash.py:50-390).
+
+``flash_forward_training`` / ``flash_forward_inference`` / ``flash_backward``
+keep the reference names, arguments, return types and exceptions. Besides the
+reference's 2-D per-head (N, d) operands they accept batched [..., N, d]
+torch tensors (leading dims are flattened into heads, every head independent).
+
+Differences from the CPU reference, by design of the B200 path:
+  * tiles are fixed at 128 x 128 inside the kernels; ``TileConfig`` is still
+    validated exactly as the reference does (results are tiling-invariant,
+    test_flash.py:72-84) and b_q / b_k are otherwise ignored;
+  * accumulation is fp32 on the tensor cores (``accum_width=64`` raises
+    InvalidValue); ``instrument`` and ``threads`` are accepted and ignored.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import NVFP4, BlockSpec, to_device
+from .errors import InvalidValue, MissingOPrime, ShapeError, TileError
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Tile row counts plus the numeric knobs (flash.py:50-71)."""
+
+    b_q: int
+    b_k: int
+    causal: bool = False
+    accum_width: int = 32
+    spec: BlockSpec = NVFP4
+
+    def validate(self, n_q, n_k, quantized):
+        if self.b_q <= 0 or self.b_k <= 0:
+            raise TileError("tile sizes must be positive")
+        if n_q % self.b_q or n_k % self.b_k:
+            raise TileError(f"tiles ({self.b_q}, {self.b_k}) must divide ({n_q}, {n_k})")
+        if quantized and n_k > self.b_k and self.b_k % self.spec.block_size:
+            raise TileError("b_k must be a multiple of the block size so probability blocks align across tiles")
+
+
+@dataclass
+class AttnOutputs:
+    """O and the log-sum-exp L; O_prime only in training mode (flash.py:74-80)."""
+
+    O: object
+    L: object
+    O_prime: object = None
+
+
+@dataclass
+class AttnGrads:
+    """oracle.py:134-138."""
+
+    dQ: object
+    dK: object
+    dV: object
+
+
+class BwdVariant(Enum):
+    """flash.py:83-95."""
+
+    CORRECT = "correct"
+    LOW_PREC_O = "lowpreco"
+    NO_FAKE_QUANT_P = "nofqp"
+    NAIVE_BF16_BWD = "naive-bf16-bwd"
+
+    @property
+    def uses_o_prime(self):
+        return self in (BwdVariant.CORRECT, BwdVariant.NO_FAKE_QUANT_P)
+
+    @property
+    def fake_quantizes_p(self):
+        return self in (BwdVariant.CORRECT, BwdVariant.LOW_PREC_O)
+
+    @property
+    def code(self):
+        return {BwdVariant.CORRECT: 0, BwdVariant.LOW_PREC_O: 1,
+                BwdVariant.NO_FAKE_QUANT_P: 2, BwdVariant.NAIVE_BF16_BWD: 3}[self]
+
+
+# ----------------------------------------------------------------------------
+# batched device entry points (what the autograd Function and benches call)
+# ----------------------------------------------------------------------------
+
+def _heads_view(t):
+    if t.dim() < 2:
+        raise ShapeError("attention operands need at least 2 dims (n, d)")
+    n, d = t.shape[-2:]
+    return t.reshape(-1, n, d), n, d
+
+
+def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd=False, lse_out=None):
+    """Fused forward on CUDA tensors [..., N, d] -> (O, L, O_hp or None, workspace).
+
+    ``train=True`` is flash_forward_training (O, L, O'), ``False`` is
+    flash_forward_inference (O, L). O is the FP4-path output, O' the
+    high-precision output the QAT backward needs (flash.py:176-246)."""
+    _lib.require_cuda()
+    q3, n_q, d = _heads_view(q)
+    k3, n_k, dk = _heads_view(k)
+    v3, n_v, dv = _heads_view(v)
+    if dk != d or dv != d or n_v != n_k or k3.shape[0] != q3.shape[0] or v3.shape[0] != q3.shape[0]:
+        raise ShapeError(f"inconsistent shapes Q{tuple(q.shape)} K{tuple(k.shape)} V{tuple(v.shape)}")
+    if d % 16:
+        raise ShapeError("d must be a multiple of the block size when quantizing")
+    if causal and n_q > n_k:
+        raise ShapeError("causal attention requires N_q <= N_k")
+    dt = q.dtype
+    if k.dtype != dt or v.dtype != dt or dt not in _lib.DT_CODE:
+        raise InvalidValue("q, k, v must share a float32 / bfloat16 / float16 dtype")
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    heads = q3.shape[0]
+    out_dtype = out_dtype or dt
+    lib = _lib.load()
+    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, int(train), int(keep_for_bwd))
+    if ws_bytes <= 0:
+        raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    o = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
+    o_hp = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device) if train else None
+    lse = lse_out if lse_out is not None else torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
+    args = _lib.AqFwdArgs(
+        q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
+        heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=int(train),
+        o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype],
+        o_hp=o_hp.data_ptr() if o_hp is not None else None, o_hp_dtype=_lib.DT_CODE[out_dtype],
+        lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=int(keep_for_bwd))
+    _lib.check(lib.aq_attn_fwd(args, _lib.stream_ptr()))
+    lead = q.shape[:-2]
+    return (o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q),
+            o_hp.reshape(*lead, n_q, d) if o_hp is not None else None, ws)
+
+
+def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.CORRECT, grad_dtype=None,
+                  fwd_workspace=None):
+    """Fused QAT backward on CUDA tensors -> (dQ, dK, dV) (flash.py:317-390)."""
+    _lib.require_cuda()
+    q3, n_q, d = _heads_view(q)
+    k3, n_k, _ = _heads_view(k)
+    v3, _, _ = _heads_view(v)
+    heads = q3.shape[0]
+    if tuple(d_o.shape) != tuple(q.shape):
+        raise ShapeError(f"dO shape {tuple(d_o.shape)} does not match Q {tuple(q.shape)}")
+    if variant.uses_o_prime and o_hp is None:
+        raise MissingOPrime(f"variant {variant.value} needs O_prime; run the training forward")
+    o_ref = o_hp if variant.uses_o_prime else o
+    if o_ref is None:
+        raise ShapeError("the forward output O is required")
+    if lse.numel() != heads * n_q:
+        raise ShapeError("outs.L has the wrong shape")
+    grad_dtype = grad_dtype or q.dtype
+    lib = _lib.load()
+    ws = torch.empty(lib.aq_attn_bwd_workspace_bytes(heads, n_q, n_k, d), dtype=torch.uint8, device=q.device)
+    dq = torch.empty((heads, n_q, d), dtype=grad_dtype, device=q.device)
+    dk = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
+    dv = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
+    d_o3 = d_o.reshape(heads, n_q, d).contiguous()
+    o_c = o.reshape(heads, n_q, d).contiguous() if o is not None else None
+    o_hp_c = o_hp.reshape(heads, n_q, d).contiguous() if o_hp is not None else None
+    o_dt = (o_hp_c if o_hp_c is not None else o_c).dtype
+    if o_c is not None and o_hp_c is not None and o_c.dtype != o_hp_c.dtype:
+        o_c = o_c.to(o_dt)
+    lse_c = lse.reshape(heads, n_q).to(torch.float32).contiguous()
+    args = _lib.AqBwdArgs(
+        q=q3.contiguous().data_ptr(), k=k3.contiguous().data_ptr(), v=v3.contiguous().data_ptr(),
+        in_dtype=_lib.DT_CODE[q.dtype], d_o=d_o3.data_ptr(), do_dtype=_lib.DT_CODE[d_o3.dtype],
+        o=o_c.data_ptr() if o_c is not None else None,
+        o_hp=o_hp_c.data_ptr() if o_hp_c is not None else None, o_dtype=_lib.DT_CODE[o_dt],
+        lse=lse_c.data_ptr(), heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal),
+        variant=variant.code, dq=dq.data_ptr(), dk=dk.data_ptr(), dv=dv.data_ptr(),
+        g_dtype=_lib.DT_CODE[grad_dtype], workspace=ws.data_ptr(),
+        fwd_workspace=fwd_workspace.data_ptr() if fwd_workspace is not None else None)
+    _lib.check(lib.aq_attn_bwd(args, _lib.stream_ptr()))
+    return (dq.reshape(q.shape[:-2] + (n_q, d)), dk.reshape(k.shape[:-2] + (n_k, d)),
+            dv.reshape(v.shape[:-2] + (n_k, d)))
+
+
+# ----------------------------------------------------------------------------
+# reference-API shims (2-D per-head numpy or torch operands)
+# ----------------------------------------------------------------------------
+
+def _check_attention_shapes(Q, K, V):
+    """oracle.py:96-103."""
+    if Q.ndim < 2 or K.ndim < 2 or V.ndim < 2:
+        raise ShapeError("attention operands must be 2-D (one head at a time)")
+    n_q, d = Q.shape[-2:]
+    n_k, d_k = K.shape[-2:]
+    if d_k != d or tuple(V.shape[-2:]) != (n_k, d):
+        raise ShapeError(f"inconsistent shapes Q{tuple(Q.shape)} K{tuple(K.shape)} V{tuple(V.shape)}")
+    return n_q, n_k, d
+
+
+def _check_cfg(cfg, n_q, n_k, d, quantized):
+    cfg.validate(n_q, n_k, quantized)
+    if cfg.accum_width not in (32, 64):
+        raise ShapeError(f"accum_width must be 32 or 64, got {cfg.accum_width}")
+    if cfg.accum_width != 32:
+        raise InvalidValue("the B200 path accumulates in fp32 (tensor cores); accum_width=64 is CPU-only")
+    if cfg.spec != NVFP4:
+        raise InvalidValue("the B200 path implements NVFP4 only")
+    if d % cfg.spec.block_size:
+        raise ShapeError("d must be a multiple of the block size when quantizing")
+    if not quantized:
+        raise InvalidValue("quantized=False (plain attention) is not implemented on the B200 path yet")
+    if cfg.causal and n_q > n_k:
+        raise ShapeError("causal attention requires N_q <= N_k")
+
+
+def _np_out(t, as_np, dtype=np.float32):
+    return t.float().cpu().numpy().astype(dtype) if as_np else t
+
+
+def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, threads=1):
+    """Training forward: O, L and the auxiliary O' (flash.py:176-246)."""
+    n_q, n_k, d = _check_attention_shapes(Q, K, V)
+    _check_cfg(cfg, n_q, n_k, d, quantized)
+    q, as_np = to_device(Q)
+    k, _ = to_device(K)
+    v, _ = to_device(V)
+    out_dt = torch.float32 if as_np else None
+    o, lse, o_hp, _ = attn_forward(q, k, v, causal=cfg.causal, train=True, out_dtype=out_dt)
+    return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=_np_out(o_hp, as_np))
+
+
+def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
+    """Inference forward on real FP4 codes: O, L (flash.py:249-314)."""
+    n_q, n_k, d = _check_attention_shapes(Q, K, V)
+    _check_cfg(cfg, n_q, n_k, d, True)
+    q, as_np = to_device(Q)
+    k, _ = to_device(K)
+    v, _ = to_device(V)
+    out_dt = torch.float32 if as_np else None
+    o, lse, _, _ = attn_forward(q, k, v, causal=cfg.causal, train=False, out_dtype=out_dt)
+    return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=None)
+
+
+def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized=True, instrument=None):
+    """Recompute-and-requantize QAT backward (flash.py:317-390)."""
+    n_q, n_k, d = _check_attention_shapes(Q, K, V)
+    _check_cfg(cfg, n_q, n_k, d, quantized)
+    if tuple(dO.shape) != tuple(Q.shape):
+        raise ShapeError(f"dO shape {tuple(dO.shape)} does not match Q {tuple(Q.shape)}")
+    if tuple(outs.L.shape) != tuple(Q.shape[:-1]):
+        raise ShapeError("outs.L has the wrong shape")
+    if variant.uses_o_prime and outs.O_prime is None:
+        raise MissingOPrime(f"variant {variant.value} needs O_prime; run the training forward")
+    q, as_np = to_device(Q)
+    k, _ = to_device(K)
+    v, _ = to_device(V)
+    d_o, _ = to_device(dO)
+    o = to_device(outs.O)[0] if outs.O is not None else None
+    o_hp = to_device(outs.O_prime)[0] if outs.O_prime is not None else None
+    lse = to_device(outs.L)[0]
+    g_dt = torch.float32 if as_np else None
+    dq, dk, dv = attn_backward(q, k, v, d_o.to(q.dtype) if d_o.dtype != q.dtype and not as_np else d_o,
+                               o, o_hp, lse, causal=cfg.causal, variant=variant, grad_dtype=g_dt)
+    return AttnGrads(dQ=_np_out(dq, as_np), dK=_np_out(dk, as_np), dV=_np_out(dv, as_np))
