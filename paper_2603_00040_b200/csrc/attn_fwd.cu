@@ -20,6 +20,7 @@
 
 #include "attn.h"
 #include "layouts.cuh"
+#include "pquant.cuh"
 #include "ptx.cuh"
 
 namespace aq {
@@ -269,8 +270,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParam
       l = l * ex2(m - m_new) + acc;
       m = m_new;
     }
-    const float L2 = m + __log2f(l);  // base-2 LSE of the scaled scores
-    if (grow < p.n_q) p.lse[head * p.n_q + grow] = L2 * 0.69314718055994530942f;
+    // natural-log L is what the reference stores (flash.py:217); pass 2 uses
+    // L2 = L * log2(e) recomputed from the stored value so the backward, which
+    // only sees L, rebuilds bit-identical P (and P^F).
+    const float L_nat = (m + __log2f(l)) * 0.69314718055994530942f;
+    if (grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
+    const float L2 = L_nat * 1.44269504088896340736f;
     const float l_scale = l;           // P^ = exp(S - m) = P * l
 
     // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
@@ -293,22 +298,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParam
       uint8_t* psf = smem + L::P_SF;
 #pragma unroll
       for (int blk = 0; blk < TILE / 16; ++blk) {
-        float amax = 0.f;
+        float pv[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) amax = fmaxf(amax, __uint_as_float(s[blk * 16 + e]));
-        uint32_t sc = cvt_e4m3(__fdiv_rn(amax, 6.0f));
-        if (sc == 0 && amax > 0.f) sc = 1;
-        const float sv = e4m3_to_f32(sc);
-        const float rs = sv > 0.f ? __frcp_rn(sv) : 0.f;
-        uint32_t w[2] = {0, 0};
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          const uint32_t byte =
-              cvt_e2m1x2(__uint_as_float(s[blk * 16 + e]) * rs, __uint_as_float(s[blk * 16 + e + 1]) * rs);
-          w[e >> 3] |= byte << (4 * (e & 7));
-        }
-        *reinterpret_cast<uint2*>(pc + t8x32_off(row, blk * 16, TILE)) = make_uint2(w[0], w[1]);
-        psf[sf512_off(row, blk)] = static_cast<uint8_t>(sc);
+        for (int e = 0; e < 16; ++e) pv[e] = __uint_as_float(s[blk * 16 + e]);
+        const PBlock q = quantize_p16(pv);
+        *reinterpret_cast<uint2*>(pc + t8x32_off(row, blk * 16, TILE)) = make_uint2(q.codes[0], q.codes[1]);
+        psf[sf512_off(row, blk)] = static_cast<uint8_t>(q.scale);
       }
       if (TRAIN) {
         uint8_t* ph = smem + L::P_H;

@@ -204,6 +204,12 @@ __device__ __forceinline__ float e2m1_to_f32(uint32_t c) {
   return (c & 8) ? -v : v;
 }
 
+// Vector fp32 reduction into global memory (no return value).
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
