@@ -90,7 +90,10 @@ def test_autograd_matches_functional(causal):
     o2, lse, o_hp, _ = aq.attn_forward(q.detach(), k.detach(), v.detach(), causal=causal, train=True)
     dq, dk, dv = aq.attn_backward(q.detach(), k.detach(), v.detach(), d_o, o2, o_hp, lse, causal=causal)
     assert torch.equal(o, o2)
-    assert torch.equal(q.grad, dq) and torch.equal(k.grad, dk) and torch.equal(v.grad, dv)
+    # dK / dV are reduced in a fixed order; dQ is accumulated with fp32 atomics
+    # across key tiles, so only its rounding order may differ
+    assert torch.equal(k.grad, dk) and torch.equal(v.grad, dv)
+    assert orc.rel_l2(q.grad.float().cpu().numpy(), dq.float().cpu().numpy()) <= 5e-3
 
 
 @pytest.mark.parametrize("n,d,causal", [(1024, 128, True), (640, 64, False)])
