@@ -81,6 +81,8 @@ typedef struct {
   float* lse;        /* [heads][n_q] natural-log LSE L (flash.py:217) */
   void* workspace;   /* aq_attn_fwd_workspace_bytes(); keep it for the backward */
   int keep_for_bwd;  /* also stage the bf16 operands the backward reuses */
+  int operands_staged; /* 1: workspace already holds this Q/K/V's quantized tiles
+                          (e.g. an FP4 KV cache); skip the quantizers */
 } AqFwdArgs;
 
 int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train,
@@ -109,6 +111,13 @@ typedef struct {
 int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d);
 /* Replaces flash_backward (flash.py:317-390). */
 int aq_attn_bwd(const AqBwdArgs* args, void* stream);
+
+/* ---- measurement utilities (bench.py roofline denominators) ---------------
+ * One CTA per SM issuing back-to-back tcgen05 MMAs from shared memory:
+ * kind 0 = NVFP4 block-scaled (mxf4nvf4, M128 N256 K64), 1 = bf16 (f16 kind,
+ * M128 N256 K16). Time the launch with events; FLOPs from aq_probe_mma_flops. */
+int aq_probe_mma_peak(int kind, int ctas, int rounds, void* stream);
+double aq_probe_mma_flops(int kind, int ctas, int rounds);
 
 #ifdef __cplusplus
 }

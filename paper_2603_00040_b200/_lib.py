@@ -29,7 +29,7 @@ class AqFwdArgs(ctypes.Structure):
         ("heads", c_i64), ("n_q", c_i64), ("n_k", c_i64), ("d", c_i64),
         ("causal", c_int), ("train", c_int),
         ("o", c_vp), ("o_dtype", c_int), ("o_hp", c_vp), ("o_hp_dtype", c_int),
-        ("lse", c_vp), ("workspace", c_vp), ("keep_for_bwd", c_int),
+        ("lse", c_vp), ("workspace", c_vp), ("keep_for_bwd", c_int), ("operands_staged", c_int),
     ]
 
 
@@ -59,6 +59,8 @@ PROTOTYPES = {
     "aq_attn_fwd": (c_int, [ctypes.POINTER(AqFwdArgs), c_vp]),
     "aq_attn_bwd_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "aq_attn_bwd": (c_int, [ctypes.POINTER(AqBwdArgs), c_vp]),
+    "aq_probe_mma_peak": (c_int, [c_int, c_int, c_int, c_vp]),
+    "aq_probe_mma_flops": (ctypes.c_double, [c_int, c_int, c_int]),
 }
 
 _lib = None

@@ -14,7 +14,7 @@ using namespace aq;
 
 namespace {
 
-constexpr int kAbiVersion = 1;
+constexpr int kAbiVersion = 2;
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
@@ -204,8 +204,10 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, a->keep_for_bwd);
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
-  int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws, w, st);
-  if (s != AQ_OK) return s;
+  if (!a->operands_staged) {
+    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws, w, st);
+    if (s != AQ_OK) return s;
+  }
   FwdParams p{};
   p.q_codes = ws + w.q_codes;
   p.q_sf = ws + w.q_sf;

@@ -1,0 +1,76 @@
+// Tensor-pipe peak probe: the roofline denominator for the attention kernels.
+//
+// One CTA per SM issues back-to-back tcgen05 MMAs (operands resident in
+// shared memory, accumulator in TMEM, no HBM traffic) for the two MMA kinds
+// the attention path uses: kind::mxf4nvf4 (NVFP4 block-scaled, K=64) and
+// kind::f16 (bf16, K=16), both M=128 N=256 cta_group::1. FLOPs = CTAs x
+// rounds x 2*M*N*K; the caller times the launch with CUDA events. This is a
+// measurement utility for bench.py, not part of the attention path.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/attnqat_b200.h"
+#include "ptx.cuh"
+
+namespace aq {
+namespace probe {
+
+constexpr int M = 128, N = 256;
+
+__global__ void __launch_bounds__(128, 1) mma_peak_kernel(int kind, int rounds) {
+  // A: 128 x 64 fp4 (4 KB) or 128 x 16 bf16 (4 KB); B: 256 rows (8 KB); SF 2 x 512 B
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  for (int i = threadIdx.x; i < (12 * 1024 + 1024) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&slot, 512);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 4096), sf = smem_u32(smem + 12 * 1024);
+    tmem_cp_32x128_x4(tmem + 256, smem_desc(sf, 0, 128));
+    tmem_cp_32x128_x4(tmem + 264, smem_desc(sf + 512, 0, 128));
+    const uint64_t da = smem_desc(a, 2048, 128), db = smem_desc(b, 4096, 128);
+    if (kind == 0) {
+      const uint32_t id = idesc_nvf4(M, N);
+      for (int r = 0; r < rounds; ++r) mma_nvf4_ss(tmem, da, db, id, tmem + 256, tmem + 264, r > 0);
+    } else {
+      const uint32_t id = idesc_f16(M, N, 1, 0, 0);
+      for (int r = 0; r < rounds; ++r) mma_f16_ss(tmem, da, db, id, r > 0);
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace probe
+}  // namespace aq
+
+extern "C" {
+
+/* FLOPs executed by one aq_probe_mma_peak launch. kind 0 = NVFP4 (K=64), 1 = bf16 (K=16). */
+double aq_probe_mma_flops(int kind, int ctas, int rounds) {
+  const double k = kind == 0 ? 64.0 : 16.0;
+  return 2.0 * aq::probe::M * aq::probe::N * k * static_cast<double>(ctas) * rounds;
+}
+
+int aq_probe_mma_peak(int kind, int ctas, int rounds, void* stream) {
+  const int smem = 13 * 1024;
+  aq::probe::mma_peak_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(kind, rounds);
+  return cudaGetLastError() == cudaSuccess ? AQ_OK : AQ_E_CUDA;
+}
+
+}  // extern "C"

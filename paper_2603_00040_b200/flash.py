@@ -96,7 +96,8 @@ def _heads_view(t):
     return t.reshape(-1, n, d), n, d
 
 
-def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd=False, lse_out=None):
+def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd=False, lse_out=None,
+                 workspace=None, operands_staged=False, out=None):
     """Fused forward on CUDA tensors [..., N, d] -> (O, L, O_hp or None, workspace).
 
     ``train=True`` is flash_forward_training (O, L, O'), ``False`` is
@@ -122,8 +123,15 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
     ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, int(train), int(keep_for_bwd))
     if ws_bytes <= 0:
         raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
-    o = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
+    if workspace is not None:
+        if workspace.numel() < ws_bytes:
+            raise ShapeError("workspace too small")
+        ws = workspace
+    else:
+        if operands_staged:
+            raise InvalidValue("operands_staged needs the workspace that holds them")
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    o = out if out is not None else torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
     o_hp = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device) if train else None
     lse = lse_out if lse_out is not None else torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
     args = _lib.AqFwdArgs(
@@ -131,7 +139,8 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
         heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=int(train),
         o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype],
         o_hp=o_hp.data_ptr() if o_hp is not None else None, o_hp_dtype=_lib.DT_CODE[out_dtype],
-        lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=int(keep_for_bwd))
+        lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=int(keep_for_bwd),
+        operands_staged=int(operands_staged))
     _lib.check(lib.aq_attn_fwd(args, _lib.stream_ptr()))
     lead = q.shape[:-2]
     return (o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q),
