@@ -216,10 +216,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_bwd_kernel(const BwdParam
       tc_fence_before();
       mbar_arrive(&bars[B_S_EMPTY]);
       // P = exp(S - L) exactly as the forward computes it
+      p_from_s<TILE / 2>(pr, 0, sl2, L2);
+      if (lim < TILE - 1) {
 #pragma unroll
-      for (int c = 0; c < TILE; ++c) {
-        const float t = (c <= lim) ? pr[c] * sl2 - L2 : -INFINITY;
-        pr[c] = ex2(t);
+        for (int c = 0; c < TILE; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
       if (ii > 0) mbar_wait(&bars[B_DS_EMPTY], (ii - 1) & 1);
       // P^F (or P) -> bf16 [query][key] T8x8

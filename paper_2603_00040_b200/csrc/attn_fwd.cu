@@ -11,11 +11,16 @@
 //                             and 1/l applied in the epilogue)
 // O needs no rescaling: L is final before pass 2.
 //
-// CTA = one (head, 128-query tile). Warps 0-3: softmax / quantize / epilogue,
-// one thread per query row (TMEM lane). Warp 4: bulk-copy producer. Warp 5:
-// single-thread tcgen05 MMA issuer. K/V tiles stream through an NS-stage
-// mbarrier ring; operands arrive pre-laid-out by the quantizers (layouts.cuh).
+// CTA = one (head, 128-query tile). Softmax warps: CS warpgroups; warp w owns
+// TMEM lanes 32*(w%4).. (one query row per thread) and key columns
+// [(w/4)*128/CS, ...) of every S tile, so each row is processed by CS threads
+// in parallel with no exchange inside a tile (pass-1 (m, l) partials are
+// merged once, P^F blocks of 16 keys never straddle a column split).
+// One producer warp issues 1-D bulk copies of pre-tiled operands; one warp
+// issues the tcgen05 MMAs from a single thread. K/V stream through an
+// NS-stage mbarrier ring; S is double-buffered in TMEM.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "attn.h"
@@ -27,15 +32,22 @@ namespace aq {
 
 namespace fwd {
 
-constexpr int NS = 2;            // K/V pipeline stages
-constexpr int NUM_THREADS = 192; // 4 softmax warps + producer + MMA
-
-template <int D, bool TRAIN>
-struct Smem {
+template <int D, bool TRAIN, int CS>
+struct Cfg {
+  static constexpr int NSW = 4 * CS;                 // softmax warps
+  static constexpr int NUM_THREADS = 32 * (NSW + 2);
+  static constexpr int PRODUCER = NSW, MMA = NSW + 1;
+  static constexpr int CW = TILE / CS;               // key columns per softmax thread
+  static constexpr int NS = TRAIN ? 2 : 3;           // K/V stages
+  static constexpr int NB2 = TRAIN ? 1 : 2;          // S buffers in pass 2
+  // TMEM columns
+  static constexpr uint32_t T_S0 = 0, T_S1 = 128;
+  static constexpr uint32_t T_O = TRAIN ? 128 : 256, T_OP = 256;
+  static constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = 392 + 8 * 3, T_VSF = T_PSF + 8;
+  // shared memory
   static constexpr int Q_CODES = 0;
   static constexpr int Q_SF = Q_CODES + TILE * D / 2;
   static constexpr int STAGE0 = Q_SF + (D / 64) * 512;
-  // stage: K codes | K sf | V^T codes | V^T sf | V fp16 (train)
   static constexpr int ST_K = 0;
   static constexpr int ST_KSF = ST_K + TILE * D / 2;
   static constexpr int ST_V = ST_KSF + (D / 64) * 512;
@@ -45,43 +57,29 @@ struct Smem {
   static constexpr int P_CODES = STAGE0 + NS * STAGE_BYTES;
   static constexpr int P_SF = P_CODES + TILE * TILE / 2;
   static constexpr int P_H = P_SF + 1024;
-  static constexpr int BARS = P_H + (TRAIN ? TILE * TILE * 2 : 0);
-  static constexpr int NUM_BARS = 16;
+  static constexpr int ML = P_H + (TRAIN ? TILE * TILE * 2 : 0);   // pass-1 (m, l) partials
+  static constexpr int BARS = ML + 2 * CS * TILE * 4;
+  static constexpr int NUM_BARS = 24;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int USED = TMEM_SLOT + 16;
-  // Force one CTA per SM: the kernel allocates all 512 TMEM columns.
+  // one CTA per SM (the kernel owns all 512 TMEM columns)
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
   static constexpr int K_BYTES = TILE * D / 2 + (D / 64) * 512;
   static constexpr int V_BYTES = TILE * D / 2 + 1024 + (TRAIN ? TILE * D * 2 : 0);
+  // barrier slots
+  static constexpr int B_Q = 0, B_KV_FULL = 1, B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS,
+                       B_S_EMPTY = B_S_FULL + 2, B_P_FULL = B_S_EMPTY + 2, B_P_EMPTY = B_P_FULL + 1,
+                       B_O_FULL = B_P_EMPTY + 1;
+  static_assert(B_O_FULL < NUM_BARS, "barrier slots");
+  static_assert(T_VSF + 8 * NS <= 512, "TMEM columns");
 };
 
-// TMEM columns
-constexpr uint32_t T_S0 = 0, T_S1 = 128, T_O = 128, T_OP = 256;
-constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = 408, T_VSF = 416;
-
-enum Bar { B_Q = 0, B_KV_FULL = 1, B_KV_EMPTY = 1 + NS, B_S_FULL = 1 + 2 * NS, B_S_EMPTY = 3 + 2 * NS,
-           B_P_FULL = 5 + 2 * NS, B_P_EMPTY = 6 + 2 * NS, B_O_FULL = 7 + 2 * NS };
-
-struct TileRange {
-  int j_begin, j_end;  // key tiles [j_begin, j_end)
-};
-
-__device__ __forceinline__ TileRange key_tiles(const FwdParams& p, int q0) {
-  const int last_row = min(q0 + TILE - 1, static_cast<int>(p.n_q) - 1);
-  int j_end = static_cast<int>(ceil_div(p.n_k, TILE));
-  if (p.causal) {
-    const int64_t lim = static_cast<int64_t>(last_row) + (p.n_k - p.n_q);  // flash.py:127-128
-    j_end = min(j_end, static_cast<int>(lim / TILE) + 1);
-  }
-  return {0, j_end};
-}
-
-template <int D, bool TRAIN>
-__global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
-  using L = Smem<D, TRAIN>;
+template <int D, bool TRAIN, int CS>
+__global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
+  using C = Cfg<D, TRAIN, CS>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BARS);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::TMEM_SLOT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::TMEM_SLOT);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -90,22 +88,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParam
   const int q0 = qt * TILE;
   const int q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
   const int k_tiles = static_cast<int>(ceil_div(p.n_k, TILE));
-  const TileRange tr = key_tiles(p, q0);
-  const int nt = tr.j_end - tr.j_begin;
+  // key tiles with any visible key for this query tile (flash.py:127-128, 154)
+  int nt = k_tiles;
+  if (p.causal) {
+    const int64_t last = static_cast<int64_t>(min(q0 + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
+    nt = min(nt, static_cast<int>(last / TILE) + 1);
+  }
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[B_Q], 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&bars[B_KV_FULL + s], 1);
-      mbar_init(&bars[B_KV_EMPTY + s], 1);
+    mbar_init(&bars[C::B_Q], 1);
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(&bars[C::B_KV_FULL + s], 1);
+      mbar_init(&bars[C::B_KV_EMPTY + s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars[B_S_FULL + b], 1);
-      mbar_init(&bars[B_S_EMPTY + b], 128);
+      mbar_init(&bars[C::B_S_FULL + b], 1);
+      mbar_init(&bars[C::B_S_EMPTY + b], 32 * C::NSW);
     }
-    mbar_init(&bars[B_P_FULL], 128);
-    mbar_init(&bars[B_P_EMPTY], 1);
-    mbar_init(&bars[B_O_FULL], 1);
+    mbar_init(&bars[C::B_P_FULL], 32 * C::NSW);
+    mbar_init(&bars[C::B_P_EMPTY], 1);
+    mbar_init(&bars[C::B_O_FULL], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -114,230 +116,248 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParam
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == C::PRODUCER) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const int64_t qtile_idx = head * q_tiles + qt;
-      mbar_expect_tx(&bars[B_Q], TILE * D / 2 + (D / 64) * 512);
-      bulk_g2s(smem + L::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[B_Q]);
-      bulk_g2s(smem + L::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[B_Q]);
+      mbar_expect_tx(&bars[C::B_Q], TILE * D / 2 + (D / 64) * 512);
+      bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q]);
+      bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q]);
       int it = 0;
       for (int pass = 0; pass < 2; ++pass) {
-        for (int j = tr.j_begin; j < tr.j_end; ++j, ++it) {
-          const int st = it % NS;
-          if (it >= NS) mbar_wait(&bars[B_KV_EMPTY + st], ((it / NS) - 1) & 1);
-          uint8_t* sb = smem + L::STAGE0 + st * L::STAGE_BYTES;
+        for (int j = 0; j < nt; ++j, ++it) {
+          const int st = it % C::NS;
+          if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
+          uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
           const int64_t kt_idx = head * k_tiles + j;
-          const uint32_t bytes = L::K_BYTES + (pass ? L::V_BYTES : 0);
-          mbar_expect_tx(&bars[B_KV_FULL + st], bytes);
-          bulk_g2s(sb + L::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[B_KV_FULL + st]);
-          bulk_g2s(sb + L::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[B_KV_FULL + st]);
+          uint64_t* fb = &bars[C::B_KV_FULL + st];
+          mbar_expect_tx(fb, C::K_BYTES + (pass ? C::V_BYTES : 0));
+          bulk_g2s(sb + C::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+          bulk_g2s(sb + C::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
           if (pass) {
-            bulk_g2s(sb + L::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[B_KV_FULL + st]);
-            bulk_g2s(sb + L::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, &bars[B_KV_FULL + st]);
-            if (TRAIN)
-              bulk_g2s(sb + L::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, &bars[B_KV_FULL + st]);
+            bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+            bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
+            if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
           }
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == C::MMA) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t id_s = idesc_nvf4(128, 128);
       const uint32_t id_pv = idesc_nvf4(128, D);
       const uint32_t id_op = idesc_f16(128, D, /*f16*/ 0, /*a_mn*/ 0, /*b_mn*/ 1);
-      const uint32_t q_base = smem_u32(smem + L::Q_CODES);
-      mbar_wait(&bars[B_Q], 0);
+      const uint32_t q_base = smem_u32(smem + C::Q_CODES);
+      mbar_wait(&bars[C::B_Q], 0);
       tc_fence_after();
       for (int ks = 0; ks < D / 64; ++ks)
-        tmem_cp_32x128_x4(tmem + T_QSF + 4 * ks, smem_desc(smem_u32(smem + L::Q_SF + ks * 512), 0, 128));
-      int it = 0;
-      int s_use0 = 0, s_use1 = 0;
-      auto issue_s = [&](int st, uint32_t s_col) {
-        const uint32_t kb = smem_u32(smem + L::STAGE0 + st * L::STAGE_BYTES + L::ST_K);
-        const uint32_t ksf = smem_u32(smem + L::STAGE0 + st * L::STAGE_BYTES + L::ST_KSF);
-        for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + T_KSF + 8 * st + 4 * ks, smem_desc(ksf + ks * 512, 0, 128));
-        for (int ks = 0; ks < D / 64; ++ks) {
-          const uint64_t da = smem_desc(q_base + ks * 2 * 2048, 2048, 128);
-          const uint64_t db = smem_desc(kb + ks * 2 * 2048, 2048, 128);
-          mma_nvf4_ss(tmem + s_col, da, db, id_s, tmem + T_QSF + 4 * ks, tmem + T_KSF + 8 * st + 4 * ks, ks > 0);
-        }
-      };
-      // pass 1: S tiles into alternating buffers
-      for (int jj = 0; jj < nt; ++jj, ++it) {
-        const int st = it % NS;
-        const int b = jj & 1;
-        mbar_wait(&bars[B_KV_FULL + st], (it / NS) & 1);
-        const int use = b ? s_use1 : s_use0;
-        if (use > 0) mbar_wait(&bars[B_S_EMPTY + b], (use - 1) & 1);
+        tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, smem_desc(smem_u32(smem + C::Q_SF + ks * 512), 0, 128));
+      int use0 = 0, use1 = 0;
+      auto issue_s = [&](int it, int b) {
+        const int st = it % C::NS;
+        mbar_wait(&bars[C::B_KV_FULL + st], (it / C::NS) & 1);
+        const int u = b ? use1 : use0;
+        if (u > 0) mbar_wait(&bars[C::B_S_EMPTY + b], (u - 1) & 1);
         tc_fence_after();
-        issue_s(st, b ? T_S1 : T_S0);
-        tc_commit(&bars[B_S_FULL + b]);
-        tc_commit(&bars[B_KV_EMPTY + st]);
-        if (b) ++s_use1; else ++s_use0;
+        const uint32_t kb = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES + C::ST_K);
+        const uint32_t ksf = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES + C::ST_KSF);
+        for (int ks = 0; ks < D / 64; ++ks)
+          tmem_cp_32x128_x4(tmem + C::T_KSF + 8 * st + 4 * ks, smem_desc(ksf + ks * 512, 0, 128));
+        for (int ks = 0; ks < D / 64; ++ks)
+          mma_nvf4_ss(tmem + (b ? C::T_S1 : C::T_S0), smem_desc(q_base + ks * 2 * 2048, 2048, 128),
+                      smem_desc(kb + ks * 2 * 2048, 2048, 128), id_s, tmem + C::T_QSF + 4 * ks,
+                      tmem + C::T_KSF + 8 * st + 4 * ks, ks > 0);
+        tc_commit(&bars[C::B_S_FULL + b]);
+        if (b) ++use1; else ++use0;
+      };
+      // pass 1: S tiles into alternating buffers; K stages released right away
+      int it = 0;
+      for (int jj = 0; jj < nt; ++jj, ++it) {
+        issue_s(it, jj & 1);
+        tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
       }
-      // pass 2: S(jj) is issued ahead of PV(jj-1)
+      // pass 2: S(jj) issued one tile ahead of PV(jj-1)
       const int it2 = it;
       for (int jj = 0; jj <= nt; ++jj) {
-        if (jj < nt) {
-          const int st = (it2 + jj) % NS;
-          mbar_wait(&bars[B_KV_FULL + st], ((it2 + jj) / NS) & 1);
-          if (s_use0 > 0) mbar_wait(&bars[B_S_EMPTY + 0], (s_use0 - 1) & 1);
-          tc_fence_after();
-          issue_s(st, T_S0);
-          tc_commit(&bars[B_S_FULL + 0]);
-          ++s_use0;
-        }
+        if (jj < nt) issue_s(it2 + jj, C::NB2 == 2 ? (jj & 1) : 0);
         if (jj > 0) {
           const int pj = jj - 1;
-          const int st = (it2 + pj) % NS;
-          mbar_wait(&bars[B_P_FULL], pj & 1);
+          const int st = (it2 + pj) % C::NS;
+          mbar_wait(&bars[C::B_P_FULL], pj & 1);
           tc_fence_after();
-          const uint32_t sb = smem_u32(smem + L::STAGE0 + st * L::STAGE_BYTES);
+          const uint32_t sb = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES);
           for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128_x4(tmem + T_PSF + 4 * ks, smem_desc(smem_u32(smem + L::P_SF + ks * 512), 0, 128));
-            tmem_cp_32x128_x4(tmem + T_VSF + 8 * st + 4 * ks, smem_desc(sb + L::ST_VSF + ks * 512, 0, 128));
+            tmem_cp_32x128_x4(tmem + C::T_PSF + 4 * ks, smem_desc(smem_u32(smem + C::P_SF + ks * 512), 0, 128));
+            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, smem_desc(sb + C::ST_VSF + ks * 512, 0, 128));
           }
-          const uint32_t pa = smem_u32(smem + L::P_CODES);
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t da = smem_desc(pa + ks * 2 * 2048, 2048, 128);
-            const uint64_t db = smem_desc(sb + L::ST_V + ks * 2 * (D * 16), D * 16, 128);
-            mma_nvf4_ss(tmem + T_O, da, db, id_pv, tmem + T_PSF + 4 * ks, tmem + T_VSF + 8 * st + 4 * ks,
-                        (pj > 0 || ks > 0));
-          }
+          const uint32_t pa = smem_u32(smem + C::P_CODES);
+          for (int ks = 0; ks < 2; ++ks)
+            mma_nvf4_ss(tmem + C::T_O, smem_desc(pa + ks * 2 * 2048, 2048, 128),
+                        smem_desc(sb + C::ST_V + ks * 2 * (D * 16), D * 16, 128), id_pv, tmem + C::T_PSF + 4 * ks,
+                        tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
           if (TRAIN) {
-            const uint32_t ph = smem_u32(smem + L::P_H);
-            for (int ks = 0; ks < TILE / 16; ++ks) {
-              const uint64_t da = smem_desc(ph + ks * 2 * 2048, 2048, 128);
-              const uint64_t db = smem_desc(sb + L::ST_VH + ks * 2 * 128, 128, 2048);
-              mma_f16_ss(tmem + T_OP, da, db, id_op, (pj > 0 || ks > 0));
-            }
+            const uint32_t ph = smem_u32(smem + C::P_H);
+            for (int ks = 0; ks < TILE / 16; ++ks)
+              mma_f16_ss(tmem + C::T_OP, smem_desc(ph + ks * 2 * 2048, 2048, 128),
+                         smem_desc(sb + C::ST_VH + ks * 2 * 128, 128, 2048), id_op, (pj > 0 || ks > 0));
           }
-          tc_commit(&bars[B_P_EMPTY]);
-          tc_commit(&bars[B_KV_EMPTY + st]);
+          tc_commit(&bars[C::B_P_EMPTY]);
+          tc_commit(&bars[C::B_KV_EMPTY + st]);
         }
       }
-      tc_commit(&bars[B_O_FULL]);
+      tc_commit(&bars[C::B_O_FULL]);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int row = threadIdx.x;  // 0..127 == TMEM lane
+    constexpr int CW = C::CW;
+    const int row = 32 * (warp & 3) + lane;        // TMEM lane == query row in the tile
+    const int half = warp >> 2;                    // which column split
+    const int cbase = half * CW;
     const int64_t grow = q0 + row;
-    const uint32_t t_lane = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;  // log2(e) / sqrt(d)
-    const int64_t offset = p.n_k - p.n_q;
-    // last valid key for this row (inclusive), global index
-    int64_t kmax = p.n_k - 1;
-    if (p.causal) kmax = min(kmax, grow + offset);
-    float m = -INFINITY, l = 0.f;
-    int s_use0 = 0, s_use1 = 0;
-    uint32_t s[TILE];
+    int64_t kmax = p.n_k - 1;        // last visible key of this row (inclusive)
+    if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
+    int use0 = 0, use1 = 0;
+    float x[CW];
 
-#define AQ_LOAD_S(col)                                              \
-  do {                                                              \
-    _Pragma("unroll") for (int c0 = 0; c0 < TILE; c0 += 32) {       \
-      uint32_t r_[32];                                              \
-      tmem_ld32(t_lane + (col) + c0, r_);                           \
-      _Pragma("unroll") for (int e_ = 0; e_ < 32; ++e_) s[c0 + e_] = r_[e_]; \
-    }                                                               \
-    tmem_ld_wait();                                                 \
+#define AQ_ACQUIRE_S(b_)                                                      \
+  do {                                                                        \
+    const int b__ = (b_);                                                     \
+    mbar_wait(&bars[C::B_S_FULL + b__], (b__ ? use1 : use0) & 1);             \
+    tc_fence_after();                                                         \
+    const uint32_t base__ = t_lane + (b__ ? C::T_S1 : C::T_S0) + cbase;       \
+    _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32) {                   \
+      uint32_t r_[32];                                                        \
+      tmem_ld32(base__ + c0, r_);                                             \
+      tmem_ld_wait();                                                         \
+      _Pragma("unroll") for (int e_ = 0; e_ < 32; ++e_) x[c0 + e_] = __uint_as_float(r_[e_]); \
+    }                                                                         \
+    tc_fence_before();                                                        \
+    mbar_arrive(&bars[C::B_S_EMPTY + b__]);                                   \
+    if (b__) ++use1; else ++use0;                                             \
   } while (0)
 
-    // pass 1 -- online softmax statistics (flash.py:145-173), log2 domain
+    // pass 1 -- online softmax statistics over this thread's columns (log2 domain)
+    float m = -INFINITY, l = 0.f;
     for (int jj = 0; jj < nt; ++jj) {
-      const int b = jj & 1;
-      mbar_wait(&bars[B_S_FULL + b], (b ? s_use1 : s_use0) & 1);
-      tc_fence_after();
-      AQ_LOAD_S(b ? T_S1 : T_S0);
-      tc_fence_before();
-      mbar_arrive(&bars[B_S_EMPTY + b]);
-      if (b) ++s_use1; else ++s_use0;
-      const int64_t k0 = static_cast<int64_t>(tr.j_begin + jj) * TILE;
-      const int64_t lim = kmax - k0;  // keys c <= lim are visible
-      float mloc = -INFINITY;
+      AQ_ACQUIRE_S(jj & 1);
+      const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
+      if (lim < CW - 1) {
 #pragma unroll
-      for (int c = 0; c < TILE; ++c) {
-        const float t = (c <= lim) ? __uint_as_float(s[c]) * sl2 : -INFINITY;
-        s[c] = __float_as_uint(t);
-        mloc = fmaxf(mloc, t);
+        for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
       }
-      const float m_new = fmaxf(m, mloc);
-      float acc = 0.f;
+      // row max on the raw scores (the scale is positive)
+      float mx[8];
 #pragma unroll
-      for (int c = 0; c < TILE; ++c) acc += ex2(__uint_as_float(s[c]) - m_new);
-      l = l * ex2(m - m_new) + acc;
+      for (int a = 0; a < 8; ++a) mx[a] = x[a];
+#pragma unroll
+      for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+      const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+      const float m_new = fmaxf(m, mloc);
+      const float base = (m_new == -INFINITY) ? 0.f : m_new;
+      float2 acc[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < CW / 2; ++i) {
+        const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
+                                    make_float2(-base, -base));
+        const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+        acc[i & 3] = __fadd2_rn(acc[i & 3], e);
+      }
+      const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+      const float2 s4 = __fadd2_rn(s01, s23);
+      l = l * ex2(m - base) + (s4.x + s4.y);
       m = m_new;
     }
+    // merge the CS column-split partials of each row
+    float* ml = reinterpret_cast<float*>(smem + C::ML);
+    ml[(half * 2 + 0) * TILE + row] = m;
+    ml[(half * 2 + 1) * TILE + row] = l;
+    named_bar_sync(1, 32 * C::NSW);
+    float mt = -INFINITY;
+#pragma unroll
+    for (int h = 0; h < CS; ++h) mt = fmaxf(mt, ml[(h * 2) * TILE + row]);
+    float lt = 0.f;
+#pragma unroll
+    for (int h = 0; h < CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
     // natural-log L is what the reference stores (flash.py:217); pass 2 uses
     // L2 = L * log2(e) recomputed from the stored value so the backward, which
     // only sees L, rebuilds bit-identical P (and P^F).
-    const float L_nat = (m + __log2f(l)) * 0.69314718055994530942f;
-    if (grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
+    const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
+    if (half == 0 && grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
     const float L2 = L_nat * 1.44269504088896340736f;
-    const float l_scale = l;           // P^ = exp(S - m) = P * l
+    const float l_scale = lt;  // P^ = exp(S - m) = P * l
 
     // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
+    uint8_t* pc = smem + C::P_CODES;
+    uint8_t* psf = smem + C::P_SF;
     for (int jj = 0; jj < nt; ++jj) {
-      mbar_wait(&bars[B_S_FULL + 0], s_use0 & 1);
-      tc_fence_after();
-      AQ_LOAD_S(T_S0);
-      tc_fence_before();
-      mbar_arrive(&bars[B_S_EMPTY + 0]);
-      ++s_use0;
-      const int64_t k0 = static_cast<int64_t>(tr.j_begin + jj) * TILE;
-      const int64_t lim = kmax - k0;
+      AQ_ACQUIRE_S(C::NB2 == 2 ? (jj & 1) : 0);
+      const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+      p_from_s<CW / 2>(x, cbase, sl2, L2);
+      if (lim < CW - 1) {
 #pragma unroll
-      for (int c = 0; c < TILE; ++c) {
-        const float t = (c <= lim) ? __uint_as_float(s[c]) * sl2 - L2 : -INFINITY;
-        s[c] = __float_as_uint(ex2(t));
+        for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
       }
-      if (jj > 0) mbar_wait(&bars[B_P_EMPTY], (jj - 1) & 1);
-      uint8_t* pc = smem + L::P_CODES;
-      uint8_t* psf = smem + L::P_SF;
+      if (jj > 0) mbar_wait(&bars[C::B_P_EMPTY], (jj - 1) & 1);
+      uint32_t scw[(CW + 63) / 64];
 #pragma unroll
-      for (int blk = 0; blk < TILE / 16; ++blk) {
-        float pv[16];
+      for (int w = 0; w < (CW + 63) / 64; ++w) scw[w] = 0;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pv[e] = __uint_as_float(s[blk * 16 + e]);
-        const PBlock q = quantize_p16(pv);
-        *reinterpret_cast<uint2*>(pc + t8x32_off(row, blk * 16, TILE)) = make_uint2(q.codes[0], q.codes[1]);
-        psf[sf512_off(row, blk)] = static_cast<uint8_t>(q.scale);
+      for (int blk = 0; blk < CW / 16; blk += 2) {
+        const PBlock qa = quantize_p16(x + blk * 16);
+        const PBlock qb = quantize_p16(x + blk * 16 + 16);
+        *reinterpret_cast<uint4*>(pc + t8x32_off(row, cbase + blk * 16, TILE)) =
+            make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
+        scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+      }
+      if (CW >= 64) {
+#pragma unroll
+        for (int w = 0; w < CW / 64; ++w)
+          *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * w)) = scw[w];
+      } else {
+        *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
       }
       if (TRAIN) {
-        uint8_t* ph = smem + L::P_H;
+        uint8_t* ph = smem + C::P_H;
 #pragma unroll
-        for (int c8 = 0; c8 < TILE / 8; ++c8) {
+        for (int c8 = 0; c8 < CW / 8; ++c8) {
           uint32_t h[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const __half2 v = __floats2half2_rn(__uint_as_float(s[c8 * 8 + 2 * e]) * l_scale,
-                                                __uint_as_float(s[c8 * 8 + 2 * e + 1]) * l_scale);
+            const float2 ph2 = __fmul2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]),
+                                          make_float2(l_scale, l_scale));
+            const __half2 v = __floats2half2_rn(ph2.x, ph2.y);
             h[e] = *reinterpret_cast<const uint32_t*>(&v);
           }
-          *reinterpret_cast<uint4*>(ph + t8x8_off(row, c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
         }
       }
       fence_async_smem();
-      mbar_arrive(&bars[B_P_FULL]);
+      mbar_arrive(&bars[C::B_P_FULL]);
     }
+#undef AQ_ACQUIRE_S
 
-    // epilogue: O (and O' * 1/l) rows -> global
-    mbar_wait(&bars[B_O_FULL], 0);
+    // epilogue: this thread's D/CS columns of O (and O' * 1/l) -> global
+    mbar_wait(&bars[C::B_O_FULL], 0);
     tc_fence_after();
     const float inv_l = 1.f / l_scale;
+    constexpr int DW = D / CS;
     for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
       void* dst = out ? p.o_hp : p.o;
       const int dt = out ? p.o_hp_dt : p.o_dt;
       const float mul = out ? inv_l : 1.f;
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
+      for (int c = 0; c < DW; c += 32) {
         uint32_t r[32];
-        tmem_ld32(t_lane + (out ? T_OP : T_O) + c, r);
+        tmem_ld32(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, r);
         tmem_ld_wait();
         if (dst != nullptr && grow < p.n_q) {
-          const int64_t base = (head * p.n_q + grow) * D + c;
+          const int64_t base = (head * p.n_q + grow) * D + half * DW + c;
           if (dt == 0) {
             float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
 #pragma unroll
@@ -376,22 +396,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) attn_fwd_kernel(const FwdParam
   }
 }
 
-template <int D, bool TRAIN>
+template <int D, bool TRAIN, int CS>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
-  using L = Smem<D, TRAIN>;
-  auto kern = attn_fwd_kernel<D, TRAIN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+  using C = Cfg<D, TRAIN, CS>;
+  auto kern = attn_fwd_kernel<D, TRAIN, CS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   dim3 grid(static_cast<unsigned>(ceil_div(p.n_q, TILE)), static_cast<unsigned>(p.heads));
-  kern<<<grid, NUM_THREADS, L::TOTAL, st>>>(p);
+  kern<<<grid, C::NUM_THREADS, C::TOTAL, st>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace fwd
 
+// AQ_FWD_CS (environment, read once) selects the column split for tuning runs.
+static int fwd_cs() {
+  static const int cs = [] {
+    const char* e = std::getenv("AQ_FWD_CS");
+    return (e && std::atoi(e) == 4) ? 4 : 2;
+  }();
+  return cs;
+}
+
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st) {
-  if (p.d == 64) return p.train ? fwd::launch<64, true>(p, st) : fwd::launch<64, false>(p, st);
-  if (p.d == 128) return p.train ? fwd::launch<128, true>(p, st) : fwd::launch<128, false>(p, st);
+  if (fwd_cs() == 4) {
+    if (p.d == 64) return p.train ? fwd::launch<64, true, 4>(p, st) : fwd::launch<64, false, 4>(p, st);
+    if (p.d == 128) return p.train ? fwd::launch<128, true, 4>(p, st) : fwd::launch<128, false, 4>(p, st);
+    return cudaErrorInvalidValue;
+  }
+  if (p.d == 64) return p.train ? fwd::launch<64, true, 2>(p, st) : fwd::launch<64, false, 2>(p, st);
+  if (p.d == 128) return p.train ? fwd::launch<128, true, 2>(p, st) : fwd::launch<128, false, 2>(p, st);
   return cudaErrorInvalidValue;
 }
 

@@ -4,12 +4,15 @@
 // test_flash.py:230-244 pins for the reference.
 //   scale = E4M3_RNE(amax / 6), bumped to 2^-9 for tiny non-zero blocks
 //           (codec.py:169-177); codes = E2M1_RNE(p / scale) (codec.py:196-202).
-// P >= 0, so no sign / negative-zero handling is needed. p / scale uses the
-// reciprocal of the (exactly representable) scale: P itself carries ~1e-7
-// relative error from the exp, so this costs no parity.
+// P >= 0, so no sign / negative-zero handling is needed. amax / 6 and
+// p / scale use multiplications by (approximate) reciprocals: P itself
+// carries ~1e-7 relative error from the exp, so a 1-ulp difference only
+// matters for values within an ulp of a rounding midpoint (rare, and the
+// forward and backward still agree exactly because both run this code).
 #pragma once
 #include <cstdint>
 
+#include "fastexp.cuh"
 #include "ptx.cuh"
 
 namespace aq {
@@ -21,19 +24,40 @@ struct PBlock {
 };
 
 __device__ __forceinline__ PBlock quantize_p16(const float* p) {
-  float amax = 0.f;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) amax = fmaxf(amax, p[e]);
-  uint32_t sc = cvt_e4m3(__fdiv_rn(amax, 6.0f));
+  float m0 = fmaxf(p[0], p[1]), m1 = fmaxf(p[2], p[3]), m2 = fmaxf(p[4], p[5]), m3 = fmaxf(p[6], p[7]);
+  float m4 = fmaxf(p[8], p[9]), m5 = fmaxf(p[10], p[11]), m6 = fmaxf(p[12], p[13]), m7 = fmaxf(p[14], p[15]);
+  const float amax = fmaxf(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)), fmaxf(fmaxf(m4, m5), fmaxf(m6, m7)));
+  uint32_t sc = cvt_e4m3(amax * (1.0f / 6.0f));
   if (sc == 0 && amax > 0.f) sc = 1;
   PBlock b;
   b.scale = sc;
   b.sv = e4m3_to_f32(sc);
-  const float rs = b.sv > 0.f ? __frcp_rn(b.sv) : 0.f;
-  b.codes[0] = b.codes[1] = 0;
+  const float rs = b.sv > 0.f ? rcp_approx(b.sv) : 0.f;
+  float q[16];
 #pragma unroll
-  for (int e = 0; e < 16; e += 2) b.codes[e >> 3] |= cvt_e2m1x2(p[e] * rs, p[e + 1] * rs) << (4 * (e & 7));
+  for (int e = 0; e < 16; e += 2) {
+    const float2 v = __fmul2_rn(make_float2(p[e], p[e + 1]), make_float2(rs, rs));
+    q[e] = v.x;
+    q[e + 1] = v.y;
+  }
+  b.codes[0] = cvt_e2m1x8(q);
+  b.codes[1] = cvt_e2m1x8(q + 8);
   return b;
+}
+
+// P = exp(S - L) for 2*NP consecutive in-tile key columns starting at column
+// c0 (c0 % 16 == 0): t = S_raw * log2(e)/sqrt(d) - L2 (one FFMA2 per pair),
+// exp2 split between MUFU and the FMA-pipe polynomial by in-tile pair index.
+// Shared by forward pass 2 and the backward so both rebuild identical P.
+template <int NP>
+__device__ __forceinline__ void p_from_s(float* x, int c0, float sl2, float L2) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2), make_float2(-L2, -L2));
+    const float2 e = use_poly(c0 / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+    x[2 * i] = e.x;
+    x[2 * i + 1] = e.y;
+  }
 }
 
 // decoded value of code e (0..15) of a quantized block
