@@ -207,6 +207,29 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Four packed e2m1 code pairs (one u32 = 8 codes) -> four exact f16x2 values.
+__device__ __forceinline__ void e2m1x8_to_h2(uint32_t codes, __half2 (&h)[4]) {
+  uint32_t r[4];
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t.reg .b32 t1, t2, t3;\n\t"
+      "shr.b32 t1, %4, 8;\n\tshr.b32 t2, %4, 16;\n\tshr.b32 t3, %4, 24;\n\t"
+      "cvt.u8.u32 b0, %4;\n\tcvt.u8.u32 b1, t1;\n\tcvt.u8.u32 b2, t2;\n\tcvt.u8.u32 b3, t3;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %0, b0;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %1, b1;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %2, b2;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %3, b3;\n\t}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+      : "r"(codes));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = *reinterpret_cast<__half2*>(&r[i]);
+}
+// Correctly rounded x / s given r = RN(1/s): one refinement step with FMA
+// (Markstein); exact for every quotient in the normal range.
+__device__ __forceinline__ float div_rn(float x, float s, float r) {
+  const float q0 = x * r;
+  const float rem = fmaf(-q0, s, x);
+  return fmaf(rem, r, q0);
+}
+
 // fp32 -> e4m3 (RN, satfinite) byte.
 __device__ __forceinline__ uint32_t cvt_e4m3(float x) {
   uint16_t r;

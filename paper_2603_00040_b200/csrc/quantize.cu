@@ -61,52 +61,81 @@ __device__ __forceinline__ uint32_t h16_bits(float x, int dt) {
                     : static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(x)));
 }
 
-// Quantize one 16-element block. Returns the scale code; fills packed codes
-// (8 bytes as two u32) and the decoded (exact) fake-quantized values.
+// Quantize one 16-element block: scale code, 16 packed codes, and (when
+// WANT_FQ) the exact dequantized values as f16x2 (exact in fp16 and bf16).
 struct Block16 {
   uint32_t scale;
   uint32_t packed[2];
-  float fq[16];
+  __half2 fq[8];
   bool finite;
 };
 
+template <bool WANT_FQ>
 __device__ __forceinline__ void quantize_block16(const float (&v)[16], Block16& out) {
-  float amax = 0.f;
+  float a[8];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) amax = fmaxf(amax, fabsf(v[j]));
-  // NaN propagates as "not <= max" ; inf fails too
-  bool finite = true;
+  for (int j = 0; j < 8; ++j) a[j] = fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1]));
+  const float amax = fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
+  // fmaxf drops NaN, so test finiteness separately: x * 0 is NaN for NaN / inf
+  float z = 0.f;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) finite &= (fabsf(v[j]) <= 3.402823466e38f);
-  out.finite = finite;
-  const float raw = __fdiv_rn(amax, 6.0f);
+  for (int j = 0; j < 16; ++j) z = fmaf(v[j], 0.f, z);
+  out.finite = (z == 0.f);
+  const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);  // = fl(amax / 6)
   uint32_t sc = cvt_e4m3(raw);
-  if (sc == 0 && amax > 0.f) sc = 1;  // tiny non-zero block keeps 2^-9
+  if (sc == 0 && amax > 0.f) sc = 1;  // tiny non-zero block keeps 2^-9 (codec.py:175-176)
   out.scale = sc;
   const float s = e4m3_to_f32(sc);
-  uint32_t w0 = 0, w1 = 0;
+  const float r = s > 0.f ? __frcp_rn(s) : 0.f;
+  float q[16];
 #pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    float q0 = 0.f, q1 = 0.f;
-    if (s > 0.f) {
-      q0 = (v[j] == 0.f) ? 0.f : __fdiv_rn(v[j], s);
-      q1 = (v[j + 1] == 0.f) ? 0.f : __fdiv_rn(v[j + 1], s);
-    }
-    const uint32_t byte = cvt_e2m1x2(q0, q1);
-    out.fq[j] = e2m1_to_f32(byte & 0xF) * s;
-    out.fq[j + 1] = e2m1_to_f32(byte >> 4) * s;
-    if (j < 8)
-      w0 |= byte << (4 * j);
-    else
-      w1 |= byte << (4 * (j - 8));
+  for (int j = 0; j < 16; ++j) {
+    // x / s correctly rounded; an exact +-0 input (and every element of an
+    // all-zero block) encodes as +0 (codec.py:84, 199-201)
+    q[j] = (v[j] == 0.f || s == 0.f) ? 0.f : div_rn(v[j], s, r);
   }
-  out.packed[0] = w0;
-  out.packed[1] = w1;
+  out.packed[0] = cvt_e2m1x8(q);
+  out.packed[1] = cvt_e2m1x8(q + 8);
+  if (WANT_FQ) {
+    const __half sh = __float2half_rn(s);  // exact: E4M3 values are fp16 values
+    const __half2 s2 = __halves2half2(sh, sh);
+    __half2 c[4];
+    e2m1x8_to_h2(out.packed[0], c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out.fq[i] = __hmul2(c[i], s2);
+    e2m1x8_to_h2(out.packed[1], c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out.fq[4 + i] = __hmul2(c[i], s2);
+  }
+}
+
+__device__ __forceinline__ uint32_t h2_to(const __half2 h, int dt) {
+  // f16 pair -> the same pair in dt (16-bit dtypes only); exact for fq values
+  if (dt == kF16) return *reinterpret_cast<const uint32_t*>(&h);
+  const float2 f = __half22float2(h);
+  const __nv_bfloat162 b = __floats2bfloat162_rn(f.x, f.y);
+  return *reinterpret_cast<const uint32_t*>(&b);
+}
+
+__device__ __forceinline__ void store_fq16(void* p, int64_t i0, int dt, const __half2 (&fq)[8]) {
+  if (dt == kF32) {
+    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + i0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = __half22float2(fq[2 * i]), b = __half22float2(fq[2 * i + 1]);
+      d[i] = make_float4(a.x, a.y, b.x, b.y);
+    }
+  } else {
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p) + i0);
+    d[0] = make_uint4(h2_to(fq[0], dt), h2_to(fq[1], dt), h2_to(fq[2], dt), h2_to(fq[3], dt));
+    d[1] = make_uint4(h2_to(fq[4], dt), h2_to(fq[5], dt), h2_to(fq[6], dt), h2_to(fq[7], dt));
+  }
 }
 
 // ---------------------------------------------------------------------------
 // K1: blocks along the contiguous (column) axis. x is [heads][n][cols] with
-// row stride `ld` elements and head stride `hs` elements. One thread per block.
+// row stride `ld` elements and head stride `hs` elements. One thread per 32
+// columns (two blocks; cols % 32 == 16 leaves a final single block).
 // Optional outputs (nullptr to skip):
 //   codes_ref [heads*n][cols/2], scales_ref [heads*n][cols/16]  (reference layout)
 //   fq        [heads*n][cols] dense dequantized values (dtype fq_dt)
@@ -114,60 +143,55 @@ __device__ __forceinline__ void quantize_block16(const float (&v)[16], Block16& 
 //   sf_t      SF512 images per tile
 //   fqh_t     T8x8 16-bit tiles of the dequantized values (dtype fqh_dt)
 // ---------------------------------------------------------------------------
-
-
+template <bool WANT_FQ>
 __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
   const int64_t nb = a.cols / 16;
+  const int64_t npair = (nb + 1) / 2;
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
-  const int64_t total = a.heads * n_pad * nb;
+  const int64_t total = a.heads * n_pad * npair;
+  const int D = static_cast<int>(a.cols);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t b = t % nb;
-    const int64_t rowp = t / nb;
+    const int64_t bp = t % npair;
+    const int64_t rowp = t / npair;
     const int64_t h = rowp / n_pad;
     const int64_t r = rowp % n_pad;
     const bool real = r < a.n;
-    float v[16];
-    if (real) {
-      load16(a.x, h * a.hs + r * a.ld + b * 16, a.x_dt, v);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = 0.f;
-    }
-    Block16 q;
-    quantize_block16(v, q);
-    if (real) {
-      const int64_t row = h * a.n + r;
-      if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
-      if (a.codes_ref) {
-        uint2* dst = reinterpret_cast<uint2*>(a.codes_ref + row * (a.cols / 2) + b * 8);
-        *dst = make_uint2(q.packed[0], q.packed[1]);
-      }
-      if (a.scales_ref) a.scales_ref[row * nb + b] = static_cast<uint8_t>(q.scale);
-      if (a.fq) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) store_elem(a.fq, row * a.cols + b * 16 + j, a.fq_dt, q.fq[j]);
-      }
-    }
+    const int64_t row = h * a.n + r;
     const int64_t tile = h * (n_pad / TILE) + r / TILE;
     const int rr = static_cast<int>(r % TILE);
-    const int D = static_cast<int>(a.cols);
-    if (a.codes_t) {
-      uint2* dst = reinterpret_cast<uint2*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, b * 16, TILE));
-      *dst = make_uint2(q.packed[0], q.packed[1]);
-    }
-    if (a.sf_t) a.sf_t[tile * sf_tile_bytes_qk(D) + sf512_off(rr, static_cast<int>(b))] = static_cast<uint8_t>(q.scale);
-    if (a.fqh_t) {
-      uint8_t* base = reinterpret_cast<uint8_t*>(a.fqh_t) + tile * h_tile_bytes(D);
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int col0 = static_cast<int>(b) * 16 + half * 8;
-        uint4 w;
-        w.x = h16_bits(q.fq[half * 8 + 0], a.fqh_dt) | (h16_bits(q.fq[half * 8 + 1], a.fqh_dt) << 16);
-        w.y = h16_bits(q.fq[half * 8 + 2], a.fqh_dt) | (h16_bits(q.fq[half * 8 + 3], a.fqh_dt) << 16);
-        w.z = h16_bits(q.fq[half * 8 + 4], a.fqh_dt) | (h16_bits(q.fq[half * 8 + 5], a.fqh_dt) << 16);
-        w.w = h16_bits(q.fq[half * 8 + 6], a.fqh_dt) | (h16_bits(q.fq[half * 8 + 7], a.fqh_dt) << 16);
-        *reinterpret_cast<uint4*>(base + t8x8_off(rr, col0)) = w;
+    for (int half = 0; half < 2; ++half) {
+      const int64_t b = bp * 2 + half;
+      if (b >= nb) break;
+      float v[16];
+      if (real) {
+        load16(a.x, h * a.hs + r * a.ld + b * 16, a.x_dt, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      }
+      Block16 q;
+      quantize_block16<WANT_FQ>(v, q);
+      if (real) {
+        if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
+        if (a.codes_ref)
+          *reinterpret_cast<uint2*>(a.codes_ref + row * (a.cols / 2) + b * 8) = make_uint2(q.packed[0], q.packed[1]);
+        if (a.scales_ref) a.scales_ref[row * nb + b] = static_cast<uint8_t>(q.scale);
+        if (WANT_FQ && a.fq) store_fq16(a.fq, row * a.cols + b * 16, a.fq_dt, q.fq);
+      }
+      if (a.codes_t)
+        *reinterpret_cast<uint2*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, static_cast<int>(b) * 16, TILE)) =
+            make_uint2(q.packed[0], q.packed[1]);
+      if (a.sf_t)
+        a.sf_t[tile * sf_tile_bytes_qk(D) + sf512_off(rr, static_cast<int>(b))] = static_cast<uint8_t>(q.scale);
+      if (WANT_FQ && a.fqh_t) {
+        uint8_t* base = reinterpret_cast<uint8_t*>(a.fqh_t) + tile * h_tile_bytes(D);
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8)
+          *reinterpret_cast<uint4*>(base + t8x8_off(rr, static_cast<int>(b) * 16 + h8 * 8)) =
+              make_uint4(h2_to(q.fq[4 * h8], a.fqh_dt), h2_to(q.fq[4 * h8 + 1], a.fqh_dt),
+                         h2_to(q.fq[4 * h8 + 2], a.fqh_dt), h2_to(q.fq[4 * h8 + 3], a.fqh_dt));
       }
     }
   }
@@ -176,7 +200,9 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 // ---------------------------------------------------------------------------
 // K2: blocks along the token axis (the V operand, quantized as V^T with the
 // token tail zero-padded to a multiple of 16; codec.py:359-381). x is
-// [heads][n][cols]. One thread per (column, 32-token group) = two blocks.
+// [heads][n][cols]. One CTA per (head, 32-token slab): the slab is staged in
+// shared memory with coalesced loads, then thread c quantizes column c's two
+// 16-token blocks and writes 16 contiguous code bytes.
 // Optional outputs:
 //   codes_ref [heads][cols][n16/2], scales_ref [heads][cols][n16/16]  (n16 = ceil16(n))
 //   fq        [heads][n][cols] dense (fake_quantize_cols)
@@ -184,59 +210,101 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 //   sf_t      SF512 images (2 K-steps per tile)
 //   fqh_t     T8x8 16-bit tiles [128 tokens][cols] of the dequantized V
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) quantize_cols_kernel(RowsArgs a) {
+constexpr int kColsSlab = 32;
+constexpr int kColsMax = 256;  // max cols handled by one CTA pass
+
+template <bool WANT_FQ>
+__global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
+  __shared__ float slab[kColsSlab][kColsMax + 1];
   const int64_t n16 = ceil_div(a.n, 16);
   const bool tiled = a.codes_t || a.sf_t || a.fqh_t;
-  const int64_t ngroups = tiled ? ceil_div(a.n, TILE) * (TILE / 32) : ceil_div(a.n, 32);
-  const int64_t total = a.heads * ngroups * a.cols;
+  const int64_t nslabs = tiled ? ceil_div(a.n, TILE) * (TILE / kColsSlab) : ceil_div(a.n, kColsSlab);
   const int D = static_cast<int>(a.cols);
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = t % a.cols;
-    const int64_t g = (t / a.cols) % ngroups;
-    const int64_t h = t / (a.cols * ngroups);
-    const int64_t tok0 = g * 32;
+  for (int64_t sidx = blockIdx.x; sidx < a.heads * nslabs; sidx += gridDim.x) {
+    const int64_t h = sidx / nslabs;
+    const int64_t tok0 = (sidx % nslabs) * kColsSlab;
+    for (int c0 = 0; c0 < D; c0 += kColsMax) {
+      const int cw = min(kColsMax, D - c0);
+      __syncthreads();
+      const bool vec = a.x_dt == kBF16 && (cw % 8) == 0 && (a.ld % 8) == 0 && (a.hs % 8) == 0 && (c0 % 8) == 0 &&
+                       (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+      if (vec) {
+        // 16-byte loads: 8 bf16 per thread per step, coalesced along the row
+        const int cv = cw / 8;
+        for (int i = threadIdx.x; i < kColsSlab * cv; i += blockDim.x) {
+          const int tt = i / cv, c = (i % cv) * 8;
+          const int64_t tok = tok0 + tt;
+          uint4 w = make_uint4(0, 0, 0, 0);
+          if (tok < a.n)
+            w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.x) + h * a.hs + tok * a.ld +
+                                                c0 + c);
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int64_t b0 = tok0 + half * 16;  // first token of this block
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int64_t tok = b0 + j;
-        v[j] = tok < a.n ? load_elem(a.x, h * a.hs + tok * a.ld + c, a.x_dt) : 0.f;
+          for (int j = 0; j < 4; ++j) {
+            slab[tt][c + 2 * j] = __uint_as_float(ww[j] << 16);
+            slab[tt][c + 2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
+          }
+        }
+      } else {
+        for (int i = threadIdx.x; i < kColsSlab * cw; i += blockDim.x) {
+          const int tt = i / cw, c = i % cw;
+          const int64_t tok = tok0 + tt;
+          slab[tt][c] = tok < a.n ? load_elem(a.x, h * a.hs + tok * a.ld + c0 + c, a.x_dt) : 0.f;
+        }
       }
-      Block16 q;
-      quantize_block16(v, q);
-      const int64_t blk = b0 / 16;
-      if (blk < n16) {
-        if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
-        if (a.codes_ref) {
-          uint2* dst = reinterpret_cast<uint2*>(a.codes_ref + (h * a.cols + c) * (n16 * 8) + blk * 8);
-          *dst = make_uint2(q.packed[0], q.packed[1]);
-        }
-        if (a.scales_ref) a.scales_ref[(h * a.cols + c) * n16 + blk] = static_cast<uint8_t>(q.scale);
-        if (a.fq) {
+      __syncthreads();
+      for (int c = threadIdx.x; c < cw; c += blockDim.x) {
+        const int64_t col = c0 + c;
+        uint32_t codes[4];
+        uint32_t scales = 0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + c, a.fq_dt, q.fq[j]);
-        }
-      }
-      if (tiled) {
-        const int64_t n_tiles = ceil_div(a.n, TILE);
-        const int64_t tile = h * n_tiles + b0 / TILE;
-        const int kt = static_cast<int>(b0 % TILE);  // token index inside the tile
-        if (a.codes_t) {
-          uint2* dst =
-              reinterpret_cast<uint2*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(static_cast<int>(c), kt, D));
-          *dst = make_uint2(q.packed[0], q.packed[1]);
-        }
-        if (a.sf_t) a.sf_t[tile * kSfTileBytesV + sf512_off(static_cast<int>(c), kt / 16)] = static_cast<uint8_t>(q.scale);
-        if (a.fqh_t) {
-          uint8_t* base = reinterpret_cast<uint8_t*>(a.fqh_t) + tile * h_tile_bytes(D);
+        for (int half = 0; half < 2; ++half) {
+          float v[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            *reinterpret_cast<uint16_t*>(base + t8x8_off(kt + j, static_cast<int>(c))) =
-                static_cast<uint16_t>(h16_bits(q.fq[j], a.fqh_dt));
+          for (int j = 0; j < 16; ++j) v[j] = slab[half * 16 + j][c];
+          Block16 q;
+          quantize_block16<WANT_FQ>(v, q);
+          codes[2 * half] = q.packed[0];
+          codes[2 * half + 1] = q.packed[1];
+          scales |= q.scale << (8 * half);
+          const int64_t b0 = tok0 + half * 16;
+          const int64_t blk = b0 / 16;
+          if (blk < n16) {
+            if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
+            if (a.codes_ref)
+              *reinterpret_cast<uint2*>(a.codes_ref + (h * a.cols + col) * (n16 * 8) + blk * 8) =
+                  make_uint2(q.packed[0], q.packed[1]);
+            if (a.scales_ref) a.scales_ref[(h * a.cols + col) * n16 + blk] = static_cast<uint8_t>(q.scale);
+            if (WANT_FQ && a.fq) {
+              const __half* fh = reinterpret_cast<const __half*>(q.fq);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + col, a.fq_dt, __half2float(fh[j]));
+            }
+          }
+          if (WANT_FQ && a.fqh_t) {
+            const int64_t tile = h * ceil_div(a.n, TILE) + b0 / TILE;
+            const int kt = static_cast<int>(b0 % TILE);
+            uint8_t* base = reinterpret_cast<uint8_t*>(a.fqh_t) + tile * h_tile_bytes(D);
+            const __half* fh = reinterpret_cast<const __half*>(q.fq);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const __half hv = fh[j];
+              const uint16_t bits = a.fqh_dt == kF16 ? __half_as_ushort(hv)
+                                                     : __bfloat16_as_ushort(__float2bfloat16_rn(__half2float(hv)));
+              *reinterpret_cast<uint16_t*>(base + t8x8_off(kt + j, static_cast<int>(col))) = bits;
+            }
+          }
+        }
+        if (tiled) {
+          const int64_t tile = h * ceil_div(a.n, TILE) + tok0 / TILE;
+          const int kt = static_cast<int>(tok0 % TILE);
+          if (a.codes_t)
+            *reinterpret_cast<uint4*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(static_cast<int>(col), kt, D)) =
+                make_uint4(codes[0], codes[1], codes[2], codes[3]);
+          if (a.sf_t)
+            *reinterpret_cast<uint16_t*>(a.sf_t + tile * kSfTileBytesV + sf512_off(static_cast<int>(col), kt / 16)) =
+                static_cast<uint16_t>(scales);
         }
       }
     }
@@ -271,14 +339,23 @@ static int grid_for(int64_t work) {
 
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
-  quantize_rows_kernel<<<grid_for(a.heads * n_pad * (a.cols / 16)), 256, 0, st>>>(a);
+  const int g = grid_for(a.heads * n_pad * ((a.cols / 16 + 1) / 2));
+  if (a.fq || a.fqh_t)
+    quantize_rows_kernel<true><<<g, 256, 0, st>>>(a);
+  else
+    quantize_rows_kernel<false><<<g, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
   const bool tiled = a.codes_t || a.sf_t || a.fqh_t;
-  const int64_t ngroups = tiled ? ceil_div(a.n, TILE) * (TILE / 32) : ceil_div(a.n, 32);
-  quantize_cols_kernel<<<grid_for(a.heads * ngroups * a.cols), 256, 0, st>>>(a);
+  const int64_t nslabs = tiled ? ceil_div(a.n, TILE) * (TILE / kColsSlab) : ceil_div(a.n, kColsSlab);
+  int64_t g = a.heads * nslabs;
+  if (g > 148 * 64) g = 148 * 64;
+  if (a.fq || a.fqh_t)
+    quantize_cols_kernel<true><<<static_cast<int>(g), 128, 0, st>>>(a);
+  else
+    quantize_cols_kernel<false><<<static_cast<int>(g), 128, 0, st>>>(a);
   return cudaGetLastError();
 }
 
