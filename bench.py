@@ -264,6 +264,8 @@ def main():
         qg, kg, vg = (t.clone().requires_grad_() for t in (q, k, v))
 
         def step():
+            for t_ in (qg, kg, vg):
+                t_.grad = None
             out = aq.attn_qat(qg, kg, vg, causal=causal)
             out.backward(d_o)
         launches_per_step = 4 + 3      # fwd (3 quantizers + attention) + bwd pre, bwd, dq convert

@@ -64,7 +64,7 @@ BwdWs bwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
   w.fwd = take(f.total);  // re-quantized operands when no forward workspace is given
   w.do_h = take(heads * qt * h_tile_bytes(static_cast<int>(d)));
   w.delta = take(heads * qt * TILE * 4);
-  w.dq_acc = take(heads * n_q * d * 4);
+  w.dq_acc = take(heads * qt * TILE * d * 4);  // [heads][n_pad][d] fp32
   w.total = off;
   return w;
 }
@@ -106,17 +106,10 @@ int stage_operands(const void* q, const void* k, const void* v, int in_dt, int64
   a.sf_t = ws + w.v_sf;
   a.fqh_t = w.v_h16 >= 0 ? ws + w.v_h16 : nullptr;
   a.fqh_dt = 2;
+  a.fqh2_t = w.v_hb >= 0 ? ws + w.v_hb : nullptr;
+  a.fqh2_dt = 1;
   e = launch_quantize_cols(a, st);
   if (e != cudaSuccess) return AQ_E_CUDA;
-  if (w.v_hb >= 0) {
-    RowsArgs b = a;
-    b.codes_t = nullptr;
-    b.sf_t = nullptr;
-    b.fqh_t = ws + w.v_hb;
-    b.fqh_dt = 1;
-    e = launch_quantize_cols(b, st);
-    if (e != cudaSuccess) return AQ_E_CUDA;
-  }
   return AQ_OK;
 }
 
@@ -296,7 +289,7 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
   p.inv_sqrt_d = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a->d)));
   e = launch_attn_bwd(p, st);
   if (e != cudaSuccess) return AQ_E_CUDA;
-  return cuda_status(launch_dq_convert(dq_acc, a->dq, a->g_dtype, a->heads * a->n_q * a->d, st));
+  return cuda_status(launch_dq_convert(dq_acc, a->dq, a->g_dtype, a->heads, a->n_q, static_cast<int>(a->d), st));
 }
 
 }  // extern "C"

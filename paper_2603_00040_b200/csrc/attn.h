@@ -17,6 +17,8 @@ struct RowsArgs {
   uint8_t* sf_t;
   void* fqh_t;
   int fqh_dt;
+  void* fqh2_t;   // optional second T8x8 copy in another 16-bit dtype (K2 only)
+  int fqh2_dt;
   int* nonfinite;
 };
 
@@ -51,7 +53,7 @@ struct BwdParams {
   const uint8_t* do_h;   // bf16 T8x8 dO tiles
   const float* lse;      // [heads][n_q]
   const float* delta;    // [heads][nq_pad] D = rowsum(dO . O_ref)
-  float* dq_acc;         // [heads][n_q][d] fp32, zero-initialised
+  float* dq_acc;         // [heads][n_pad][d] fp32 (n_pad = 128-multiple), zero-initialised
   void* dk;
   void* dv;
   int g_dt;
@@ -71,6 +73,7 @@ cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
                            int d, float* delta, uint8_t* do_h, float* dq_acc, cudaStream_t st);
-cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int g_dt, int64_t count, cudaStream_t st);
+cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int g_dt, int64_t heads, int64_t n_q, int d,
+                              cudaStream_t st);
 
 }  // namespace aq

@@ -77,22 +77,29 @@ __device__ __forceinline__ void quantize_block16(const float (&v)[16], Block16& 
   for (int j = 0; j < 8; ++j) a[j] = fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1]));
   const float amax = fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
   // fmaxf drops NaN, so test finiteness separately: x * 0 is NaN for NaN / inf
-  float z = 0.f;
+  float2 z = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) z = fmaf(v[j], 0.f, z);
-  out.finite = (z == 0.f);
+  for (int j = 0; j < 16; j += 2) z = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(0.f, 0.f), z);
+  out.finite = (z.x + z.y == 0.f);
   const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);  // = fl(amax / 6)
   uint32_t sc = cvt_e4m3(raw);
   if (sc == 0 && amax > 0.f) sc = 1;  // tiny non-zero block keeps 2^-9 (codec.py:175-176)
   out.scale = sc;
   const float s = e4m3_to_f32(sc);
   const float r = s > 0.f ? __frcp_rn(s) : 0.f;
+  // x / s correctly rounded (Markstein step, packed fp32x2); adding +0 maps
+  // an exact -0.0 input (and every element of an all-zero block, r = 0) to
+  // +0, which encodes as nibble 0x0 (codec.py:84, 199-201)
+  const float2 r2 = make_float2(r, r), s2n = make_float2(-s, -s), zero2 = make_float2(0.f, 0.f);
   float q[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    // x / s correctly rounded; an exact +-0 input (and every element of an
-    // all-zero block) encodes as +0 (codec.py:84, 199-201)
-    q[j] = (v[j] == 0.f || s == 0.f) ? 0.f : div_rn(v[j], s, r);
+  for (int j = 0; j < 16; j += 2) {
+    const float2 x = make_float2(v[j], v[j + 1]);
+    const float2 q0 = __fmul2_rn(x, r2);
+    const float2 rem = __ffma2_rn(q0, s2n, x);
+    const float2 qq = __fadd2_rn(__ffma2_rn(rem, r2, q0), zero2);
+    q[j] = qq.x;
+    q[j + 1] = qq.y;
   }
   out.packed[0] = cvt_e2m1x8(q);
   out.packed[1] = cvt_e2m1x8(q + 8);
@@ -210,14 +217,14 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 //   sf_t      SF512 images (2 K-steps per tile)
 //   fqh_t     T8x8 16-bit tiles [128 tokens][cols] of the dequantized V
 // ---------------------------------------------------------------------------
-constexpr int kColsSlab = 32;
-constexpr int kColsMax = 256;  // max cols handled by one CTA pass
+constexpr int kColsSlab = 64;   // tokens per CTA step (4 blocks of 16)
+constexpr int kColsMax = 128;   // columns staged per pass
 
 template <bool WANT_FQ>
 __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
   __shared__ float slab[kColsSlab][kColsMax + 1];
   const int64_t n16 = ceil_div(a.n, 16);
-  const bool tiled = a.codes_t || a.sf_t || a.fqh_t;
+  const bool tiled = a.codes_t || a.sf_t || a.fqh_t || a.fqh2_t;
   const int64_t nslabs = tiled ? ceil_div(a.n, TILE) * (TILE / kColsSlab) : ceil_div(a.n, kColsSlab);
   const int D = static_cast<int>(a.cols);
   for (int64_t sidx = blockIdx.x; sidx < a.heads * nslabs; sidx += gridDim.x) {
@@ -226,19 +233,26 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
     for (int c0 = 0; c0 < D; c0 += kColsMax) {
       const int cw = min(kColsMax, D - c0);
       __syncthreads();
-      const bool vec = a.x_dt == kBF16 && (cw % 8) == 0 && (a.ld % 8) == 0 && (a.hs % 8) == 0 && (c0 % 8) == 0 &&
+      const bool vec = a.x_dt == kBF16 && cw == kColsMax && (a.ld % 8) == 0 && (a.hs % 8) == 0 &&
                        (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
       if (vec) {
-        // 16-byte loads: 8 bf16 per thread per step, coalesced along the row
-        const int cv = cw / 8;
-        for (int i = threadIdx.x; i < kColsSlab * cv; i += blockDim.x) {
-          const int tt = i / cv, c = (i % cv) * 8;
+        // all 16-byte loads of the slab in flight at once (8 per thread), then unpack
+        constexpr int CV = kColsMax / 8, PER = kColsSlab * CV / 128;
+        uint4 w[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = threadIdx.x + k * 128;
+          const int tt = i / CV, c = (i % CV) * 8;
           const int64_t tok = tok0 + tt;
-          uint4 w = make_uint4(0, 0, 0, 0);
-          if (tok < a.n)
-            w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.x) + h * a.hs + tok * a.ld +
-                                                c0 + c);
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+          w[k] = tok < a.n ? *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.x) + h * a.hs +
+                                                             tok * a.ld + c0 + c)
+                           : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = threadIdx.x + k * 128;
+          const int tt = i / CV, c = (i % CV) * 8;
+          const uint32_t ww[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             slab[tt][c + 2 * j] = __uint_as_float(ww[j] << 16);
@@ -255,56 +269,83 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
       __syncthreads();
       for (int c = threadIdx.x; c < cw; c += blockDim.x) {
         const int64_t col = c0 + c;
-        uint32_t codes[4];
-        uint32_t scales = 0;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float v[16];
+        for (int g32 = 0; g32 < kColsSlab / 32; ++g32) {
+          uint32_t codes[4];
+          uint32_t scales = 0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = slab[half * 16 + j][c];
-          Block16 q;
-          quantize_block16<WANT_FQ>(v, q);
-          codes[2 * half] = q.packed[0];
-          codes[2 * half + 1] = q.packed[1];
-          scales |= q.scale << (8 * half);
-          const int64_t b0 = tok0 + half * 16;
-          const int64_t blk = b0 / 16;
-          if (blk < n16) {
-            if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
-            if (a.codes_ref)
-              *reinterpret_cast<uint2*>(a.codes_ref + (h * a.cols + col) * (n16 * 8) + blk * 8) =
-                  make_uint2(q.packed[0], q.packed[1]);
-            if (a.scales_ref) a.scales_ref[(h * a.cols + col) * n16 + blk] = static_cast<uint8_t>(q.scale);
-            if (WANT_FQ && a.fq) {
+          for (int hb = 0; hb < 2; ++hb) {
+            const int tb = g32 * 32 + hb * 16;  // first slab row of this block
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = slab[tb + j][c];
+            Block16 q;
+            quantize_block16<WANT_FQ>(v, q);
+            codes[2 * hb] = q.packed[0];
+            codes[2 * hb + 1] = q.packed[1];
+            scales |= q.scale << (8 * hb);
+            const int64_t b0 = tok0 + tb;
+            const int64_t blk = b0 / 16;
+            if (blk < n16) {
+              if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
+              if (a.codes_ref)
+                *reinterpret_cast<uint2*>(a.codes_ref + (h * a.cols + col) * (n16 * 8) + blk * 8) =
+                    make_uint2(q.packed[0], q.packed[1]);
+              if (a.scales_ref) a.scales_ref[(h * a.cols + col) * n16 + blk] = static_cast<uint8_t>(q.scale);
+              if (WANT_FQ && a.fq) {
+                const __half* fh = reinterpret_cast<const __half*>(q.fq);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + col, a.fq_dt, __half2float(fh[j]));
+              }
+            }
+            if (WANT_FQ && (a.fqh_t || a.fqh2_t)) {
+              // overwrite this column of the slab with its dequantized values; the
+              // T8x8 tile is written cooperatively below with 16-byte stores
               const __half* fh = reinterpret_cast<const __half*>(q.fq);
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + col, a.fq_dt, __half2float(fh[j]));
+              for (int j = 0; j < 16; ++j) slab[tb + j][c] = __half2float(fh[j]);
             }
           }
-          if (WANT_FQ && a.fqh_t) {
-            const int64_t tile = h * ceil_div(a.n, TILE) + b0 / TILE;
-            const int kt = static_cast<int>(b0 % TILE);
-            uint8_t* base = reinterpret_cast<uint8_t*>(a.fqh_t) + tile * h_tile_bytes(D);
-            const __half* fh = reinterpret_cast<const __half*>(q.fq);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const __half hv = fh[j];
-              const uint16_t bits = a.fqh_dt == kF16 ? __half_as_ushort(hv)
-                                                     : __bfloat16_as_ushort(__float2bfloat16_rn(__half2float(hv)));
-              *reinterpret_cast<uint16_t*>(base + t8x8_off(kt + j, static_cast<int>(col))) = bits;
-            }
+          if (tiled) {
+            const int64_t tstart = tok0 + g32 * 32;
+            const int64_t tile = h * ceil_div(a.n, TILE) + tstart / TILE;
+            const int kt = static_cast<int>(tstart % TILE);
+            if (a.codes_t)
+              *reinterpret_cast<uint4*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(static_cast<int>(col), kt, D)) =
+                  make_uint4(codes[0], codes[1], codes[2], codes[3]);
+            if (a.sf_t)
+              *reinterpret_cast<uint16_t*>(a.sf_t + tile * kSfTileBytesV + sf512_off(static_cast<int>(col), kt / 16)) =
+                  static_cast<uint16_t>(scales);
           }
         }
-        if (tiled) {
-          const int64_t tile = h * ceil_div(a.n, TILE) + tok0 / TILE;
-          const int kt = static_cast<int>(tok0 % TILE);
-          if (a.codes_t)
-            *reinterpret_cast<uint4*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(static_cast<int>(col), kt, D)) =
-                make_uint4(codes[0], codes[1], codes[2], codes[3]);
-          if (a.sf_t)
-            *reinterpret_cast<uint16_t*>(a.sf_t + tile * kSfTileBytesV + sf512_off(static_cast<int>(col), kt / 16)) =
-                static_cast<uint16_t>(scales);
+      }
+      if (WANT_FQ && (a.fqh_t || a.fqh2_t)) {
+        __syncthreads();
+        const int64_t tile = h * ceil_div(a.n, TILE) + tok0 / TILE;
+        const int kt = static_cast<int>(tok0 % TILE);
+        const int cv = cw / 8;
+        for (int copy = 0; copy < 2; ++copy) {
+          void* dstp = copy ? a.fqh2_t : a.fqh_t;
+          const int dt = copy ? a.fqh2_dt : a.fqh_dt;
+          if (dstp == nullptr) continue;
+          uint8_t* base = reinterpret_cast<uint8_t*>(dstp) + tile * h_tile_bytes(D);
+          for (int i = threadIdx.x; i < kColsSlab * cv; i += blockDim.x) {
+            const int tt = i % kColsSlab, c8 = (i / kColsSlab) * 8;
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float x0 = slab[tt][c8 + 2 * e], x1 = slab[tt][c8 + 2 * e + 1];
+              if (dt == kF16) {
+                const __half2 hv = __floats2half2_rn(x0, x1);
+                w[e] = *reinterpret_cast<const uint32_t*>(&hv);
+              } else {
+                const __nv_bfloat162 bv = __floats2bfloat162_rn(x0, x1);
+                w[e] = *reinterpret_cast<const uint32_t*>(&bv);
+              }
+            }
+            *reinterpret_cast<uint4*>(base + t8x8_off(kt + tt, c0 + c8)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
         }
       }
     }
@@ -348,11 +389,11 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
-  const bool tiled = a.codes_t || a.sf_t || a.fqh_t;
+  const bool tiled = a.codes_t || a.sf_t || a.fqh_t || a.fqh2_t;
   const int64_t nslabs = tiled ? ceil_div(a.n, TILE) * (TILE / kColsSlab) : ceil_div(a.n, kColsSlab);
   int64_t g = a.heads * nslabs;
   if (g > 148 * 64) g = 148 * 64;
-  if (a.fq || a.fqh_t)
+  if (a.fq || a.fqh_t || a.fqh2_t)
     quantize_cols_kernel<true><<<static_cast<int>(g), 128, 0, st>>>(a);
   else
     quantize_cols_kernel<false><<<static_cast<int>(g), 128, 0, st>>>(a);
