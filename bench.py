@@ -43,6 +43,9 @@ CONFIGS = {
     "c2": (4, 32, 8192, 128, True, "fwd"),
     "c3": (1, 40, 32760, 128, False, "fwd"),
     "c4": (8, 32, 4096, 128, True, "train"),
+    # C4 as a full data-parallel QAT layer step: projections + attention fwd/bwd +
+    # NCCL gradient all-reduce + AdamW; global batch 8 sharded over ranks
+    "c4-layer": (8, 32, 4096, 128, True, "layer"),
 }
 
 
@@ -244,6 +247,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B, H, N, d, causal, mode = cfg
+    if mode == "layer":
+        run_layer_mode(args, cfg, rank, world, local)
+        return
     dev = torch.device("cuda", local)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     q, k, v = (torch.randn(B, H, N, d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(3))
@@ -399,6 +405,94 @@ def main():
             "tokens_per_s": tokens_s,
             "roofline": roof, "mma_peaks_tflops": peaks, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_layer_mode(args, cfg, rank, world, local):
+    """Data-parallel QAT layer step (projections + NVFP4 attention fwd/bwd + NCCL
+    gradient all-reduce + AdamW) with the global batch sharded over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_00040_b200 import train as T
+
+    B, H, N, d, causal, _ = cfg
+    if B % world:
+        raise SystemExit(f"global batch {B} not divisible by {world} ranks")
+    b = B // world
+    D = H * d
+    dev = torch.device("cuda", local)
+    layer = T.AttnLayer(D, H, d, seed=0, device=dev)
+    opt = torch.optim.AdamW(layer.parameters(), lr=1e-4)
+    ar = T.GradAllReduce(list(layer.parameters()), world)
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    x = torch.randn(b, N, D, generator=gen, device=dev).bfloat16()
+    tgt = torch.randn(b, N, D, generator=gen, device=dev).bfloat16()
+    st = torch.cuda.current_stream()
+
+    def step(xb):
+        opt.zero_grad(set_to_none=True)
+        y = layer(xb, causal)
+        loss = torch.mean((y.float() - tgt.float()) ** 2)
+        loss.backward()
+        ar.wait()
+        opt.step()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(x)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(st)
+        for _ in range(args.steps):
+            step(x)
+        e1.record(st)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    attn = alg_flops(b, H, N, d, causal, "train")
+    proj = 24.0 * b * N * D * D        # 4 projection GEMMs, fwd + 2x bwd
+    value = world * (attn + proj) / (ms_max * 1e-3) / 1e12
+    # end to end: host batch in (pinned), loss out, every step
+    hx = x.cpu().pin_memory()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    a0.record(st)
+    for _ in range(args.steps):
+        loss = step(hx.to(dev, non_blocking=True))
+        loss.item()
+    a1.record(st)
+    barrier()
+    et = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "nvfp4 attention / bf16 projections / fp32 accum",
+            "data": "synthetic N(0,1), generated on device",
+            "config": {"workload": args.config, "B": B, "H": H, "N": N, "d": d, "causal": causal,
+                       "mode": "QAT layer step (proj + attn fwd/bwd + NCCL grad all-reduce + AdamW)",
+                       "global_batch": B, "parallelism": f"dp{world} batch-sharded"},
+            "tokens_per_s": B * N / (ms_max * 1e-3),
+            "flops_breakdown_per_rank": {"attention_alg": attn, "projections": proj},
+            "e2e": {"value": world * (attn + proj) / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": hx.numel() * 2, "d2h_bytes_per_step": 4,
+                    "ms_per_step": float(et.item())},
+            "clocks": clk.summary(), "gpu_launches": 7 * args.steps,
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
