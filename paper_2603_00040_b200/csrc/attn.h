@@ -40,6 +40,7 @@ struct FwdParams {
   int causal;
   int train;
   float scale_log2;
+  int debug;  // timing experiments only (0 in production): 1 skip P quant, 2 skip exp, 4 skip pass-1 math
 };
 
 struct BwdParams {

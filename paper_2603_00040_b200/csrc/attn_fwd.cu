@@ -38,12 +38,13 @@ struct Cfg {
   static constexpr int NUM_THREADS = 32 * (NSW + 2);
   static constexpr int PRODUCER = NSW, MMA = NSW + 1;
   static constexpr int CW = TILE / CS;               // key columns per softmax thread
-  static constexpr int NS = TRAIN ? 2 : 3;           // K/V stages
+  static constexpr int NS = TRAIN ? 2 : 5;           // K/V stages
+  static constexpr int NB1 = 3;                      // S buffers in pass 1 (reuses O / O' columns)
   static constexpr int NB2 = TRAIN ? 1 : 2;          // S buffers in pass 2
-  // TMEM columns
-  static constexpr uint32_t T_S0 = 0, T_S1 = 128;
+  static constexpr int NP = 2;                       // P^F (and P^) buffers
+  // TMEM columns: S buffer b at 128*b
   static constexpr uint32_t T_O = TRAIN ? 128 : 256, T_OP = 256;
-  static constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = 392 + 8 * 3, T_VSF = T_PSF + 8;
+  static constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = T_KSF + 8 * NS, T_VSF = T_PSF + 8 * NP;
   // shared memory
   static constexpr int Q_CODES = 0;
   static constexpr int Q_SF = Q_CODES + TILE * D / 2;
@@ -54,10 +55,11 @@ struct Cfg {
   static constexpr int ST_VSF = ST_V + TILE * D / 2;
   static constexpr int ST_VH = ST_VSF + 1024;
   static constexpr int STAGE_BYTES = ST_VH + (TRAIN ? TILE * D * 2 : 0);
-  static constexpr int P_CODES = STAGE0 + NS * STAGE_BYTES;
-  static constexpr int P_SF = P_CODES + TILE * TILE / 2;
-  static constexpr int P_H = P_SF + 1024;
-  static constexpr int ML = P_H + (TRAIN ? TILE * TILE * 2 : 0);   // pass-1 (m, l) partials
+  static constexpr int P0 = STAGE0 + NS * STAGE_BYTES;
+  static constexpr int PB_CODES = 0, PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024;
+  static constexpr int P_BYTES = PB_H + (TRAIN ? TILE * TILE * 2 : 0);
+  static constexpr int P_H = P0 + NP * P_BYTES;  // end of the P buffers
+  static constexpr int ML = P_H;   // pass-1 (m, l) partials
   static constexpr int BARS = ML + 2 * CS * TILE * 4;
   static constexpr int NUM_BARS = 24;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
@@ -68,10 +70,13 @@ struct Cfg {
   static constexpr int V_BYTES = TILE * D / 2 + 1024 + (TRAIN ? TILE * D * 2 : 0);
   // barrier slots
   static constexpr int B_Q = 0, B_KV_FULL = 1, B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS,
-                       B_S_EMPTY = B_S_FULL + 2, B_P_FULL = B_S_EMPTY + 2, B_P_EMPTY = B_P_FULL + 1,
-                       B_O_FULL = B_P_EMPTY + 1;
+                       B_S_EMPTY = B_S_FULL + NB1, B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP,
+                       B_O_FULL = B_P_EMPTY + NP;
+  static_assert(USED <= 227 * 1024, "shared memory");
   static_assert(B_O_FULL < NUM_BARS, "barrier slots");
   static_assert(T_VSF + 8 * NS <= 512, "TMEM columns");
+  // number of pass-1 uses of S buffer b (pass 2 continues its phase count)
+  __device__ static int pass1_uses(int nt, int b) { return nt > b ? (nt - b + NB1 - 1) / NB1 : 0; }
 };
 
 template <int D, bool TRAIN, int CS>
@@ -101,12 +106,14 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       mbar_init(&bars[C::B_KV_FULL + s], 1);
       mbar_init(&bars[C::B_KV_EMPTY + s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::NB1; ++b) {
       mbar_init(&bars[C::B_S_FULL + b], 1);
       mbar_init(&bars[C::B_S_EMPTY + b], 32 * C::NSW);
     }
-    mbar_init(&bars[C::B_P_FULL], 32 * C::NSW);
-    mbar_init(&bars[C::B_P_EMPTY], 1);
+    for (int b = 0; b < C::NP; ++b) {
+      mbar_init(&bars[C::B_P_FULL + b], 32 * C::NSW);
+      mbar_init(&bars[C::B_P_EMPTY + b], 1);
+    }
     mbar_init(&bars[C::B_O_FULL], 1);
     fence_mbar_init();
   }
@@ -118,96 +125,126 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
 
   if (warp == C::PRODUCER) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const int64_t qtile_idx = head * q_tiles + qt;
+    // (whole warp runs the loop so indices stay warp-uniform; one lane copies)
+    const int64_t qtile_idx = head * q_tiles + qt;
+    if (elect_one()) {
       mbar_expect_tx(&bars[C::B_Q], TILE * D / 2 + (D / 64) * 512);
       bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q]);
       bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q]);
-      int it = 0;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < nt; ++j, ++it) {
-          const int st = it % C::NS;
-          if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
-          uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
-          const int64_t kt_idx = head * k_tiles + j;
-          uint64_t* fb = &bars[C::B_KV_FULL + st];
-          mbar_expect_tx(fb, C::K_BYTES + (pass ? C::V_BYTES : 0));
-          bulk_g2s(sb + C::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-          bulk_g2s(sb + C::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
-          if (pass) {
-            bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-            bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
-            if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
+    }
+    int it = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = 0; j < nt; ++j, ++it) {
+        const int st = it % C::NS;
+        if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
+        uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
+        const int64_t kt_idx = head * k_tiles + j;
+        uint64_t* fb = &bars[C::B_KV_FULL + st];
+        if (elect_one()) {
+          if ((p.debug & 8) && it >= C::NS) {  // timing experiment: no K/V traffic
+            mbar_arrive(fb);
+          } else {
+            mbar_expect_tx(fb, C::K_BYTES + (pass ? C::V_BYTES : 0));
+            bulk_g2s(sb + C::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+            bulk_g2s(sb + C::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
+            if (pass) {
+              bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+              bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
+              if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
+            }
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == C::MMA) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc_nvf4(128, 128);
-      const uint32_t id_pv = idesc_nvf4(128, D);
-      const uint32_t id_op = idesc_f16(128, D, /*f16*/ 0, /*a_mn*/ 0, /*b_mn*/ 1);
-      const uint32_t q_base = smem_u32(smem + C::Q_CODES);
-      mbar_wait(&bars[C::B_Q], 0);
-      tc_fence_after();
+    // The whole warp runs the schedule (waits, descriptor arithmetic in uniform
+    // registers); one elected lane issues tcgen05.cp / mma / commit.
+    constexpr uint32_t id_s = idesc_nvf4(128, 128);
+    constexpr uint32_t id_pv = idesc_nvf4(128, D);
+    constexpr uint32_t id_op = idesc_f16(128, D, /*f16*/ 0, /*a_mn*/ 0, /*b_mn*/ 1);
+    constexpr uint64_t t_k = desc_template(2048, 128);       // Q / K / P^F codes (K-major T8x32, 128 rows)
+    constexpr uint64_t t_v = desc_template(D * 16, 128);     // V^T codes (K-major T8x32, D rows)
+    constexpr uint64_t t_sf = desc_template(0, 128);         // SF512 images for tcgen05.cp
+    constexpr uint64_t t_ph = desc_template(2048, 128);      // P^ fp16 (K-major T8x8)
+    constexpr uint64_t t_vh = desc_template(128, 2048);      // V^F fp16 (MN-major T8x8)
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t q_base = s0 + C::Q_CODES;
+    mbar_wait(&bars[C::B_Q], 0);
+    tc_fence_after();
+    if (elect_one()) {
       for (int ks = 0; ks < D / 64; ++ks)
-        tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, smem_desc(smem_u32(smem + C::Q_SF + ks * 512), 0, 128));
-      int use0 = 0, use1 = 0;
-      auto issue_s = [&](int it, int b) {
-        const int st = it % C::NS;
-        mbar_wait(&bars[C::B_KV_FULL + st], (it / C::NS) & 1);
-        const int u = b ? use1 : use0;
-        if (u > 0) mbar_wait(&bars[C::B_S_EMPTY + b], (u - 1) & 1);
-        tc_fence_after();
-        const uint32_t kb = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES + C::ST_K);
-        const uint32_t ksf = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES + C::ST_KSF);
+        tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, desc_at(t_sf, s0 + C::Q_SF + ks * 512));
+    }
+    __syncwarp();
+    // S(it) into buffer b, its u-th use
+    auto issue_s = [&](int it, int b, int u) {
+      const int st = it % C::NS;
+      mbar_wait(&bars[C::B_KV_FULL + st], (it / C::NS) & 1);
+      if (u > 0) mbar_wait(&bars[C::B_S_EMPTY + b], (u - 1) & 1);
+      tc_fence_after();
+      const uint32_t kb = s0 + C::STAGE0 + st * C::STAGE_BYTES + C::ST_K;
+      const uint32_t ksf = s0 + C::STAGE0 + st * C::STAGE_BYTES + C::ST_KSF;
+      if (elect_one()) {
+#pragma unroll
         for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + C::T_KSF + 8 * st + 4 * ks, smem_desc(ksf + ks * 512, 0, 128));
+          tmem_cp_32x128_x4(tmem + C::T_KSF + 8 * st + 4 * ks, desc_at(t_sf, ksf + ks * 512));
+#pragma unroll
         for (int ks = 0; ks < D / 64; ++ks)
-          mma_nvf4_ss(tmem + (b ? C::T_S1 : C::T_S0), smem_desc(q_base + ks * 2 * 2048, 2048, 128),
-                      smem_desc(kb + ks * 2 * 2048, 2048, 128), id_s, tmem + C::T_QSF + 4 * ks,
-                      tmem + C::T_KSF + 8 * st + 4 * ks, ks > 0);
+          mma_nvf4_ss(tmem + 128 * b, desc_at(t_k, q_base + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
+                      tmem + C::T_QSF + 4 * ks, tmem + C::T_KSF + 8 * st + 4 * ks, ks > 0);
         tc_commit(&bars[C::B_S_FULL + b]);
-        if (b) ++use1; else ++use0;
-      };
-      // pass 1: S tiles into alternating buffers; K stages released right away
-      int it = 0;
-      for (int jj = 0; jj < nt; ++jj, ++it) {
-        issue_s(it, jj & 1);
-        tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
       }
-      // pass 2: S(jj) issued one tile ahead of PV(jj-1)
-      const int it2 = it;
-      for (int jj = 0; jj <= nt; ++jj) {
-        if (jj < nt) issue_s(it2 + jj, C::NB2 == 2 ? (jj & 1) : 0);
-        if (jj > 0) {
-          const int pj = jj - 1;
-          const int st = (it2 + pj) % C::NS;
-          mbar_wait(&bars[C::B_P_FULL], pj & 1);
-          tc_fence_after();
-          const uint32_t sb = smem_u32(smem + C::STAGE0 + st * C::STAGE_BYTES);
+      __syncwarp();
+    };
+    // pass 1: S tiles round-robin over NB1 buffers; K stages released right away
+    int it = 0;
+    for (int jj = 0; jj < nt; ++jj, ++it) {
+      issue_s(it, jj % C::NB1, jj / C::NB1);
+      if (elect_one()) tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
+      __syncwarp();
+    }
+    // pass 2: S(jj) issued ahead of PV(jj-1); P double-buffered
+    const int it2 = it;
+    for (int jj = 0; jj <= nt; ++jj) {
+      if (jj < nt) {
+        const int b = jj % C::NB2;
+        issue_s(it2 + jj, b, C::pass1_uses(nt, b) + jj / C::NB2);
+      }
+      if (jj > 0) {
+        const int pj = jj - 1;
+        const int pb = pj & 1;
+        const int st = (it2 + pj) % C::NS;
+        mbar_wait(&bars[C::B_P_FULL + pb], (pj >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
+        const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
+        if (elect_one()) {
+#pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128_x4(tmem + C::T_PSF + 4 * ks, smem_desc(smem_u32(smem + C::P_SF + ks * 512), 0, 128));
-            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, smem_desc(sb + C::ST_VSF + ks * 512, 0, 128));
+            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
+            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
           }
-          const uint32_t pa = smem_u32(smem + C::P_CODES);
+#pragma unroll
           for (int ks = 0; ks < 2; ++ks)
-            mma_nvf4_ss(tmem + C::T_O, smem_desc(pa + ks * 2 * 2048, 2048, 128),
-                        smem_desc(sb + C::ST_V + ks * 2 * (D * 16), D * 16, 128), id_pv, tmem + C::T_PSF + 4 * ks,
+            mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
+                        desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
                         tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
           if (TRAIN) {
-            const uint32_t ph = smem_u32(smem + C::P_H);
+#pragma unroll
             for (int ks = 0; ks < TILE / 16; ++ks)
-              mma_f16_ss(tmem + C::T_OP, smem_desc(ph + ks * 2 * 2048, 2048, 128),
-                         smem_desc(sb + C::ST_VH + ks * 2 * 128, 128, 2048), id_op, (pj > 0 || ks > 0));
+              mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
+                         desc_at(t_vh, sb + C::ST_VH + ks * 256), id_op, (pj > 0 || ks > 0));
           }
-          tc_commit(&bars[C::B_P_EMPTY]);
+          tc_commit(&bars[C::B_P_EMPTY + pb]);
           tc_commit(&bars[C::B_KV_EMPTY + st]);
         }
+        __syncwarp();
       }
-      tc_commit(&bars[C::B_O_FULL]);
     }
+    if (elect_one()) tc_commit(&bars[C::B_O_FULL]);
+    __syncwarp();
   } else {
     // ------------------------------------------------------------ softmax warps
     constexpr int CW = C::CW;
@@ -219,35 +256,52 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     const float sl2 = p.scale_log2;  // log2(e) / sqrt(d)
     int64_t kmax = p.n_k - 1;        // last visible key of this row (inclusive)
     if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
-    int use0 = 0, use1 = 0;
     float x[CW];
 
-#define AQ_ACQUIRE_S(b_)                                                      \
+#define AQ_ACQUIRE_S(b_, u_)                                                  \
   do {                                                                        \
     const int b__ = (b_);                                                     \
-    mbar_wait(&bars[C::B_S_FULL + b__], (b__ ? use1 : use0) & 1);             \
+    mbar_wait(&bars[C::B_S_FULL + b__], (u_) & 1);                            \
     tc_fence_after();                                                         \
-    const uint32_t base__ = t_lane + (b__ ? C::T_S1 : C::T_S0) + cbase;       \
-    _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32) {                   \
-      uint32_t r_[32];                                                        \
-      tmem_ld32(base__ + c0, r_);                                             \
-      tmem_ld_wait();                                                         \
-      _Pragma("unroll") for (int e_ = 0; e_ < 32; ++e_) x[c0 + e_] = __uint_as_float(r_[e_]); \
-    }                                                                         \
+    const uint32_t base__ = t_lane + 128 * b__ + cbase;                       \
+    uint32_t r_[CW];                                                          \
+    _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32)                     \
+      tmem_ld32(base__ + c0, *reinterpret_cast<uint32_t(*)[32]>(r_ + c0));    \
+    tmem_ld_wait();                                                           \
+    _Pragma("unroll") for (int e_ = 0; e_ < CW; ++e_) x[e_] = __uint_as_float(r_[e_]); \
     tc_fence_before();                                                        \
     mbar_arrive(&bars[C::B_S_EMPTY + b__]);                                   \
-    if (b__) ++use1; else ++use0;                                             \
   } while (0)
 
-    // pass 1 -- online softmax statistics over this thread's columns (log2 domain)
+    // pass 1 -- online softmax statistics over this thread's columns (log2
+    // domain). The exponentials use a reference max m that is only raised when
+    // a tile's max exceeds it by more than 2^8 (terms stay <= 256), so they do
+    // not wait for the tile's max reduction; a raise recomputes the tile.
     float m = -INFINITY, l = 0.f;
     for (int jj = 0; jj < nt; ++jj) {
-      AQ_ACQUIRE_S(jj & 1);
+      AQ_ACQUIRE_S(jj % C::NB1, jj / C::NB1);
       const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
       if (lim < CW - 1) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
       }
+      auto expsum = [&](float base) {
+        float2 acc[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) {
+          const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
+                                      make_float2(-base, -base));
+          const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+          acc[i & 3] = __fadd2_rn(acc[i & 3], e);
+        }
+        const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+        const float2 s4 = __fadd2_rn(s01, s23);
+        return s4.x + s4.y;
+      };
+      if (p.debug & 4) { l = 1.f; m = 0.f; continue; }
+      float sum = expsum(m == -INFINITY ? 0.f : m);
       // row max on the raw scores (the scale is positive)
       float mx[8];
 #pragma unroll
@@ -256,22 +310,13 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
       const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
-      const float m_new = fmaxf(m, mloc);
-      const float base = (m_new == -INFINITY) ? 0.f : m_new;
-      float2 acc[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < CW / 2; ++i) {
-        const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
-                                    make_float2(-base, -base));
-        const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
-        acc[i & 3] = __fadd2_rn(acc[i & 3], e);
+      if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
+        const float m_new = mloc;
+        l = (m == -INFINITY) ? 0.f : l * ex2(m - m_new);
+        m = m_new;
+        sum = expsum(m);
       }
-      const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
-      const float2 s4 = __fadd2_rn(s01, s23);
-      l = l * ex2(m - base) + (s4.x + s4.y);
-      m = m_new;
+      l += sum;
     }
     // merge the CS column-split partials of each row
     float* ml = reinterpret_cast<float*>(smem + C::ML);
@@ -293,22 +338,31 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     const float l_scale = lt;  // P^ = exp(S - m) = P * l
 
     // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
-    uint8_t* pc = smem + C::P_CODES;
-    uint8_t* psf = smem + C::P_SF;
     for (int jj = 0; jj < nt; ++jj) {
-      AQ_ACQUIRE_S(C::NB2 == 2 ? (jj & 1) : 0);
+      {
+        const int b = jj % C::NB2;
+        AQ_ACQUIRE_S(b, C::pass1_uses(nt, b) + jj / C::NB2);
+      }
       const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
-      p_from_s<CW / 2>(x, cbase, sl2, L2);
+      if (!(p.debug & 2)) p_from_s<CW / 2>(x, cbase, sl2, L2);
       if (lim < CW - 1) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
       }
-      if (jj > 0) mbar_wait(&bars[C::B_P_EMPTY], (jj - 1) & 1);
+      const int pb = jj & 1;
+      if (jj >= 2) mbar_wait(&bars[C::B_P_EMPTY + pb], ((jj >> 1) - 1) & 1);
+      uint8_t* pc = smem + C::P0 + pb * C::P_BYTES + C::PB_CODES;
+      uint8_t* psf = smem + C::P0 + pb * C::P_BYTES + C::PB_SF;
       uint32_t scw[(CW + 63) / 64];
 #pragma unroll
       for (int w = 0; w < (CW + 63) / 64; ++w) scw[w] = 0;
 #pragma unroll
       for (int blk = 0; blk < CW / 16; blk += 2) {
+        if (p.debug & 1) {
+          *reinterpret_cast<uint4*>(pc + t8x32_off(row, cbase + blk * 16, TILE)) =
+              make_uint4(__float_as_uint(x[blk * 16]), 0, 0, 0);
+          continue;
+        }
         const PBlock qa = quantize_p16(x + blk * 16);
         const PBlock qb = quantize_p16(x + blk * 16 + 16);
         *reinterpret_cast<uint4*>(pc + t8x32_off(row, cbase + blk * 16, TILE)) =
@@ -323,7 +377,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
       }
       if (TRAIN) {
-        uint8_t* ph = smem + C::P_H;
+        uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
 #pragma unroll
         for (int c8 = 0; c8 < CW / 8; ++c8) {
           uint32_t h[4];
@@ -338,7 +392,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         }
       }
       fence_async_smem();
-      mbar_arrive(&bars[C::B_P_FULL]);
+      mbar_arrive(&bars[C::B_P_FULL + pb]);
     }
 #undef AQ_ACQUIRE_S
 
@@ -410,6 +464,14 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 }  // namespace fwd
 
 // AQ_FWD_CS (environment, read once) selects the column split for tuning runs.
+static int fwd_debug() {
+  static const int d = [] {
+    const char* e = std::getenv("AQ_FWD_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return d;
+}
+
 static int fwd_cs() {
   static const int cs = [] {
     const char* e = std::getenv("AQ_FWD_CS");
@@ -418,7 +480,9 @@ static int fwd_cs() {
   return cs;
 }
 
-cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st) {
+cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
+  FwdParams p = p_in;
+  p.debug = fwd_debug();
   if (fwd_cs() == 4) {
     if (p.d == 64) return p.train ? fwd::launch<64, true, 4>(p, st) : fwd::launch<64, false, 4>(p, st);
     if (p.d == 128) return p.train ? fwd::launch<128, true, 4>(p, st) : fwd::launch<128, false, 4>(p, st);

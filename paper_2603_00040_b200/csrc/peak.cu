@@ -41,12 +41,30 @@ __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int kind, int rounds) 
     if (kind == 0) {
       const uint32_t id = idesc_nvf4(M, N);
       for (int r = 0; r < rounds; ++r) mma_nvf4_ss(tmem, da, db, id, tmem + 256, tmem + 264, r > 0);
-    } else {
+    } else if (kind == 1) {
       const uint32_t id = idesc_f16(M, N, 1, 0, 0);
       for (int r = 0; r < rounds; ++r) mma_f16_ss(tmem, da, db, id, r > 0);
+    } else if (kind == 2) {  // NVFP4 M128 N128
+      const uint32_t id = idesc_nvf4(M, 128);
+      for (int r = 0; r < rounds; ++r) mma_nvf4_ss(tmem, da, db, id, tmem + 256, tmem + 264, r > 0);
+    } else if (kind == 3) {  // NVFP4 M128 N128 with a tcgen05.cp of scale factors before each MMA
+      const uint32_t id = idesc_nvf4(M, 128);
+      for (int r = 0; r < rounds; ++r) {
+        tmem_cp_32x128_x4(tmem + 264, smem_desc(sf + 512, 0, 128));
+        mma_nvf4_ss(tmem, da, db, id, tmem + 256, tmem + 264, r > 0);
+      }
+    } else if (kind == 4) {  // round trip: MMA (N128) -> commit -> mbarrier wait, serialized
+      const uint32_t id = idesc_nvf4(M, 128);
+      for (int r = 0; r < rounds; ++r) {
+        mma_nvf4_ss(tmem, da, db, id, tmem + 256, tmem + 264, r > 0);
+        tc_commit(&bar);
+        mbar_wait(&bar, r & 1);
+      }
     }
-    tc_commit(&bar);
-    mbar_wait(&bar, 0);
+    if (kind != 4) {
+      tc_commit(&bar);
+      mbar_wait(&bar, 0);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -63,8 +81,9 @@ extern "C" {
 
 /* FLOPs executed by one aq_probe_mma_peak launch. kind 0 = NVFP4 (K=64), 1 = bf16 (K=16). */
 double aq_probe_mma_flops(int kind, int ctas, int rounds) {
-  const double k = kind == 0 ? 64.0 : 16.0;
-  return 2.0 * aq::probe::M * aq::probe::N * k * static_cast<double>(ctas) * rounds;
+  const double k = (kind == 1) ? 16.0 : 64.0;
+  const double n = (kind >= 2) ? 128.0 : aq::probe::N;
+  return 2.0 * aq::probe::M * n * k * static_cast<double>(ctas) * rounds;
 }
 
 int aq_probe_mma_peak(int kind, int ctas, int rounds, void* stream) {

@@ -142,6 +142,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// One lane of a fully active warp (the lowest); the other lanes get false.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor, no swizzle ("interleaved" 8-row x 16-byte
 // core matrices). lbo/sbo in bytes: lbo = stride between core matrices along
@@ -156,6 +165,14 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   d |= static_cast<uint64_t>(1) << 46;
   return d;
 }
+
+// Descriptor with a zero start address: add (smem_byte_address >> 4) to it.
+// Addresses stay below 2^18 bytes so the 14-bit field never carries.
+__host__ __device__ constexpr uint64_t desc_template(uint32_t lbo, uint32_t sbo) {
+  return (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) | (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) |
+         (static_cast<uint64_t>(1) << 46);
+}
+__device__ __forceinline__ uint64_t desc_at(uint64_t tmpl, uint32_t saddr) { return tmpl + (saddr >> 4); }
 
 // Instruction descriptor, kind::f16 (fp32 accumulate). fmt: 0 = f16, 1 = bf16.
 // a_mn / b_mn: 1 = MN-major operand.
