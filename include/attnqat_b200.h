@@ -118,6 +118,9 @@ int aq_attn_bwd(const AqBwdArgs* args, void* stream);
  * M128 N256 K16). Time the launch with events; FLOPs from aq_probe_mma_flops. */
 int aq_probe_mma_peak(int kind, int ctas, int rounds, void* stream);
 double aq_probe_mma_flops(int kind, int ctas, int rounds);
+/* Cycle counters of the forward softmax warps (filled when the environment
+ * sets AQ_FWD_DEBUG bit 32; tuning aid). out: 16 counters. */
+int aq_debug_fwd_profile(unsigned long long* out, int reset);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ import torch
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libattnqat_b200.so")
+LIB_PATH = os.environ.get("AQ_LIB_PATH") or os.path.join(_HERE, "libattnqat_b200.so")  # override: tuning builds
 
 DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
@@ -61,6 +61,7 @@ PROTOTYPES = {
     "aq_attn_bwd": (c_int, [ctypes.POINTER(AqBwdArgs), c_vp]),
     "aq_probe_mma_peak": (c_int, [c_int, c_int, c_int, c_vp]),
     "aq_probe_mma_flops": (ctypes.c_double, [c_int, c_int, c_int]),
+    "aq_debug_fwd_profile": (c_int, [ctypes.POINTER(ctypes.c_ulonglong), c_int]),
 }
 
 _lib = None

@@ -32,6 +32,10 @@ namespace aq {
 
 namespace fwd {
 
+// Timing-experiment counters (AQ_FWD_DEBUG bit 32): cycle sums per softmax
+// segment, accumulated from lane 0 of every softmax warp.
+__device__ unsigned long long g_prof[16];
+
 template <int D, bool TRAIN, int CS>
 struct Cfg {
   static constexpr int NSW = 4 * CS;                 // softmax warps
@@ -205,43 +209,45 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       if (elect_one()) tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
       __syncwarp();
     }
-    // pass 2: S(jj) issued ahead of PV(jj-1); P double-buffered
+    // pass 2: S tiles run up to NB2 ahead of the PV MMAs (S(ns) reuses the
+    // buffer of S(ns - NB2), which the softmax warps release as soon as they
+    // have loaded it); P double-buffered
     const int it2 = it;
-    for (int jj = 0; jj <= nt; ++jj) {
-      if (jj < nt) {
-        const int b = jj % C::NB2;
-        issue_s(it2 + jj, b, C::pass1_uses(nt, b) + jj / C::NB2);
+    for (int ns = 0, np = 0; np < nt;) {
+      if (ns < nt && ns <= np + C::NB2) {
+        const int b = ns % C::NB2;
+        issue_s(it2 + ns, b, C::pass1_uses(nt, b) + ns / C::NB2);
+        ++ns;
+        continue;
       }
-      if (jj > 0) {
-        const int pj = jj - 1;
-        const int pb = pj & 1;
-        const int st = (it2 + pj) % C::NS;
-        mbar_wait(&bars[C::B_P_FULL + pb], (pj >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
-        const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
-        if (elect_one()) {
+      const int pj = np++;
+      const int pb = pj & 1;
+      const int st = (it2 + pj) % C::NS;
+      mbar_wait(&bars[C::B_P_FULL + pb], (pj >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
+      const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
+      if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
-            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
-          }
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
-                        desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
-                        tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
-          if (TRAIN) {
-#pragma unroll
-            for (int ks = 0; ks < TILE / 16; ++ks)
-              mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
-                         desc_at(t_vh, sb + C::ST_VH + ks * 256), id_op, (pj > 0 || ks > 0));
-          }
-          tc_commit(&bars[C::B_P_EMPTY + pb]);
-          tc_commit(&bars[C::B_KV_EMPTY + st]);
+        for (int ks = 0; ks < 2; ++ks) {
+          tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
+          tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
         }
-        __syncwarp();
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
+                      desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
+                      tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
+        if (TRAIN) {
+#pragma unroll
+          for (int ks = 0; ks < TILE / 16; ++ks)
+            mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
+                       desc_at(t_vh, sb + C::ST_VH + ks * 256), id_op, (pj > 0 || ks > 0));
+        }
+        tc_commit(&bars[C::B_P_EMPTY + pb]);
+        tc_commit(&bars[C::B_KV_EMPTY + st]);
       }
+      __syncwarp();
     }
     if (elect_one()) tc_commit(&bars[C::B_O_FULL]);
     __syncwarp();
@@ -257,20 +263,24 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     int64_t kmax = p.n_k - 1;        // last visible key of this row (inclusive)
     if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
     float x[CW];
+    long long prof_wait = 0, prof_ld = 0, prof_p1 = 0, prof_p2m = 0, prof_pw = 0, prof_q = 0, prof_f = 0;
+    const long long prof_start = clock64();
 
 #define AQ_ACQUIRE_S(b_, u_)                                                  \
   do {                                                                        \
     const int b__ = (b_);                                                     \
+    const long long t0__ = clock64();                                         \
     mbar_wait(&bars[C::B_S_FULL + b__], (u_) & 1);                            \
     tc_fence_after();                                                         \
+    const long long t1__ = clock64();                                         \
     const uint32_t base__ = t_lane + 128 * b__ + cbase;                       \
-    uint32_t r_[CW];                                                          \
-    _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32)                     \
-      tmem_ld32(base__ + c0, *reinterpret_cast<uint32_t(*)[32]>(r_ + c0));    \
+    _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(base__ + c0, x + c0); \
     tmem_ld_wait();                                                           \
-    _Pragma("unroll") for (int e_ = 0; e_ < CW; ++e_) x[e_] = __uint_as_float(r_[e_]); \
     tc_fence_before();                                                        \
     mbar_arrive(&bars[C::B_S_EMPTY + b__]);                                   \
+    const long long t2__ = clock64();                                         \
+    prof_wait += t1__ - t0__;                                                 \
+    prof_ld += t2__ - t1__;                                                   \
   } while (0)
 
     // pass 1 -- online softmax statistics over this thread's columns (log2
@@ -280,6 +290,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     float m = -INFINITY, l = 0.f;
     for (int jj = 0; jj < nt; ++jj) {
       AQ_ACQUIRE_S(jj % C::NB1, jj / C::NB1);
+      const long long tp1 = clock64();
       const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
       if (lim < CW - 1) {
 #pragma unroll
@@ -317,7 +328,9 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         sum = expsum(m);
       }
       l += sum;
+      prof_p1 += clock64() - tp1;
     }
+    const long long p1_wait = prof_wait, p1_ld = prof_ld;
     // merge the CS column-split partials of each row
     float* ml = reinterpret_cast<float*>(smem + C::ML);
     ml[(half * 2 + 0) * TILE + row] = m;
@@ -344,13 +357,16 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         AQ_ACQUIRE_S(b, C::pass1_uses(nt, b) + jj / C::NB2);
       }
       const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+      const long long tm0 = clock64();
       if (!(p.debug & 2)) p_from_s<CW / 2>(x, cbase, sl2, L2);
       if (lim < CW - 1) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
       }
       const int pb = jj & 1;
+      const long long tm1 = clock64();
       if (jj >= 2) mbar_wait(&bars[C::B_P_EMPTY + pb], ((jj >> 1) - 1) & 1);
+      const long long tm2 = clock64();
       uint8_t* pc = smem + C::P0 + pb * C::P_BYTES + C::PB_CODES;
       uint8_t* psf = smem + C::P0 + pb * C::P_BYTES + C::PB_SF;
       uint32_t scw[(CW + 63) / 64];
@@ -391,37 +407,62 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
           *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
         }
       }
+      const long long tm3 = clock64();
       fence_async_smem();
       mbar_arrive(&bars[C::B_P_FULL + pb]);
+      const long long tm4 = clock64();
+      prof_p2m += tm1 - tm0;
+      prof_pw += tm2 - tm1;
+      prof_q += tm3 - tm2;
+      prof_f += tm4 - tm3;
     }
 #undef AQ_ACQUIRE_S
 
+    if ((p.debug & 32) && lane == 0) {
+      atomicAdd(&g_prof[0], static_cast<unsigned long long>(p1_wait));
+      atomicAdd(&g_prof[1], static_cast<unsigned long long>(p1_ld));
+      atomicAdd(&g_prof[2], static_cast<unsigned long long>(prof_p1));
+      atomicAdd(&g_prof[3], static_cast<unsigned long long>(prof_wait - p1_wait));
+      atomicAdd(&g_prof[4], static_cast<unsigned long long>(prof_ld - p1_ld));
+      atomicAdd(&g_prof[5], static_cast<unsigned long long>(prof_p2m));
+      atomicAdd(&g_prof[6], static_cast<unsigned long long>(prof_pw));
+      atomicAdd(&g_prof[7], static_cast<unsigned long long>(prof_q));
+      atomicAdd(&g_prof[8], static_cast<unsigned long long>(prof_f));
+      atomicAdd(&g_prof[9], static_cast<unsigned long long>(clock64() - prof_start));
+      atomicAdd(&g_prof[10], static_cast<unsigned long long>(nt));
+      atomicAdd(&g_prof[11], 1ull);
+    }
     // epilogue: this thread's D/CS columns of O (and O' * 1/l) -> global
     mbar_wait(&bars[C::B_O_FULL], 0);
     tc_fence_after();
     const float inv_l = 1.f / l_scale;
-    constexpr int DW = D / CS;
+    constexpr int DW = D / CS;             // output columns of this thread
+    constexpr int CH = DW < 32 ? DW : 32;  // columns per TMEM load
     for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
       void* dst = out ? p.o_hp : p.o;
       const int dt = out ? p.o_hp_dt : p.o_dt;
       const float mul = out ? inv_l : 1.f;
 #pragma unroll
-      for (int c = 0; c < DW; c += 32) {
+      for (int c = 0; c < DW; c += CH) {
         uint32_t r[32];
-        tmem_ld32(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, r);
+        if (CH == 32) {
+          tmem_ld32(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, r);
+        } else {
+          tmem_ld16(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, *reinterpret_cast<uint32_t(*)[16]>(r));
+        }
         tmem_ld_wait();
         if (dst != nullptr && grow < p.n_q) {
           const int64_t base = (head * p.n_q + grow) * D + half * DW + c;
           if (dt == 0) {
             float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
 #pragma unroll
-            for (int e = 0; e < 32; e += 4)
+            for (int e = 0; e < CH; e += 4)
               d4[e / 4] = make_float4(__uint_as_float(r[e]) * mul, __uint_as_float(r[e + 1]) * mul,
                                       __uint_as_float(r[e + 2]) * mul, __uint_as_float(r[e + 3]) * mul);
           } else {
             uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + base);
 #pragma unroll
-            for (int e = 0; e < 32; e += 8) {
+            for (int e = 0; e < CH; e += 8) {
               uint32_t h[4];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -463,7 +504,8 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 
 }  // namespace fwd
 
-// AQ_FWD_CS (environment, read once) selects the column split for tuning runs.
+// AQ_FWD_CS (environment, read once) selects the column split for tuning runs
+// (default 4: 16 softmax warps, 32 key columns per thread).
 static int fwd_debug() {
   static const int d = [] {
     const char* e = std::getenv("AQ_FWD_DEBUG");
@@ -475,9 +517,18 @@ static int fwd_debug() {
 static int fwd_cs() {
   static const int cs = [] {
     const char* e = std::getenv("AQ_FWD_CS");
-    return (e && std::atoi(e) == 4) ? 4 : 2;
+    return (e && std::atoi(e) == 2) ? 2 : 4;
   }();
   return cs;
+}
+
+extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, fwd::g_prof, sizeof(fwd::g_prof)) != cudaSuccess) return 5;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(fwd::g_prof, z, sizeof(z)) != cudaSuccess) return 5;
+  }
+  return 0;
 }
 
 cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {

@@ -31,7 +31,7 @@ __device__ __forceinline__ PBlock quantize_p16(const float* p) {
   if (sc == 0 && amax > 0.f) sc = 1;
   PBlock b;
   b.scale = sc;
-  b.sv = e4m3_to_f32(sc);
+  b.sv = e4m3_to_f32_cvt(sc);
   const float rs = b.sv > 0.f ? rcp_approx(b.sv) : 0.f;
   float q[16];
 #pragma unroll

@@ -1,0 +1,26 @@
+"""Per-segment cycle breakdown of the forward softmax warps (AQ_FWD_DEBUG=32)."""
+import ctypes, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_00040_b200 as aq  # noqa: E402
+from paper_2603_00040_b200 import _lib  # noqa: E402
+lib = _lib.load()
+fn = lib.aq_debug_fwd_profile
+fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+B, H, N, d, causal = 4, 32, 8192, 128, True
+q, k, v = (torch.randn(B, H, N, d, device="cuda").bfloat16() for _ in range(3))
+o, lse, _, ws = aq.attn_forward(q, k, v, causal=causal, train=False)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 16)()
+fn(buf, 1)
+aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, operands_staged=True)
+torch.cuda.synchronize()
+fn(buf, 0)
+v = list(buf)
+tiles = v[10]
+names = ["p1 S wait", "p1 TMEM ld", "p1 math", "p2 S wait", "p2 TMEM ld", "p2 exp", "p2 P_EMPTY wait", "p2 quant+st",
+         "p2 fence+arrive", "total"]
+print("per warp-tile cycles (averaged over warps):")
+for i, n in enumerate(names):
+    print(f"  {n:18s} {v[i] / tiles:9.1f}")
+print("warps", v[11], "tiles", tiles)
