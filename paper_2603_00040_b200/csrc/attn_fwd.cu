@@ -11,14 +11,19 @@
 //                             and 1/l applied in the epilogue)
 // O needs no rescaling: L is final before pass 2.
 //
-// CTA = one (head, 128-query tile). Softmax warps: CS warpgroups; warp w owns
-// TMEM lanes 32*(w%4).. (one query row per thread) and key columns
-// [(w/4)*128/CS, ...) of every S tile, so each row is processed by CS threads
-// in parallel with no exchange inside a tile (pass-1 (m, l) partials are
-// merged once, P^F blocks of 16 keys never straddle a column split).
-// One producer warp issues 1-D bulk copies of pre-tiled operands; one warp
-// issues the tcgen05 MMAs from a single thread. K/V stream through an
-// NS-stage mbarrier ring; S is double-buffered in TMEM.
+// Persistent kernel: one CTA per SM walks a static list of (head, query tile)
+// work items (longest causal rows first). Roles:
+//  * softmax warps (4*CS): warp w owns TMEM lanes 32*(w%4).. (one query row
+//    per thread) and key columns [(w/4)*128/CS, ...) of every S tile; pass-1
+//    (m, l) partials of a row are merged once per item, P^F blocks of 16 keys
+//    never straddle a column split;
+//  * one producer warp: 1-D bulk copies of pre-tiled Q / K / V operands
+//    (layouts.cuh), running ahead across item boundaries;
+//  * one MMA warp: the whole warp runs the schedule in warp-uniform registers,
+//    an elected lane issues tcgen05.cp / mma / commit.
+// K/V stream through an NS-stage ring, S through NB1 (pass 1) / NB2 (pass 2)
+// TMEM buffers, P^F through NP SMEM buffers; every ring counts phases across
+// items.
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -32,9 +37,15 @@ namespace aq {
 
 namespace fwd {
 
-// Timing-experiment counters (AQ_FWD_DEBUG bit 32): cycle sums per softmax
-// segment, accumulated from lane 0 of every softmax warp.
+// Tuning aid, compiled in with -DAQ_FWD_PROFILE and enabled at run time by
+// AQ_FWD_DEBUG bit 32: cycle sums per softmax segment, accumulated from lane
+// 0 of every softmax warp.
 __device__ unsigned long long g_prof[16];
+#ifdef AQ_FWD_PROFILE
+#define AQ_PROF(...) __VA_ARGS__
+#else
+#define AQ_PROF(...)
+#endif
 
 template <int D, bool TRAIN, int CS>
 struct Cfg {
@@ -43,7 +54,7 @@ struct Cfg {
   static constexpr int PRODUCER = NSW, MMA = NSW + 1;
   static constexpr int CW = TILE / CS;               // key columns per softmax thread
   static constexpr int NS = TRAIN ? 2 : 5;           // K/V stages
-  static constexpr int NB1 = 3;                      // S buffers in pass 1 (reuses O / O' columns)
+  static constexpr int NB1 = 3;                      // S buffers in pass 1 (1 and 2 alias O / O')
   static constexpr int NB2 = TRAIN ? 1 : 2;          // S buffers in pass 2
   static constexpr int NP = 2;                       // P^F (and P^) buffers
   // TMEM columns: S buffer b at 128*b
@@ -62,25 +73,56 @@ struct Cfg {
   static constexpr int P0 = STAGE0 + NS * STAGE_BYTES;
   static constexpr int PB_CODES = 0, PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024;
   static constexpr int P_BYTES = PB_H + (TRAIN ? TILE * TILE * 2 : 0);
-  static constexpr int P_H = P0 + NP * P_BYTES;  // end of the P buffers
-  static constexpr int ML = P_H;   // pass-1 (m, l) partials
+  static constexpr int ML = P0 + NP * P_BYTES;       // pass-1 (m, l) partials
   static constexpr int BARS = ML + 2 * CS * TILE * 4;
-  static constexpr int NUM_BARS = 24;
+  static constexpr int NUM_BARS = 32;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int USED = TMEM_SLOT + 16;
   // one CTA per SM (the kernel owns all 512 TMEM columns)
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
+  static constexpr int Q_BYTES = TILE * D / 2 + (D / 64) * 512;
   static constexpr int K_BYTES = TILE * D / 2 + (D / 64) * 512;
   static constexpr int V_BYTES = TILE * D / 2 + 1024 + (TRAIN ? TILE * D * 2 : 0);
   // barrier slots
-  static constexpr int B_Q = 0, B_KV_FULL = 1, B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS,
-                       B_S_EMPTY = B_S_FULL + NB1, B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP,
-                       B_O_FULL = B_P_EMPTY + NP;
+  static constexpr int B_Q_FULL = 0, B_Q_EMPTY = 1, B_O_FULL = 2, B_O_EMPTY = 3, B_KV_FULL = 4,
+                       B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS, B_S_EMPTY = B_S_FULL + NB1,
+                       B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP, B_END = B_P_EMPTY + NP;
+  static_assert(B_END <= NUM_BARS, "barrier slots");
   static_assert(USED <= 227 * 1024, "shared memory");
-  static_assert(B_O_FULL < NUM_BARS, "barrier slots");
   static_assert(T_VSF + 8 * NS <= 512, "TMEM columns");
-  // number of pass-1 uses of S buffer b (pass 2 continues its phase count)
-  __device__ static int pass1_uses(int nt, int b) { return nt > b ? (nt - b + NB1 - 1) / NB1 : 0; }
+};
+
+// Work item w -> (head, query tile, key tiles). Causal items are ordered by
+// decreasing row length so the static round-robin over CTAs balances.
+struct Item {
+  int64_t head;
+  int qt, nt;
+};
+
+__device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_tiles, int k_tiles) {
+  Item it;
+  if (p.causal) {
+    it.qt = q_tiles - 1 - static_cast<int>(w / p.heads);
+    it.head = w % p.heads;
+    const int64_t last =
+        static_cast<int64_t>(min(it.qt * TILE + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
+    it.nt = min(k_tiles, static_cast<int>(last / TILE) + 1);  // flash.py:127-128, 154
+  } else {
+    it.qt = static_cast<int>(w % q_tiles);
+    it.head = w / q_tiles;
+    it.nt = k_tiles;
+  }
+  return it;
+}
+
+// running use counters of the NB1 S buffers (warp-uniform, no dynamic indexing)
+struct SUses {
+  int u0 = 0, u1 = 0, u2 = 0;
+  __device__ __forceinline__ int take(int b) {
+    const int u = b == 0 ? u0 : (b == 1 ? u1 : u2);
+    if (b == 0) ++u0; else if (b == 1) ++u1; else ++u2;
+    return u;
+  }
 };
 
 template <int D, bool TRAIN, int CS>
@@ -92,20 +134,15 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int qt = blockIdx.x;
-  const int64_t head = blockIdx.y;
-  const int q0 = qt * TILE;
   const int q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
   const int k_tiles = static_cast<int>(ceil_div(p.n_k, TILE));
-  // key tiles with any visible key for this query tile (flash.py:127-128, 154)
-  int nt = k_tiles;
-  if (p.causal) {
-    const int64_t last = static_cast<int64_t>(min(q0 + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
-    nt = min(nt, static_cast<int>(last / TILE) + 1);
-  }
+  const int64_t n_items = p.heads * q_tiles;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[C::B_Q], 1);
+    mbar_init(&bars[C::B_Q_FULL], 1);
+    mbar_init(&bars[C::B_Q_EMPTY], 1);
+    mbar_init(&bars[C::B_O_FULL], 1);
+    mbar_init(&bars[C::B_O_EMPTY], 32 * C::NSW);
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(&bars[C::B_KV_FULL + s], 1);
       mbar_init(&bars[C::B_KV_EMPTY + s], 1);
@@ -118,7 +155,6 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       mbar_init(&bars[C::B_P_FULL + b], 32 * C::NSW);
       mbar_init(&bars[C::B_P_EMPTY + b], 1);
     }
-    mbar_init(&bars[C::B_O_FULL], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -129,25 +165,25 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
 
   if (warp == C::PRODUCER) {
     // ------------------------------------------------------------ producer
-    // (whole warp runs the loop so indices stay warp-uniform; one lane copies)
-    const int64_t qtile_idx = head * q_tiles + qt;
-    if (elect_one()) {
-      mbar_expect_tx(&bars[C::B_Q], TILE * D / 2 + (D / 64) * 512);
-      bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q]);
-      bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q]);
-    }
-    int it = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int j = 0; j < nt; ++j, ++it) {
-        const int st = it % C::NS;
-        if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
-        uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
-        const int64_t kt_idx = head * k_tiles + j;
-        uint64_t* fb = &bars[C::B_KV_FULL + st];
-        if (elect_one()) {
-          if ((p.debug & 8) && it >= C::NS) {  // timing experiment: no K/V traffic
-            mbar_arrive(fb);
-          } else {
+    int it = 0, k = 0;
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const Item item = work_item(p, w, q_tiles, k_tiles);
+      const int64_t qtile_idx = item.head * q_tiles + item.qt;
+      if (k > 0) mbar_wait(&bars[C::B_Q_EMPTY], (k - 1) & 1);
+      if (elect_one()) {
+        mbar_expect_tx(&bars[C::B_Q_FULL], C::Q_BYTES);
+        bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q_FULL]);
+        bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q_FULL]);
+      }
+      __syncwarp();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = 0; j < item.nt; ++j, ++it) {
+          const int st = it % C::NS;
+          if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
+          uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
+          const int64_t kt_idx = item.head * k_tiles + j;
+          uint64_t* fb = &bars[C::B_KV_FULL + st];
+          if (elect_one()) {
             mbar_expect_tx(fb, C::K_BYTES + (pass ? C::V_BYTES : 0));
             bulk_g2s(sb + C::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
             bulk_g2s(sb + C::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
@@ -157,14 +193,12 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
               if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp == C::MMA) {
     // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs the schedule (waits, descriptor arithmetic in uniform
-    // registers); one elected lane issues tcgen05.cp / mma / commit.
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
     constexpr uint32_t id_pv = idesc_nvf4(128, D);
     constexpr uint32_t id_op = idesc_f16(128, D, /*f16*/ 0, /*a_mn*/ 0, /*b_mn*/ 1);
@@ -175,17 +209,13 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     constexpr uint64_t t_vh = desc_template(128, 2048);      // V^F fp16 (MN-major T8x8)
     const uint32_t s0 = smem_u32(smem);
     const uint32_t q_base = s0 + C::Q_CODES;
-    mbar_wait(&bars[C::B_Q], 0);
-    tc_fence_after();
-    if (elect_one()) {
-      for (int ks = 0; ks < D / 64; ++ks)
-        tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, desc_at(t_sf, s0 + C::Q_SF + ks * 512));
-    }
-    __syncwarp();
-    // S(it) into buffer b, its u-th use
-    auto issue_s = [&](int it, int b, int u) {
-      const int st = it % C::NS;
-      mbar_wait(&bars[C::B_KV_FULL + st], (it / C::NS) & 1);
+    int it = 0, pc = 0, k = 0;
+    SUses su;
+    // S(it) into buffer b
+    auto issue_s = [&](int it_, int b) {
+      const int u = su.take(b);
+      const int st = it_ % C::NS;
+      mbar_wait(&bars[C::B_KV_FULL + st], (it_ / C::NS) & 1);
       if (u > 0) mbar_wait(&bars[C::B_S_EMPTY + b], (u - 1) & 1);
       tc_fence_after();
       const uint32_t kb = s0 + C::STAGE0 + st * C::STAGE_BYTES + C::ST_K;
@@ -202,223 +232,296 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       }
       __syncwarp();
     };
-    // pass 1: S tiles round-robin over NB1 buffers; K stages released right away
-    int it = 0;
-    for (int jj = 0; jj < nt; ++jj, ++it) {
-      issue_s(it, jj % C::NB1, jj / C::NB1);
-      if (elect_one()) tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
-      __syncwarp();
-    }
-    // pass 2: S tiles run up to NB2 ahead of the PV MMAs (S(ns) reuses the
-    // buffer of S(ns - NB2), which the softmax warps release as soon as they
-    // have loaded it); P double-buffered
-    const int it2 = it;
-    for (int ns = 0, np = 0; np < nt;) {
-      if (ns < nt && ns <= np + C::NB2) {
-        const int b = ns % C::NB2;
-        issue_s(it2 + ns, b, C::pass1_uses(nt, b) + ns / C::NB2);
-        ++ns;
-        continue;
-      }
-      const int pj = np++;
-      const int pb = pj & 1;
-      const int st = (it2 + pj) % C::NS;
-      mbar_wait(&bars[C::B_P_FULL + pb], (pj >> 1) & 1);
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const int nt = work_item(p, w, q_tiles, k_tiles).nt;
+      mbar_wait(&bars[C::B_Q_FULL], k & 1);
       tc_fence_after();
-      const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
-      const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
       if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
-          tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
-        }
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-          mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
-                      desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
-                      tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
-        if (TRAIN) {
-#pragma unroll
-          for (int ks = 0; ks < TILE / 16; ++ks)
-            mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
-                       desc_at(t_vh, sb + C::ST_VH + ks * 256), id_op, (pj > 0 || ks > 0));
-        }
-        tc_commit(&bars[C::B_P_EMPTY + pb]);
-        tc_commit(&bars[C::B_KV_EMPTY + st]);
+        for (int ks = 0; ks < D / 64; ++ks)
+          tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, desc_at(t_sf, s0 + C::Q_SF + ks * 512));
       }
       __syncwarp();
+      // pass 1: S tiles round-robin over NB1 buffers; buffers 1 and 2 alias
+      // the O (/O') columns, so they wait for the previous item's epilogue
+      for (int jj = 0; jj < nt; ++jj, ++it) {
+        if (jj == 1 && k > 0) mbar_wait(&bars[C::B_O_EMPTY], (k - 1) & 1);
+        issue_s(it, jj % C::NB1);
+        if (elect_one()) tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
+        __syncwarp();
+      }
+      if (nt == 1 && k > 0) mbar_wait(&bars[C::B_O_EMPTY], (k - 1) & 1);
+      // pass 2: S tiles run up to NB2 ahead of the PV MMAs (S(ns) reuses the
+      // buffer of S(ns - NB2), released as soon as the softmax warps loaded it)
+      const int it2 = it;
+      for (int ns = 0, np = 0; np < nt;) {
+        if (ns < nt && ns <= np + C::NB2) {
+          issue_s(it2 + ns, ns % C::NB2);
+          if (ns == nt - 1 && elect_one()) tc_commit(&bars[C::B_Q_EMPTY]);  // last read of Q
+          __syncwarp();
+          ++ns;
+          continue;
+        }
+        const int pj = np++;
+        const int pb = pc & 1;
+        const int st = (it2 + pj) % C::NS;
+        mbar_wait(&bars[C::B_P_FULL + pb], (pc >> 1) & 1);
+        ++pc;
+        tc_fence_after();
+        const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
+        const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
+            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
+          }
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
+                        desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
+                        tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
+          if (TRAIN) {
+#pragma unroll
+            for (int ks = 0; ks < TILE / 16; ++ks)
+              mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
+                         desc_at(t_vh, sb + C::ST_VH + ks * 256), id_op, (pj > 0 || ks > 0));
+          }
+          tc_commit(&bars[C::B_P_EMPTY + pb]);
+          tc_commit(&bars[C::B_KV_EMPTY + st]);
+        }
+        __syncwarp();
+      }
+      it = it2 + nt;
+      if (elect_one()) tc_commit(&bars[C::B_O_FULL]);
+      __syncwarp();
     }
-    if (elect_one()) tc_commit(&bars[C::B_O_FULL]);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ softmax warps
     constexpr int CW = C::CW;
     const int row = 32 * (warp & 3) + lane;        // TMEM lane == query row in the tile
     const int half = warp >> 2;                    // which column split
     const int cbase = half * CW;
-    const int64_t grow = q0 + row;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;  // log2(e) / sqrt(d)
-    int64_t kmax = p.n_k - 1;        // last visible key of this row (inclusive)
-    if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
+    const bool prof = (p.debug & 32) != 0;
     float x[CW];
-    long long prof_wait = 0, prof_ld = 0, prof_p1 = 0, prof_p2m = 0, prof_pw = 0, prof_q = 0, prof_f = 0;
-    const long long prof_start = clock64();
+    SUses su;
+    int pc = 0, k = 0;
+    AQ_PROF(long long prof_wait = 0, prof_ld = 0, prof_p1 = 0, prof_p2m = 0, prof_pw = 0, prof_q = 0, prof_f = 0;)
+    AQ_PROF(long long p1_wait = 0, p1_ld = 0, tiles = 0;)
+    AQ_PROF(const long long prof_start = clock64();)
 
-#define AQ_ACQUIRE_S(b_, u_)                                                  \
+#define AQ_ACQUIRE_S(b_)                                                      \
   do {                                                                        \
     const int b__ = (b_);                                                     \
-    const long long t0__ = clock64();                                         \
-    mbar_wait(&bars[C::B_S_FULL + b__], (u_) & 1);                            \
+    const int u__ = su.take(b__);                                             \
+    AQ_PROF(const long long t0__ = clock64();)                                \
+    mbar_wait(&bars[C::B_S_FULL + b__], u__ & 1);                             \
     tc_fence_after();                                                         \
-    const long long t1__ = clock64();                                         \
+    AQ_PROF(const long long t1__ = clock64();)                                \
     const uint32_t base__ = t_lane + 128 * b__ + cbase;                       \
     _Pragma("unroll") for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(base__ + c0, x + c0); \
     tmem_ld_wait();                                                           \
     tc_fence_before();                                                        \
     mbar_arrive(&bars[C::B_S_EMPTY + b__]);                                   \
-    const long long t2__ = clock64();                                         \
-    prof_wait += t1__ - t0__;                                                 \
-    prof_ld += t2__ - t1__;                                                   \
+    AQ_PROF(prof_wait += t1__ - t0__; prof_ld += clock64() - t1__;)           \
   } while (0)
 
-    // pass 1 -- online softmax statistics over this thread's columns (log2
-    // domain). The exponentials use a reference max m that is only raised when
-    // a tile's max exceeds it by more than 2^8 (terms stay <= 256), so they do
-    // not wait for the tile's max reduction; a raise recomputes the tile.
-    float m = -INFINITY, l = 0.f;
-    for (int jj = 0; jj < nt; ++jj) {
-      AQ_ACQUIRE_S(jj % C::NB1, jj / C::NB1);
-      const long long tp1 = clock64();
-      const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
-      if (lim < CW - 1) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
-      }
-      auto expsum = [&](float base) {
-        float2 acc[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < CW / 2; ++i) {
-          const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
-                                      make_float2(-base, -base));
-          const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
-          acc[i & 3] = __fadd2_rn(acc[i & 3], e);
-        }
-        const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
-        const float2 s4 = __fadd2_rn(s01, s23);
-        return s4.x + s4.y;
-      };
-      if (p.debug & 4) { l = 1.f; m = 0.f; continue; }
-      float sum = expsum(m == -INFINITY ? 0.f : m);
-      // row max on the raw scores (the scale is positive)
-      float mx[8];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) mx[a] = x[a];
-#pragma unroll
-      for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
-      const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
-      if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
-        const float m_new = mloc;
-        l = (m == -INFINITY) ? 0.f : l * ex2(m - m_new);
-        m = m_new;
-        sum = expsum(m);
-      }
-      l += sum;
-      prof_p1 += clock64() - tp1;
-    }
-    const long long p1_wait = prof_wait, p1_ld = prof_ld;
-    // merge the CS column-split partials of each row
-    float* ml = reinterpret_cast<float*>(smem + C::ML);
-    ml[(half * 2 + 0) * TILE + row] = m;
-    ml[(half * 2 + 1) * TILE + row] = l;
-    named_bar_sync(1, 32 * C::NSW);
-    float mt = -INFINITY;
-#pragma unroll
-    for (int h = 0; h < CS; ++h) mt = fmaxf(mt, ml[(h * 2) * TILE + row]);
-    float lt = 0.f;
-#pragma unroll
-    for (int h = 0; h < CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
-    // natural-log L is what the reference stores (flash.py:217); pass 2 uses
-    // L2 = L * log2(e) recomputed from the stored value so the backward, which
-    // only sees L, rebuilds bit-identical P (and P^F).
-    const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
-    if (half == 0 && grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
-    const float L2 = L_nat * 1.44269504088896340736f;
-    const float l_scale = lt;  // P^ = exp(S - m) = P * l
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const Item item = work_item(p, w, q_tiles, k_tiles);
+      const int nt = item.nt;
+      const int64_t head = item.head;
+      const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
+      int64_t kmax = p.n_k - 1;  // last visible key of this row (inclusive)
+      if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
+      AQ_PROF(tiles += nt;)
 
-    // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
-    for (int jj = 0; jj < nt; ++jj) {
-      {
-        const int b = jj % C::NB2;
-        AQ_ACQUIRE_S(b, C::pass1_uses(nt, b) + jj / C::NB2);
-      }
-      const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
-      const long long tm0 = clock64();
-      if (!(p.debug & 2)) p_from_s<CW / 2>(x, cbase, sl2, L2);
-      if (lim < CW - 1) {
+      // pass 1 -- online softmax statistics over this thread's columns (log2
+      // domain). The exponentials use a reference max m that is only raised
+      // when a tile's max exceeds it by more than 2^8 (terms stay <= 256), so
+      // they do not wait for the tile's max reduction; a raise recomputes.
+      float m = -INFINITY, l = 0.f;
+      for (int jj = 0; jj < nt; ++jj) {
+        AQ_ACQUIRE_S(jj % C::NB1);
+        AQ_PROF(const long long tp1 = clock64();)
+        const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
+        if (lim < CW - 1) {
 #pragma unroll
-        for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
-      }
-      const int pb = jj & 1;
-      const long long tm1 = clock64();
-      if (jj >= 2) mbar_wait(&bars[C::B_P_EMPTY + pb], ((jj >> 1) - 1) & 1);
-      const long long tm2 = clock64();
-      uint8_t* pc = smem + C::P0 + pb * C::P_BYTES + C::PB_CODES;
-      uint8_t* psf = smem + C::P0 + pb * C::P_BYTES + C::PB_SF;
-      uint32_t scw[(CW + 63) / 64];
-#pragma unroll
-      for (int w = 0; w < (CW + 63) / 64; ++w) scw[w] = 0;
-#pragma unroll
-      for (int blk = 0; blk < CW / 16; blk += 2) {
-        if (p.debug & 1) {
-          *reinterpret_cast<uint4*>(pc + t8x32_off(row, cbase + blk * 16, TILE)) =
-              make_uint4(__float_as_uint(x[blk * 16]), 0, 0, 0);
-          continue;
+          for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
         }
-        const PBlock qa = quantize_p16(x + blk * 16);
-        const PBlock qb = quantize_p16(x + blk * 16 + 16);
-        *reinterpret_cast<uint4*>(pc + t8x32_off(row, cbase + blk * 16, TILE)) =
-            make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
-        scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
-      }
-      if (CW >= 64) {
+        auto expsum = [&](float base) {
+          float2 acc[4];
 #pragma unroll
-        for (int w = 0; w < CW / 64; ++w)
-          *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * w)) = scw[w];
-      } else {
-        *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
-      }
-      if (TRAIN) {
-        uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
+          for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c8 = 0; c8 < CW / 8; ++c8) {
-          uint32_t h[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 ph2 = __fmul2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]),
-                                          make_float2(l_scale, l_scale));
-            const __half2 v = __floats2half2_rn(ph2.x, ph2.y);
-            h[e] = *reinterpret_cast<const uint32_t*>(&v);
+          for (int i = 0; i < CW / 2; ++i) {
+            const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
+                                        make_float2(-base, -base));
+            const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+            acc[i & 3] = __fadd2_rn(acc[i & 3], e);
           }
-          *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
+          const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+          const float2 s4 = __fadd2_rn(s01, s23);
+          return s4.x + s4.y;
+        };
+        float sum = expsum(m == -INFINITY ? 0.f : m);
+        // row max on the raw scores (the scale is positive)
+        float mx[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mx[a] = x[a];
+#pragma unroll
+        for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+        const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+        if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
+          l = (m == -INFINITY) ? 0.f : l * ex2(m - mloc);
+          m = mloc;
+          sum = expsum(m);
+        }
+        l += sum;
+        AQ_PROF(prof_p1 += clock64() - tp1;)
+      }
+      AQ_PROF(p1_wait = prof_wait; p1_ld = prof_ld;)
+      // merge the CS column-split partials of each row
+      float* ml = reinterpret_cast<float*>(smem + C::ML);
+      ml[(half * 2 + 0) * TILE + row] = m;
+      ml[(half * 2 + 1) * TILE + row] = l;
+      named_bar_sync(1, 32 * C::NSW);
+      float mt = -INFINITY;
+#pragma unroll
+      for (int h = 0; h < CS; ++h) mt = fmaxf(mt, ml[(h * 2) * TILE + row]);
+      float lt = 0.f;
+#pragma unroll
+      for (int h = 0; h < CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
+      named_bar_sync(1, 32 * C::NSW);  // the partials buffer is reused by the next item
+      // natural-log L is what the reference stores (flash.py:217); pass 2 uses
+      // L2 = L * log2(e) recomputed from the stored value so the backward, which
+      // only sees L, rebuilds bit-identical P (and P^F).
+      const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
+      if (half == 0 && grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
+      const float L2 = L_nat * 1.44269504088896340736f;
+      const float l_scale = lt;  // P^ = exp(S - m) = P * l
+
+      // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
+      for (int jj = 0; jj < nt; ++jj) {
+        AQ_ACQUIRE_S(jj % C::NB2);
+        AQ_PROF(const long long tm0 = clock64();)
+        const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+        p_from_s<CW / 2>(x, cbase, sl2, L2);
+        if (lim < CW - 1) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
+        }
+        const int pb = pc & 1;
+        AQ_PROF(const long long tm1 = clock64();)
+        if (pc >= 2) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc >> 1) - 1) & 1);
+        ++pc;
+        AQ_PROF(const long long tm2 = clock64();)
+        uint8_t* pcodes = smem + C::P0 + pb * C::P_BYTES + C::PB_CODES;
+        uint8_t* psf = smem + C::P0 + pb * C::P_BYTES + C::PB_SF;
+        uint32_t scw[(CW + 63) / 64];
+#pragma unroll
+        for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
+#pragma unroll
+        for (int blk = 0; blk < CW / 16; blk += 2) {
+          const PBlock qa = quantize_p16(x + blk * 16);
+          const PBlock qb = quantize_p16(x + blk * 16 + 16);
+          *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
+              make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
+          scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+        }
+        if (CW >= 64) {
+#pragma unroll
+          for (int s = 0; s < CW / 64; ++s)
+            *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
+        } else {
+          *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
+        }
+        if (TRAIN) {
+          uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
+#pragma unroll
+          for (int c8 = 0; c8 < CW / 8; ++c8) {
+            uint32_t h[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 ph2 = __fmul2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]),
+                                            make_float2(l_scale, l_scale));
+              const __half2 v = __floats2half2_rn(ph2.x, ph2.y);
+              h[e] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
+          }
+        }
+        AQ_PROF(const long long tm3 = clock64();)
+        fence_async_smem();
+        mbar_arrive(&bars[C::B_P_FULL + pb]);
+        AQ_PROF(const long long tm4 = clock64(); prof_p2m += tm1 - tm0; prof_pw += tm2 - tm1;)
+        AQ_PROF(prof_q += tm3 - tm2; prof_f += tm4 - tm3;)
+      }
+
+      // epilogue: this thread's D/CS columns of O (and O' * 1/l) -> registers,
+      // release the O columns, then store
+      mbar_wait(&bars[C::B_O_FULL], k & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l_scale;
+      constexpr int DW = D / CS;             // output columns of this thread
+      float o[TRAIN ? 2 : 1][DW];
+#pragma unroll
+      for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
+#pragma unroll
+        for (int c = 0; c < DW; c += (DW < 32 ? DW : 32)) {
+          if (DW >= 32) {
+            tmem_ld32f(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, o[out] + c);
+          } else {
+            uint32_t r[16];
+            tmem_ld16(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[out][c + e] = __uint_as_float(r[e]);
+          }
         }
       }
-      const long long tm3 = clock64();
-      fence_async_smem();
-      mbar_arrive(&bars[C::B_P_FULL + pb]);
-      const long long tm4 = clock64();
-      prof_p2m += tm1 - tm0;
-      prof_pw += tm2 - tm1;
-      prof_q += tm3 - tm2;
-      prof_f += tm4 - tm3;
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[C::B_O_EMPTY]);
+      if (grow < p.n_q) {
+#pragma unroll
+        for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
+          void* dst = out ? p.o_hp : p.o;
+          if (dst == nullptr) continue;
+          const int dt = out ? p.o_hp_dt : p.o_dt;
+          const float mul = out ? inv_l : 1.f;
+          const int64_t base = (head * p.n_q + grow) * D + half * DW;
+          if (dt == 0) {
+            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
+#pragma unroll
+            for (int e = 0; e < DW; e += 4)
+              d4[e / 4] = make_float4(o[out][e] * mul, o[out][e + 1] * mul, o[out][e + 2] * mul, o[out][e + 3] * mul);
+          } else {
+            uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + base);
+#pragma unroll
+            for (int e = 0; e < DW; e += 8) {
+              uint32_t h[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float a = o[out][e + 2 * q] * mul, bb = o[out][e + 2 * q + 1] * mul;
+                if (dt == 1) {
+                  const __nv_bfloat162 v = __floats2bfloat162_rn(a, bb);
+                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
+                } else {
+                  const __half2 v = __floats2half2_rn(a, bb);
+                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
+                }
+              }
+              d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+            }
+          }
+        }
+      }
     }
 #undef AQ_ACQUIRE_S
-
-    if ((p.debug & 32) && lane == 0) {
+#ifdef AQ_FWD_PROFILE
+    if (prof && lane == 0) {
       atomicAdd(&g_prof[0], static_cast<unsigned long long>(p1_wait));
       atomicAdd(&g_prof[1], static_cast<unsigned long long>(p1_ld));
       atomicAdd(&g_prof[2], static_cast<unsigned long long>(prof_p1));
@@ -429,58 +532,12 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       atomicAdd(&g_prof[7], static_cast<unsigned long long>(prof_q));
       atomicAdd(&g_prof[8], static_cast<unsigned long long>(prof_f));
       atomicAdd(&g_prof[9], static_cast<unsigned long long>(clock64() - prof_start));
-      atomicAdd(&g_prof[10], static_cast<unsigned long long>(nt));
+      atomicAdd(&g_prof[10], static_cast<unsigned long long>(tiles));
       atomicAdd(&g_prof[11], 1ull);
     }
-    // epilogue: this thread's D/CS columns of O (and O' * 1/l) -> global
-    mbar_wait(&bars[C::B_O_FULL], 0);
-    tc_fence_after();
-    const float inv_l = 1.f / l_scale;
-    constexpr int DW = D / CS;             // output columns of this thread
-    constexpr int CH = DW < 32 ? DW : 32;  // columns per TMEM load
-    for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
-      void* dst = out ? p.o_hp : p.o;
-      const int dt = out ? p.o_hp_dt : p.o_dt;
-      const float mul = out ? inv_l : 1.f;
-#pragma unroll
-      for (int c = 0; c < DW; c += CH) {
-        uint32_t r[32];
-        if (CH == 32) {
-          tmem_ld32(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, r);
-        } else {
-          tmem_ld16(t_lane + (out ? C::T_OP : C::T_O) + half * DW + c, *reinterpret_cast<uint32_t(*)[16]>(r));
-        }
-        tmem_ld_wait();
-        if (dst != nullptr && grow < p.n_q) {
-          const int64_t base = (head * p.n_q + grow) * D + half * DW + c;
-          if (dt == 0) {
-            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
-#pragma unroll
-            for (int e = 0; e < CH; e += 4)
-              d4[e / 4] = make_float4(__uint_as_float(r[e]) * mul, __uint_as_float(r[e + 1]) * mul,
-                                      __uint_as_float(r[e + 2]) * mul, __uint_as_float(r[e + 3]) * mul);
-          } else {
-            uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + base);
-#pragma unroll
-            for (int e = 0; e < CH; e += 8) {
-              uint32_t h[4];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const float a = __uint_as_float(r[e + 2 * k]) * mul, bb = __uint_as_float(r[e + 2 * k + 1]) * mul;
-                if (dt == 1) {
-                  const __nv_bfloat162 v = __floats2bfloat162_rn(a, bb);
-                  h[k] = *reinterpret_cast<const uint32_t*>(&v);
-                } else {
-                  const __half2 v = __floats2half2_rn(a, bb);
-                  h[k] = *reinterpret_cast<const uint32_t*>(&v);
-                }
-              }
-              d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
-            }
-          }
-        }
-      }
-    }
+#else
+    (void)prof;
+#endif
   }
 
   tc_fence_before();
@@ -497,28 +554,30 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   auto kern = attn_fwd_kernel<D, TRAIN, CS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(ceil_div(p.n_q, TILE)), static_cast<unsigned>(p.heads));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = p.heads * ceil_div(p.n_q, TILE);
+  const int grid = static_cast<int>(items < sms ? items : sms);
   kern<<<grid, C::NUM_THREADS, C::TOTAL, st>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace fwd
 
-// AQ_FWD_CS (environment, read once) selects the column split for tuning runs
-// (default 4: 16 softmax warps, 32 key columns per thread).
+// Tuning-aid environment switches (read once): AQ_FWD_CS = 2 | 4 column
+// splits (default 4: 16 softmax warps, 32 key columns per thread);
+// AQ_FWD_DEBUG bit 32 = per-segment cycle counters (aq_debug_fwd_profile).
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 static int fwd_debug() {
-  static const int d = [] {
-    const char* e = std::getenv("AQ_FWD_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int d = env_int("AQ_FWD_DEBUG", 0);
   return d;
 }
-
 static int fwd_cs() {
-  static const int cs = [] {
-    const char* e = std::getenv("AQ_FWD_CS");
-    return (e && std::atoi(e) == 2) ? 2 : 4;
-  }();
+  static const int cs = env_int("AQ_FWD_CS", 4) == 2 ? 2 : 4;
   return cs;
 }
 
@@ -534,13 +593,13 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
 cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
   FwdParams p = p_in;
   p.debug = fwd_debug();
-  if (fwd_cs() == 4) {
-    if (p.d == 64) return p.train ? fwd::launch<64, true, 4>(p, st) : fwd::launch<64, false, 4>(p, st);
-    if (p.d == 128) return p.train ? fwd::launch<128, true, 4>(p, st) : fwd::launch<128, false, 4>(p, st);
+  if (fwd_cs() == 2) {
+    if (p.d == 64) return p.train ? fwd::launch<64, true, 2>(p, st) : fwd::launch<64, false, 2>(p, st);
+    if (p.d == 128) return p.train ? fwd::launch<128, true, 2>(p, st) : fwd::launch<128, false, 2>(p, st);
     return cudaErrorInvalidValue;
   }
-  if (p.d == 64) return p.train ? fwd::launch<64, true, 2>(p, st) : fwd::launch<64, false, 2>(p, st);
-  if (p.d == 128) return p.train ? fwd::launch<128, true, 2>(p, st) : fwd::launch<128, false, 2>(p, st);
+  if (p.d == 64) return p.train ? fwd::launch<64, true, 4>(p, st) : fwd::launch<64, false, 4>(p, st);
+  if (p.d == 128) return p.train ? fwd::launch<128, true, 4>(p, st) : fwd::launch<128, false, 4>(p, st);
   return cudaErrorInvalidValue;
 }
 
