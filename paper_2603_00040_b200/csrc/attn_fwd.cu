@@ -93,7 +93,9 @@ struct Cfg {
 };
 
 // Work item w -> (head, query tile, key tiles). Causal items are ordered by
-// decreasing row length so the static round-robin over CTAs balances.
+// decreasing row length across all heads (longest-processing-time first), so
+// the static round-robin over CTAs balances; K/V re-reads this causes stay
+// far below the HBM roofline (ncu: ~1 TB/s on C2).
 struct Item {
   int64_t head;
   int qt, nt;
