@@ -71,6 +71,7 @@ cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st);
 cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
                               int out_dt, cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
                            int d, float* delta, uint8_t* do_h, float* dq_acc, cudaStream_t st);

@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int NS = TRAIN ? 2 : 5;           // K/V stages
   static constexpr int NB1 = 3;                      // S buffers in pass 1 (1 and 2 alias O / O')
   static constexpr int NB2 = TRAIN ? 1 : 2;          // S buffers in pass 2
-  static constexpr int NP = 2;                       // P^F (and P^) buffers
+  static constexpr int NP = TRAIN ? 2 : 3;           // P^F (and P^) buffers
   // TMEM columns: S buffer b at 128*b
   static constexpr uint32_t T_O = TRAIN ? 128 : 256, T_OP = 256;
   static constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = T_KSF + 8 * NS, T_VSF = T_PSF + 8 * NP;
@@ -264,9 +264,9 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
           continue;
         }
         const int pj = np++;
-        const int pb = pc & 1;
+        const int pb = pc % C::NP;
         const int st = (it2 + pj) % C::NS;
-        mbar_wait(&bars[C::B_P_FULL + pb], (pc >> 1) & 1);
+        mbar_wait(&bars[C::B_P_FULL + pb], (pc / C::NP) & 1);
         ++pc;
         tc_fence_after();
         const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
@@ -414,9 +414,9 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
 #pragma unroll
           for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
         }
-        const int pb = pc & 1;
+        const int pb = pc % C::NP;
         AQ_PROF(const long long tm1 = clock64();)
-        if (pc >= 2) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc >> 1) - 1) & 1);
+        if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
         ++pc;
         AQ_PROF(const long long tm2 = clock64();)
         uint8_t* pcodes = smem + C::P0 + pb * C::P_BYTES + C::PB_CODES;
@@ -568,7 +568,8 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 }  // namespace fwd
 
 // Tuning-aid environment switches (read once): AQ_FWD_CS = 2 | 4 column
-// splits (default 4: 16 softmax warps, 32 key columns per thread);
+// splits of the training forward (default 2: 8 softmax warps, 64 key columns
+// per thread);
 // AQ_FWD_DEBUG bit 32 = per-segment cycle counters (aq_debug_fwd_profile).
 static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -579,7 +580,9 @@ static int fwd_debug() {
   return d;
 }
 static int fwd_cs() {
-  static const int cs = env_int("AQ_FWD_CS", 4) == 2 ? 2 : 4;
+  // default 2: the same column split (and (m, l) merge order) as the
+  // inference kernel, so training and inference forwards agree bit for bit
+  static const int cs = env_int("AQ_FWD_CS", 2) == 4 ? 4 : 2;
   return cs;
 }
 
@@ -595,6 +598,9 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
 cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
   FwdParams p = p_in;
   p.debug = fwd_debug();
+  // inference: the split-pass kernel (attn_fwd_infer.cu); AQ_FWD_INFER=0 keeps
+  // it on this kernel (tuning comparisons)
+  if (!p.train && env_int("AQ_FWD_INFER", 1)) return launch_attn_fwd_infer(p, st);
   if (fwd_cs() == 2) {
     if (p.d == 64) return p.train ? fwd::launch<64, true, 2>(p, st) : fwd::launch<64, false, 2>(p, st);
     if (p.d == 128) return p.train ? fwd::launch<128, true, 2>(p, st) : fwd::launch<128, false, 2>(p, st);
