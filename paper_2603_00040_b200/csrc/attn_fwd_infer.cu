@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             for (int i = 0; i < CW / 2; ++i) {
               const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
                                           make_float2(-base, -base));
-              const float2 e = use_poly(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+              const float2 e = use_poly_p1(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
               acc[i & 3] = __fadd2_rn(acc[i & 3], e);
             }
             const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);

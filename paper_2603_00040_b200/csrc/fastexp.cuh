@@ -49,4 +49,12 @@ __device__ __forceinline__ float2 ex2_pair(float2 t) {
 #endif
 __host__ __device__ constexpr bool use_poly(int pair) { return (pair & 7) < AQ_POLY_PAIRS_OF_8; }
 
+// Pass-1 (exp-sum for L) split; independent of the pass-2 / backward split
+// (P must match between forward and backward, L only between the two forward
+// kernels, which share this code).
+#ifndef AQ_POLY_P1_PAIRS_OF_8
+#define AQ_POLY_P1_PAIRS_OF_8 AQ_POLY_PAIRS_OF_8
+#endif
+__host__ __device__ constexpr bool use_poly_p1(int pair) { return (pair & 7) < AQ_POLY_P1_PAIRS_OF_8; }
+
 }  // namespace aq
