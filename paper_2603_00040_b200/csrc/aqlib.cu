@@ -48,7 +48,7 @@ FwdWs fwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int 
 }
 
 struct BwdWs {
-  int64_t fwd, do_h, delta, dq_acc, total;
+  int64_t fwd, do_h, delta, total;
 };
 
 BwdWs bwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
@@ -64,7 +64,6 @@ BwdWs bwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
   w.fwd = take(f.total);  // re-quantized operands when no forward workspace is given
   w.do_h = take(heads * qt * h_tile_bytes(static_cast<int>(d)));
   w.delta = take(heads * qt * TILE * 4);
-  w.dq_acc = take(heads * qt * TILE * d * 4);  // [heads][n_pad][d] fp32
   w.total = off;
   return w;
 }
@@ -260,9 +259,8 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
     w = fw;
   }
   float* delta = reinterpret_cast<float*>(ws + bw.delta);
-  float* dq_acc = reinterpret_cast<float*>(ws + bw.dq_acc);
   cudaError_t e = launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, static_cast<int>(a->d),
-                                 delta, ws + bw.do_h, dq_acc, st);
+                                 delta, ws + bw.do_h, st);
   if (e != cudaSuccess) return AQ_E_CUDA;
   BwdParams p{};
   p.q_codes = ops + w.q_codes;
@@ -275,7 +273,7 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
   p.do_h = ws + bw.do_h;
   p.lse = a->lse;
   p.delta = delta;
-  p.dq_acc = dq_acc;
+  p.dq = a->dq;
   p.dk = a->dk;
   p.dv = a->dv;
   p.g_dt = a->g_dtype;
@@ -287,9 +285,7 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
   p.fq_p = (a->variant == AQ_BWD_CORRECT || a->variant == AQ_BWD_LOW_PREC_O) ? 1 : 0;  // flash.py:93-95
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
   p.inv_sqrt_d = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a->d)));
-  e = launch_attn_bwd(p, st);
-  if (e != cudaSuccess) return AQ_E_CUDA;
-  return cuda_status(launch_dq_convert(dq_acc, a->dq, a->g_dtype, a->heads, a->n_q, static_cast<int>(a->d), st));
+  return cuda_status(launch_attn_bwd(p, st));
 }
 
 }  // extern "C"

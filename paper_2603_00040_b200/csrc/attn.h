@@ -54,7 +54,7 @@ struct BwdParams {
   const uint8_t* do_h;   // bf16 T8x8 dO tiles
   const float* lse;      // [heads][n_q]
   const float* delta;    // [heads][nq_pad] D = rowsum(dO . O_ref)
-  float* dq_acc;         // [heads][n_pad][d] fp32 (n_pad = 128-multiple), zero-initialised
+  void* dq;
   void* dk;
   void* dv;
   int g_dt;
@@ -74,8 +74,6 @@ cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
-                           int d, float* delta, uint8_t* do_h, float* dq_acc, cudaStream_t st);
-cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int g_dt, int64_t heads, int64_t n_q, int d,
-                              cudaStream_t st);
+                           int d, float* delta, uint8_t* do_h, cudaStream_t st);
 
 }  // namespace aq
