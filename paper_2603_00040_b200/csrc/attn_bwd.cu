@@ -13,16 +13,17 @@
 //   dQ += dS K^F                  bf16 MMA            (flash.py:384)
 //   dK += dS^T Q^F                bf16 MMA            (flash.py:385)
 //
-// Two kernels, each owning its accumulators in TMEM for the whole reduction,
-// so no gradient goes through atomics or an fp32 HBM accumulator and every
+// Two roles, each owning its accumulators in TMEM for the whole reduction, so
+// no gradient goes through atomics or an fp32 HBM accumulator and every
 // gradient is deterministic:
-//  * K7a attn_bwd_kv: CTA = (head, 128-key tile); dK, dV stationary while it
-//    loops over query tiles (the reference's key-outer loop, flash.py:360-365);
-//  * K7b attn_bwd_q:  CTA = (head, 128-query tile); dQ stationary while it
-//    loops over key tiles, recomputing S, P, dP, dS (dQ does not need P^F).
-// Both: 8 compute warps (thread = query row x 64-key half), one producer warp
-// (1-D bulk copies of pre-tiled operands), one MMA warp (warp-uniform
-// schedule; one elected lane issues tcgen05.cp / mma / commit).
+//  * KV role: CTA = (head, 128-key tile); dK, dV stationary while it loops
+//    over query tiles (the reference's key-outer loop, flash.py:360-365);
+//  * Q role:  CTA = (head, 128-query tile); dQ stationary while it loops over
+//    key tiles, recomputing S, P, dP, dS (dQ does not need P^F).
+// Both run in one launch (attn_bwd_kernel). Each CTA: compute warps (thread =
+// query row x KPT keys, Cfg<D>), one producer warp (1-D bulk copies of
+// pre-tiled operands), one MMA warp (warp-uniform schedule; one elected lane
+// issues tcgen05.cp / mma / commit).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -35,10 +36,35 @@ namespace aq {
 
 namespace bwd {
 
-constexpr int NCW = 8;                       // compute warps
-constexpr int NUM_THREADS = 32 * (NCW + 2);
-constexpr int PRODUCER = NCW, MMA = NCW + 1;
-constexpr int HALF = TILE / 2;               // keys per compute thread
+// Compute warps: 4 TMEM row groups x NKG key groups. 16 warps hide more
+// latency but cap registers at 96/thread: d=64 gains 9%, d=128 loses 2%
+// (spills), so the count is per head dim.
+template <int D>
+struct Cfg {
+  static constexpr int NCW = D == 64 ? 16 : 8;
+  static constexpr int NKG = NCW / 4;
+  static constexpr int KPT = TILE / NKG;     // keys per compute thread
+  static constexpr int NUM_THREADS = 32 * (NCW + 2);
+  static constexpr int PRODUCER = NCW, MMA = NCW + 1;
+};
+constexpr int HALF = TILE / 2;               // dP half width of the KV kernel
+
+// N consecutive fp32 columns of this warp's TMEM lanes
+template <int N>
+__device__ __forceinline__ void tmem_load_f(uint32_t taddr, float* v) {
+  if constexpr (N % 32 == 0) {
+#pragma unroll
+    for (int c = 0; c < N; c += 32) tmem_ld32f(taddr + c, v + c);
+    tmem_ld_wait();
+  } else {
+    static_assert(N == 16, "TMEM load width");
+    uint32_t r[16];
+    tmem_ld16(taddr, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+  }
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -71,11 +97,12 @@ __device__ __forceinline__ void store_run(void* dst, int64_t base, int dt, const
   }
 }
 
-// dS = (dP - D) . P / sqrt(d) for a 64-key run -> bf16 [query][key] T8x8
+// dS = (dP - D) . P / sqrt(d) for a KPT-key run -> bf16 [query][key] T8x8
+template <int KPT>
 __device__ __forceinline__ void store_ds(uint8_t* ds_h, int row, int kb, const float* dp, const float* pr, float Dq,
                                          float inv_sqrt_d) {
 #pragma unroll
-  for (int c8 = 0; c8 < HALF; c8 += 8) {
+  for (int c8 = 0; c8 < KPT; c8 += 8) {
     float ds[8];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
@@ -126,6 +153,8 @@ enum KvBar {
 template <int D>
 __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head) {
   using L = KvSmem<D>;
+  constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
+  constexpr int PRODUCER = Cfg<D>::PRODUCER, MMA = Cfg<D>::MMA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BARS);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::TMEM_SLOT);
   const int warp = threadIdx.x / 32;
@@ -150,7 +179,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       mbar_init(&bars[KV_B_DO_FULL + s], 1);
       mbar_init(&bars[KV_B_DO_EMPTY + s], 1);
       mbar_init(&bars[KV_B_DP_FULL + s], 1);
-      mbar_init(&bars[KV_B_DP_EMPTY + s], 128);
+      mbar_init(&bars[KV_B_DP_EMPTY + s], 32 * NCW / 2);
     }
     mbar_init(&bars[KV_B_QH_FULL], 1);
     mbar_init(&bars[KV_B_QH_EMPTY], 1);
@@ -307,8 +336,9 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   } else {
     // ------------------------------------------------------------ compute warps
     const int row = 32 * (warp & 3) + lane;
-    const int half = warp >> 2;
-    const int kb = half * HALF;   // first key (in tile) of this thread
+    const int kg = warp >> 2;
+    const int kb = kg * KPT;      // first key (in tile) of this thread
+    const int dph = kb / HALF;    // dP half holding those keys
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
     uint8_t* p_h = smem + L::P_H;
@@ -322,24 +352,22 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       int64_t kmax = p.n_k - 1;
       if (p.causal) kmax = min(kmax, q + offset);
       const int64_t lim = qvalid ? kmax - (k0 + kb) : -1;  // visible keys: c <= lim
-      float pr[HALF];
+      float pr[KPT];
       mbar_wait(&bars[KV_B_S_FULL], ph);
       tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += 32) tmem_ld32f(t_lane + KV_T_S + kb + c0, pr + c0);
-      tmem_ld_wait();
+      tmem_load_f<KPT>(t_lane + KV_T_S + kb, pr);
       tc_fence_before();
       mbar_arrive(&bars[KV_B_S_EMPTY]);
       // P = exp(S - L) exactly as the forward computes it
-      p_from_s<HALF / 2>(pr, kb, sl2, L2);
-      if (lim < HALF - 1) {
+      p_from_s<KPT / 2>(pr, kb, sl2, L2);
+      if (lim < KPT - 1) {
 #pragma unroll
-        for (int c = 0; c < HALF; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
+        for (int c = 0; c < KPT; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
       if (ii > 0) mbar_wait(&bars[KV_B_PF_FREE], (ii - 1) & 1);
       // P^F (or P) -> bf16 [query][key] T8x8
 #pragma unroll
-      for (int blk = 0; blk < HALF / 16; ++blk) {
+      for (int blk = 0; blk < KPT / 16; ++blk) {
         uint4 w[2];
         if (p.fq_p) {
           const PBlock qb = quantize_p16(pr + blk * 16);
@@ -371,39 +399,34 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       fence_async_smem();
       mbar_arrive(&bars[KV_B_PF_FULL]);
       // dS = (dP - D) . P / sqrt(d) -> bf16
-      mbar_wait(&bars[KV_B_DP_FULL + half], ph);
+      mbar_wait(&bars[KV_B_DP_FULL + dph], ph);
       tc_fence_after();
-      float dp[HALF];
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += 32) tmem_ld32f(t_lane + KV_T_DP + c0, dp + c0);
-      tmem_ld_wait();
+      float dp[KPT];
+      tmem_load_f<KPT>(t_lane + KV_T_DP + kb % HALF, dp);
       tc_fence_before();
-      mbar_arrive(&bars[KV_B_DP_EMPTY + half]);
+      mbar_arrive(&bars[KV_B_DP_EMPTY + dph]);
       if (ii > 0) mbar_wait(&bars[KV_B_DS_FREE], (ii - 1) & 1);
-      store_ds(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
+      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
       fence_async_smem();
       mbar_arrive(&bars[KV_B_DS_FULL]);
     }
-    // epilogue: dK, dV rows (thread = key row, d/2 columns)
+    // epilogue: dK, dV rows (thread = key row, D/NKG columns)
     if (ni > 0) {
       mbar_wait(&bars[KV_B_DONE], 0);
       tc_fence_after();
     }
     const int64_t key = k0 + row;
-    constexpr int DH = D / 2;
+    constexpr int DH = D / NKG;
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       float g[DH];
       if (ni > 0) {
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32)
-          tmem_ld32f(t_lane + (which ? KV_T_DV : KV_T_DK) + half * DH + c0, g + c0);
-        tmem_ld_wait();
+        tmem_load_f<DH>(t_lane + (which ? KV_T_DV : KV_T_DK) + kg * DH, g);
       } else {
 #pragma unroll
         for (int e = 0; e < DH; ++e) g[e] = 0.f;  // no visible query: zero gradient
       }
-      if (key < p.n_k) store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + half * DH, p.g_dt, g);
+      if (key < p.n_k) store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + kg * DH, p.g_dt, g);
     }
   }
 
@@ -449,6 +472,8 @@ enum QBar {
 template <int D>
 __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, int qt, int64_t head) {
   using L = QSmem<D>;
+  constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
+  constexpr int PRODUCER = Cfg<D>::PRODUCER, MMA = Cfg<D>::MMA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BARS);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::TMEM_SLOT);
   const int warp = threadIdx.x / 32;
@@ -594,8 +619,8 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
   } else {
     // ------------------------------------------------------------ compute warps
     const int row = 32 * (warp & 3) + lane;
-    const int half = warp >> 2;
-    const int kb = half * HALF;
+    const int kg = warp >> 2;
+    const int kb = kg * KPT;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
     const int64_t q = q0 + row;
@@ -608,48 +633,42 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     for (int j = 0; j < nt; ++j) {
       const uint32_t ph = j & 1;
       const int64_t lim = qvalid ? kmax - (static_cast<int64_t>(j) * TILE + kb) : -1;
-      float pr[HALF];
+      float pr[KPT];
       mbar_wait(&bars[Q_B_S_FULL], ph);
       tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += 32) tmem_ld32f(t_lane + Q_T_S + kb + c0, pr + c0);
-      tmem_ld_wait();
+      tmem_load_f<KPT>(t_lane + Q_T_S + kb, pr);
       tc_fence_before();
       mbar_arrive(&bars[Q_B_S_EMPTY]);
-      p_from_s<HALF / 2>(pr, kb, sl2, L2);
-      if (lim < HALF - 1) {
+      p_from_s<KPT / 2>(pr, kb, sl2, L2);
+      if (lim < KPT - 1) {
 #pragma unroll
-        for (int c = 0; c < HALF; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
+        for (int c = 0; c < KPT; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
       mbar_wait(&bars[Q_B_DP_FULL], ph);
       tc_fence_after();
-      float dp[HALF];
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += 32) tmem_ld32f(t_lane + Q_T_DP + kb + c0, dp + c0);
-      tmem_ld_wait();
+      float dp[KPT];
+      tmem_load_f<KPT>(t_lane + Q_T_DP + kb, dp);
       tc_fence_before();
       mbar_arrive(&bars[Q_B_DP_EMPTY]);
       if (j > 0) mbar_wait(&bars[Q_B_DS_EMPTY], (j - 1) & 1);
-      store_ds(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
+      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
       fence_async_smem();
       mbar_arrive(&bars[Q_B_DS_FULL]);
     }
-    // epilogue: dQ rows (thread = query row, d/2 columns), written once in the output dtype
+    // epilogue: dQ rows (thread = query row, D/NKG columns), written once in the output dtype
     if (nt > 0) {
       mbar_wait(&bars[Q_B_DONE], 0);
       tc_fence_after();
     }
-    constexpr int DH = D / 2;
+    constexpr int DH = D / NKG;
     float g[DH];
     if (nt > 0) {
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) tmem_ld32f(t_lane + Q_T_DQ + half * DH + c0, g + c0);
-      tmem_ld_wait();
+      tmem_load_f<DH>(t_lane + Q_T_DQ + kg * DH, g);
     } else {
 #pragma unroll
       for (int e = 0; e < DH; ++e) g[e] = 0.f;
     }
-    if (qvalid) store_run<DH>(p.dq, (head * p.n_q + q) * D + half * DH, p.g_dt, g);
+    if (qvalid) store_run<DH>(p.dq, (head * p.n_q + q) * D + kg * DH, p.g_dt, g);
   }
 
   tc_fence_before();
@@ -667,7 +686,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 // one head run together and share its operands in L2 (head-fastest order
 // is 18% slower at C4); KV and Q items share no barriers.
 template <int D>
-__global__ void __launch_bounds__(NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
+__global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t head = blockIdx.y;
   const int r = blockIdx.x;
@@ -739,7 +758,7 @@ cudaError_t launch(const BwdParams& p, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int kv_tiles = static_cast<int>(ceil_div(p.n_k, TILE)), q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
-  kern<<<dim3(static_cast<unsigned>(kv_tiles + q_tiles), static_cast<unsigned>(p.heads)), NUM_THREADS, smem, st>>>(
+  kern<<<dim3(static_cast<unsigned>(kv_tiles + q_tiles), static_cast<unsigned>(p.heads)), Cfg<D>::NUM_THREADS, smem, st>>>(
       p, kv_tiles, q_tiles);
   return cudaGetLastError();
 }
