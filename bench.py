@@ -125,7 +125,14 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU reference
 
 def _cpu_head(args):
-    n, d, causal, mode, seed = args
+    # one BLAS thread per worker: the pool already runs one head per core, and
+    # nested BLAS threads oversubscribe the host (100x slower backward)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return _cpu_head_body(*args)
+
+
+def _cpu_head_body(n, d, causal, mode, seed):
     from oracle import nvfp4_attn_oracle as orc
     rng = np.random.default_rng(seed)
     Q, K, V = (rng.standard_normal((n, d)).astype(np.float32).astype(np.float64) for _ in range(3))
@@ -160,7 +167,7 @@ class CpuReference:
         return flops / dt / 1e12, dt
 
     def sample(self):
-        s = f"{self.cores} heads (one per process) of N={self.n} d={self.d} {'causal' if self.causal else 'non-causal'}"
+        s = f"{self.cores} heads (one per process, 1 BLAS thread each) of N={self.n} d={self.d} {'causal' if self.causal else 'non-causal'}"
         s += " inference fwd" if self.mode == "fwd" else " training fwd+bwd"
         if self.n != self.N:
             s += f"; N={self.N} extrapolated from N={self.n} (N^2 scaling is already in the FLOP count)"
@@ -274,7 +281,7 @@ def main():
                 t_.grad = None
             out = aq.attn_qat(qg, kg, vg, causal=causal)
             out.backward(d_o)
-        launches_per_step = 4 + 3      # fwd (3 quantizers + attention) + bwd pre, bwd, dq convert
+        launches_per_step = 4 + 2      # fwd (3 quantizers + attention) + bwd pre, fused bwd (dK/dV + dQ roles)
 
     def barrier():
         if world > 1:
@@ -318,7 +325,7 @@ def main():
         k1.synchronize()
         kms = k0.elapsed_time(k1) / reps
         achieved = alg_flops(B, H, N, d, causal, "fwd") / (kms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "attn_fwd_kernel<128,false>", "achieved": achieved,
+        roof = {"bound": "tensor", "kernel": "attn_fwd_infer_kernel<128>", "achieved": achieved,
                 "peak": peaks["nvfp4"], "unit": "TFLOP/s", "frac": achieved / peaks["nvfp4"],
                 "peak_source": "measured live: tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak)",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,

@@ -10,7 +10,7 @@ ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c
     python scripts/time_fwd.py 0 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c 1 -o gpurun_out/prof/attn_fwd_train_c4 \
     python scripts/time_fwd.py 2 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:attn_bwd -s 1 -c 1 -o gpurun_out/prof/attn_bwd_c4 \
+ncu --set full --clock-control none --import-source on -k regex:attn_bwd_kernel -s 1 -c 1 -o gpurun_out/prof/attn_bwd_c4 \
     python scripts/time_bwd.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:quantize -s 2 -c 3 -o gpurun_out/prof/quantize_c2 \
     python scripts/time_quant.py > /dev/null 2>&1

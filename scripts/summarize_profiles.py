@@ -34,7 +34,7 @@ for cfg in ("c2", "c4"):
         fh.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none, bench.py --config {cfg} "
                  "--steps 2 --warmup 3 (cold-cache, serialised launches)\n")
         ours = [(k, t) for k, t in ls if any(s in k for s in ("attn_", "quantize", "bwd_pre", "dq_convert"))]
-        per_step = {"c2": 4, "c4": 7}[cfg]
+        per_step = {"c2": 4, "c4": 6}[cfg]
         tot = sum(t for _, t in ours[-per_step:]) or 1
         for k, t in ls:
             fh.write(f"{t:12.1f} us  {k[:110]}\n")
