@@ -338,58 +338,61 @@ def main():
                 "mixed_ceiling_frac": value / world / (1.17 * peaks["bf16"]),
                 "traffic": _traffic_from_profiles(args.config)}
 
-    # ---- end to end through the public API with host buffers
+    # ---- end to end through the public API with host buffers: pinned host
+    # inputs in, host outputs back, every step; the host entry points stream
+    # head chunks so H2D, kernels and D2H overlap (paper_2603_00040_b200/host.py)
     e2e = None
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
     if mode == "fwd":
-        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
         ho = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
+        hl = torch.empty(B, H, N, dtype=torch.float32).pin_memory()
 
         def e2e_step():
-            dq_, dk_, dv_ = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
-            out, _, _, _ = aq.attn_forward(dq_, dk_, dv_, causal=causal, train=False, workspace=ws)
-            ho.copy_(out, non_blocking=True)
-        for _ in range(2):
-            e2e_step()
-        barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(st)
-        for _ in range(args.steps):
-            e2e_step()
-        a1.record(st)
-        barrier()
-        ems = a0.elapsed_time(a1) / args.steps
-        et = torch.tensor([ems], device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * flops_rank / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": o.numel() * 2,
-               "ms_per_step": float(et.item())}
+            aq.attn_forward_host(hq, hk, hv, causal=causal, train=False, out=ho, lse_out=hl)
+        h2d_b, d2h_b = 3 * q.numel() * 2, ho.numel() * 2 + hl.numel() * 4
     else:
-        hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, d_o))
+        hdo = d_o.cpu().pin_memory()
+        ho = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
         hg = [torch.empty_like(h).pin_memory() for h in (hq, hk, hv)]
 
         def e2e_step():
-            tq, tk, tv = (h.to(dev, non_blocking=True).requires_grad_() for h in (hq, hk, hv))
-            out = aq.attn_qat(tq, tk, tv, causal=causal)
-            out.backward(hdo.to(dev, non_blocking=True))
-            for h, g in zip(hg, (tq.grad, tk.grad, tv.grad)):
-                h.copy_(g, non_blocking=True)
-        for _ in range(2):
+            aq.attn_qat_host(hq, hk, hv, hdo, causal=causal, out=ho, grads_out=hg)
+        h2d_b, d2h_b = 4 * q.numel() * 2, 4 * q.numel() * 2
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    if os.environ.get("AQ_E2E_DEBUG"):
+        for i in range(4):
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            b0.record(st)
             e2e_step()
-        barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(st)
-        for _ in range(args.steps):
+            t1 = time.perf_counter()
+            b1.record(st)
+            barrier()
+            print(f"e2e debug step {i}: {b0.elapsed_time(b1):.2f} ms device, host enqueue {1e3*(t1-t0):.2f} ms",
+                  file=sys.stderr)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
+        evs[0].record(st)
+        for i in range(10):
             e2e_step()
-        a1.record(st)
+            evs[i + 1].record(st)
         barrier()
-        ems = a0.elapsed_time(a1) / args.steps
-        et = torch.tensor([ems], device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * flops_rank / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": 4 * q.numel() * 2, "d2h_bytes_per_step": 3 * q.numel() * 2,
-               "ms_per_step": float(et.item())}
+        print("back-to-back:", [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(10)], file=sys.stderr)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(st)
+    for _ in range(args.steps):
+        e2e_step()
+    a1.record(st)
+    barrier()
+    ems = a0.elapsed_time(a1) / args.steps
+    et = torch.tensor([ems], device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * flops_rank / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "ms_per_step": float(et.item()),
+           "api": "attn_forward_host (inference)" if mode == "fwd" else "attn_qat_host (fwd+bwd)",
+           "pcie_gbs": (h2d_b + d2h_b) / (float(et.item()) * 1e-3) / 1e9}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -11,7 +11,7 @@ from .codec import (MXFP4, NVFP4, BlockSpec, QuantTensor, ScaleFormat, dequantiz
                     fake_quantize_cols, fake_quantize_padded, quantize, quantize_cols, quantize_padded)
 from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, ShapeError, StabilityError,
                      TileError)
-from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward,
-                    flash_backward, flash_forward_inference, flash_forward_training)
+from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward, attn_forward_host,
+                    attn_qat_host, flash_backward, flash_forward_inference, flash_forward_training)
 
 __version__ = "0.1.0"

@@ -25,6 +25,10 @@
 #include "pquant.cuh"
 #include "ptx.cuh"
 
+#ifndef AQ_FWDI_QSLOTS
+#define AQ_FWDI_QSLOTS 2
+#endif
+
 namespace aq {
 namespace fwdi {
 
@@ -37,32 +41,35 @@ struct Cfg {
                        MMA_B = MMA_A + 1;
   static constexpr int NUM_THREADS = 32 * (MMA_B + 1);
   static constexpr int NSA = 4, NSB = 3, NP = 2;     // ring depths
+  static constexpr int NQ = AQ_FWDI_QSLOTS;           // Q slots: how far pass 1 may run ahead of pass 2
   // TMEM
   static constexpr uint32_t T_SA = 0, T_SB = 128, T_O = 256;
-  static constexpr uint32_t T_QSF = 384, T_KSFA = T_QSF + 16, T_KSFB = T_KSFA + 8 * NSA, T_PSF = T_KSFB + 8 * NSB,
+  static constexpr uint32_t T_QSF = 384, T_KSFA = T_QSF + 8 * NQ, T_KSFB = T_KSFA + 8 * NSA, T_PSF = T_KSFB + 8 * NSB,
                             T_VSF = T_PSF + 8 * NP;
   // SMEM
   static constexpr int QC_BYTES = TILE * D / 2, QSF_BYTES = (D / 64) * 512, Q_BYTES = QC_BYTES + QSF_BYTES;
-  static constexpr int Q0 = 0;                                    // 2 Q slots
-  static constexpr int KA0 = Q0 + 2 * Q_BYTES;                    // ring A: K codes + SF
+  static constexpr int Q0 = 0;                                    // NQ Q slots
+  static constexpr int KA0 = Q0 + NQ * Q_BYTES;                   // ring A: K codes + SF
   static constexpr int KA_BYTES = QC_BYTES + QSF_BYTES;
   static constexpr int KB0 = KA0 + NSA * KA_BYTES;                // ring B: K + V^T codes + SF
   static constexpr int KB_V = KA_BYTES, KB_VSF = KB_V + TILE * D / 2, KB_BYTES = KB_VSF + 1024;
   static constexpr int P0 = KB0 + NSB * KB_BYTES;                 // P^F codes + SF
   static constexpr int PB_SF = TILE * TILE / 2, P_BYTES = PB_SF + 1024;
   static constexpr int ML = P0 + NP * P_BYTES;                    // pass-1 (m, l) partials [CS][2][TILE]
-  static constexpr int LB = ML + CS * 2 * TILE * 4;               // L handoff [2][TILE]
-  static constexpr int BARS = LB + 2 * TILE * 4;
+  static constexpr int LB = ML + CS * 2 * TILE * 4;               // L handoff [NQ][TILE]
+  static constexpr int BARS = LB + NQ * TILE * 4;
   static constexpr int NUM_BARS = 48;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int USED = TMEM_SLOT + 16;
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
   // barriers
-  static constexpr int B_Q_FULL = 0, B_Q_EMPTY = 2, B_L_FULL = 4, B_L_EMPTY = 6, B_QSF = 40, B_O_FULL = 8, B_O_EMPTY = 9,
-                       B_SA_FULL = 10, B_SA_EMPTY = 11, B_SB_FULL = 12, B_SB_EMPTY = 13, B_KA_FULL = 14,
-                       B_KA_EMPTY = B_KA_FULL + NSA, B_KB_FULL = B_KA_EMPTY + NSA, B_KB_EMPTY = B_KB_FULL + NSB,
-                       B_P_FULL = B_KB_EMPTY + NSB, B_P_EMPTY = B_P_FULL + NP, B_END = B_P_EMPTY + NP;
-  static_assert(B_END <= B_QSF && B_QSF + 2 <= NUM_BARS, "barriers");
+  static constexpr int B_Q_FULL = 0, B_Q_EMPTY = NQ, B_L_FULL = 2 * NQ, B_L_EMPTY = 3 * NQ, B_QSF = 4 * NQ,
+                       B_O_FULL = 5 * NQ, B_O_EMPTY = B_O_FULL + 1, B_SA_FULL = B_O_EMPTY + 1,
+                       B_SA_EMPTY = B_SA_FULL + 1, B_SB_FULL = B_SA_EMPTY + 1, B_SB_EMPTY = B_SB_FULL + 1,
+                       B_KA_FULL = B_SB_EMPTY + 1, B_KA_EMPTY = B_KA_FULL + NSA, B_KB_FULL = B_KA_EMPTY + NSA,
+                       B_KB_EMPTY = B_KB_FULL + NSB, B_P_FULL = B_KB_EMPTY + NSB, B_P_EMPTY = B_P_FULL + NP,
+                       B_END = B_P_EMPTY + NP;
+  static_assert(B_END <= NUM_BARS, "barriers");
   static_assert(USED <= 227 * 1024, "shared memory");
   static_assert(T_VSF + 8 * NSB <= 512, "TMEM columns");
 };
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   constexpr int GRP = 32 * C::NSW;  // threads per softmax group
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NQ; ++s) {
       mbar_init(&bars[C::B_Q_FULL + s], 1);
       mbar_init(&bars[C::B_Q_EMPTY + s], 1);
       mbar_init(&bars[C::B_L_FULL + s], GRP);
@@ -147,8 +154,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     int it = 0, k = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const Item item = work_item(p, w, q_tiles, k_tiles);
-      const int qs = k & 1;
-      if (k >= 2) mbar_wait(&bars[C::B_Q_EMPTY + qs], ((k >> 1) - 1) & 1);
+      const int qs = k % C::NQ;
+      if (k >= C::NQ) mbar_wait(&bars[C::B_Q_EMPTY + qs], ((k / C::NQ) - 1) & 1);
       const int64_t qidx = item.head * q_tiles + item.qt;
       if (elect_one()) {
         uint64_t* fb = &bars[C::B_Q_FULL + qs];
@@ -197,9 +204,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     int it = 0, k = 0, su = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
-      const int qs = k & 1;
+      const int qs = k % C::NQ;
       const uint32_t qb = s0 + C::Q0 + qs * C::Q_BYTES;
-      mbar_wait(&bars[C::B_Q_FULL + qs], (k >> 1) & 1);
+      mbar_wait(&bars[C::B_Q_FULL + qs], (k / C::NQ) & 1);
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < D / 64; ++ks)
@@ -233,10 +240,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     int it = 0, k = 0, su = 0, pc = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
-      const int qs = k & 1;
+      const int qs = k % C::NQ;
       const uint32_t qb = s0 + C::Q0 + qs * C::Q_BYTES;
       // the Q slot and its TMEM scale factors were staged by MMA A
-      mbar_wait(&bars[C::B_QSF + qs], (k >> 1) & 1);
+      mbar_wait(&bars[C::B_QSF + qs], (k / C::NQ) & 1);
       tc_fence_after();
       for (int ns = 0, np = 0; np < nt;) {
         if (ns < nt && ns <= np + 1) {
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
       int64_t kmax = p.n_k - 1;
       if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
-      const int qs = k & 1;
+      const int qs = k % C::NQ;
       if (grp_a) {
         // ---------------- pass 1: online (m, l) over this thread's 64 columns
         // (log2 domain). Same code and merge order as the CS=2 column split of
@@ -339,7 +346,11 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             for (int i = 0; i < CW / 2; ++i) {
               const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
                                           make_float2(-base, -base));
+#ifdef AQ_DBG_NOEXP1
+              const float2 e = t;
+#else
               const float2 e = use_poly_p1(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+#endif
               acc[i & 3] = __fadd2_rn(acc[i & 3], e);
             }
             const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
@@ -376,12 +387,12 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         // rebuilds L2 = fl(L) * log2(e) exactly like the backward does
         const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
         if (half == 0 && grow < p.n_q) p.lse[item.head * p.n_q + grow] = L_nat;
-        if (k >= 2) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k >> 1) - 1) & 1);
+        if (k >= C::NQ) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k / C::NQ) - 1) & 1);
         if (half == 0) lb[qs * TILE + row] = L_nat;
         mbar_arrive(&bars[C::B_L_FULL + qs]);
       } else {
         // ---------------- pass 2: P, P^F, O
-        mbar_wait(&bars[C::B_L_FULL + qs], (k >> 1) & 1);
+        mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
         const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
         mbar_arrive(&bars[C::B_L_EMPTY + qs]);
         for (int jj = 0; jj < nt; ++jj) {
@@ -394,7 +405,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           tc_fence_before();
           mbar_arrive(&bars[C::B_SB_EMPTY]);
           const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+#ifndef AQ_DBG_NOEXP2
           p_from_s<CW / 2>(x, cbase, sl2, L2);
+#endif
           if (lim < CW - 1) {
 #pragma unroll
             for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
@@ -409,8 +422,14 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
 #pragma unroll
           for (int blk = 0; blk < CW / 16; blk += 2) {
+#ifdef AQ_DBG_NOQ2
+            PBlock qa, qb;
+            qa.scale = __float_as_uint(x[blk * 16]) & 0xff; qa.codes[0] = __float_as_uint(x[blk * 16 + 1]); qa.codes[1] = __float_as_uint(x[blk * 16 + 2]);
+            qb = qa;
+#else
             const PBlock qa = quantize_p16(x + blk * 16);
             const PBlock qb = quantize_p16(x + blk * 16 + 16);
+#endif
             *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
                 make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
             scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));

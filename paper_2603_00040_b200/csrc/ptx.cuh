@@ -30,8 +30,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef AQ_WAIT_MODE
+#define AQ_WAIT_MODE 2
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if AQ_WAIT_MODE == 2
+  // no suspend-time hint: the hardware's default time limit
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#elif AQ_WAIT_MODE == 3
+  // non-blocking probe (busy spin)
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#else
   // suspend-time hint (ns): a waiting warp sleeps until the phase completes
   // (or the hint elapses) instead of re-issuing the probe, so idle waiters do
   // not steal issue slots from the softmax warps on the same SMSP
@@ -42,14 +64,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
       : "memory");
+#endif
   return ok != 0;
 }
 // Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// The first probe is inline; the retry loop (and its trap counter) only runs
+// when the phase is not complete yet, so the common case costs one TRYWAIT.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins == (1u << 22)) __trap();
   }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if AQ_WAIT_MODE == 0
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins == (1u << 22)) __trap();
+  }
+#elif AQ_WAIT_MODE == 1
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#else
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+#endif
 }
 
 // ---------------------------------------------------------------- bulk copy

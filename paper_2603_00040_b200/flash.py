@@ -23,6 +23,7 @@ import torch
 
 from . import _lib
 from .codec import NVFP4, BlockSpec, to_device
+from .host import default_chunk, run_pipelined
 from .errors import InvalidValue, MissingOPrime, ShapeError, TileError
 
 
@@ -97,7 +98,7 @@ def _heads_view(t):
 
 
 def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd=False, lse_out=None,
-                 workspace=None, operands_staged=False, out=None):
+                 workspace=None, operands_staged=False, out=None, o_hp_out=None):
     """Fused forward on CUDA tensors [..., N, d] -> (O, L, O_hp or None, workspace).
 
     ``train=True`` is flash_forward_training (O, L, O'), ``False`` is
@@ -132,7 +133,9 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
             raise InvalidValue("operands_staged needs the workspace that holds them")
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
     o = out if out is not None else torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
-    o_hp = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device) if train else None
+    o_hp = None
+    if train:
+        o_hp = o_hp_out if o_hp_out is not None else torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
     lse = lse_out if lse_out is not None else torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
     args = _lib.AqFwdArgs(
         q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
@@ -148,7 +151,7 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
 
 
 def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.CORRECT, grad_dtype=None,
-                  fwd_workspace=None):
+                  fwd_workspace=None, workspace=None, grads_out=None):
     """Fused QAT backward on CUDA tensors -> (dQ, dK, dV) (flash.py:317-390)."""
     _lib.require_cuda()
     q3, n_q, d = _heads_view(q)
@@ -166,10 +169,21 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
         raise ShapeError("outs.L has the wrong shape")
     grad_dtype = grad_dtype or q.dtype
     lib = _lib.load()
-    ws = torch.empty(lib.aq_attn_bwd_workspace_bytes(heads, n_q, n_k, d), dtype=torch.uint8, device=q.device)
-    dq = torch.empty((heads, n_q, d), dtype=grad_dtype, device=q.device)
-    dk = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
-    dv = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
+    ws_bytes = lib.aq_attn_bwd_workspace_bytes(heads, n_q, n_k, d)
+    if workspace is not None:
+        if workspace.numel() < ws_bytes:
+            raise ShapeError("backward workspace too small")
+        ws = workspace
+    else:
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    if grads_out is not None:
+        dq, dk, dv = (g.reshape(heads, -1, d) for g in grads_out)
+        if dq.dtype != grad_dtype or dk.dtype != grad_dtype or dv.dtype != grad_dtype:
+            raise InvalidValue("grads_out dtypes must match grad_dtype")
+    else:
+        dq = torch.empty((heads, n_q, d), dtype=grad_dtype, device=q.device)
+        dk = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
+        dv = torch.empty((heads, n_k, d), dtype=grad_dtype, device=q.device)
     d_o3 = d_o.reshape(heads, n_q, d).contiguous()
     o_c = o.reshape(heads, n_q, d).contiguous() if o is not None else None
     o_hp_c = o_hp.reshape(heads, n_q, d).contiguous() if o_hp is not None else None
@@ -189,6 +203,97 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
     _lib.check(lib.aq_attn_bwd(args, _lib.stream_ptr()))
     return (dq.reshape(q.shape[:-2] + (n_q, d)), dk.reshape(k.shape[:-2] + (n_k, d)),
             dv.reshape(v.shape[:-2] + (n_k, d)))
+
+
+# ----------------------------------------------------------------------------
+# host-buffer entry points (the reference's host-in / host-out contract, with
+# H2D, kernels and D2H overlapped across head chunks -- host.py)
+# ----------------------------------------------------------------------------
+
+def _host_heads(t):
+    if t.device.type != "cpu":
+        raise InvalidValue("host entry points take CPU tensors (pinned for overlapped copies)")
+    return _heads_view(t)
+
+
+def _host_empty(shape, dtype, like=None):
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def attn_forward_host(q, k, v, causal=False, train=False, out=None, lse_out=None, o_hp_out=None,
+                      out_dtype=None, chunk_heads=None):
+    """Forward from host tensors [..., N, d] into host outputs -> (O, L, O' or None).
+
+    Same math as ``attn_forward`` (train selects flash_forward_training vs
+    flash_forward_inference); the head axis is streamed through the GPU in
+    chunks so uploads, kernels and downloads overlap."""
+    _lib.require_cuda()
+    q3, n_q, d = _host_heads(q)
+    k3, n_k, _ = _host_heads(k)
+    v3, _, _ = _host_heads(v)
+    heads = q3.shape[0]
+    out_dtype = out_dtype or q.dtype
+    o = out.reshape(heads, n_q, d) if out is not None else _host_empty((heads, n_q, d), out_dtype)
+    lse = lse_out.reshape(heads, n_q) if lse_out is not None else _host_empty((heads, n_q), torch.float32)
+    outs = [o, lse]
+    if train:
+        o_hp = o_hp_out.reshape(heads, n_q, d) if o_hp_out is not None else _host_empty((heads, n_q, d), out_dtype)
+        outs.append(o_hp)
+    per_head = (q3[0].numel() + 2 * k3[0].numel()) * q3.element_size()
+    chunk = chunk_heads or default_chunk(heads, per_head)
+    lib = _lib.load()
+    ws_bytes = lambda h: (lib.aq_attn_fwd_workspace_bytes(h, n_q, n_k, d, int(train), 0),)  # noqa: E731
+    if ws_bytes(1)[0] <= 0:
+        raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
+
+    def fn(dev, res, scr):
+        attn_forward(dev[0], dev[1], dev[2], causal=causal, train=train, out_dtype=out_dtype, out=res[0],
+                     lse_out=res[1], o_hp_out=res[2] if train else None, workspace=scr[0])
+    run_pipelined(fn, [q3, k3, v3], outs, chunk, scratch=[("fwd_ws", ws_bytes, torch.uint8)])
+    lead = q.shape[:-2]
+    return (o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q),
+            outs[2].reshape(*lead, n_q, d) if train else None)
+
+
+def attn_qat_host(q, k, v, d_o, causal=False, variant=BwdVariant.CORRECT, out=None, grads_out=None,
+                  chunk_heads=None):
+    """One QAT attention training step from host tensors: forward (O, O', L) and
+    backward (dQ, dK, dV) per head chunk, H2D / kernels / D2H overlapped.
+    Returns (O, dQ, dK, dV) in host memory."""
+    _lib.require_cuda()
+    q3, n_q, d = _host_heads(q)
+    k3, n_k, _ = _host_heads(k)
+    v3, _, _ = _host_heads(v)
+    do3, _, _ = _host_heads(d_o)
+    heads = q3.shape[0]
+    dt = q.dtype
+    o = out.reshape(heads, n_q, d) if out is not None else _host_empty((heads, n_q, d), dt)
+    if grads_out is not None:
+        dq, dk, dv = (g.reshape(heads, -1, d) for g in grads_out)
+    else:
+        dq = _host_empty((heads, n_q, d), dt)
+        dk, dv = (_host_empty((heads, n_k, d), dt) for _ in range(2))
+    per_head = (2 * q3[0].numel() + 2 * k3[0].numel()) * q3.element_size()
+    chunk = chunk_heads or default_chunk(heads, per_head)
+    lib = _lib.load()
+    if lib.aq_attn_fwd_workspace_bytes(1, n_q, n_k, d, 1, 1) <= 0:
+        raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
+    scratch = [("fwd_ws", lambda h: (lib.aq_attn_fwd_workspace_bytes(h, n_q, n_k, d, 1, 1),), torch.uint8),
+               ("bwd_ws", lambda h: (lib.aq_attn_bwd_workspace_bytes(h, n_q, n_k, d),), torch.uint8),
+               ("o_hp", lambda h: (h, n_q, d), dt), ("lse", lambda h: (h, n_q), torch.float32)]
+
+    def fn(dev, res, scr):
+        qd, kd, vd, dod = dev
+        n = qd.shape[0]
+        o_hp_d, lse_d = scr[2][:n], scr[3][:n]
+        attn_forward(qd, kd, vd, causal=causal, train=True, keep_for_bwd=True, out=res[0], o_hp_out=o_hp_d,
+                     lse_out=lse_d, workspace=scr[0])
+        attn_backward(qd, kd, vd, dod, res[0], o_hp_d, lse_d, causal=causal, variant=variant, grad_dtype=dt,
+                      fwd_workspace=scr[0], workspace=scr[1], grads_out=res[1:])
+    run_pipelined(fn, [q3, k3, v3, do3], [o, dq, dk, dv], chunk, scratch=scratch)
+    lead = q.shape[:-2]
+    return (o.reshape(*lead, n_q, d), dq.reshape(*lead, n_q, d), dk.reshape(*lead, n_k, d),
+            dv.reshape(*lead, n_k, d))
 
 
 # ----------------------------------------------------------------------------
@@ -222,6 +327,15 @@ def _check_cfg(cfg, n_q, n_k, d, quantized):
         raise ShapeError("causal attention requires N_q <= N_k")
 
 
+def _is_host(x):
+    return not isinstance(x, torch.Tensor)
+
+
+def _host_f32(x):
+    """NumPy operand -> float32 CPU tensor (float64 rounds to float32, as on upload)."""
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
+
+
 def _np_out(t, as_np, dtype=np.float32):
     return t.float().cpu().numpy().astype(dtype) if as_np else t
 
@@ -230,24 +344,31 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     """Training forward: O, L and the auxiliary O' (flash.py:176-246)."""
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
     _check_cfg(cfg, n_q, n_k, d, quantized)
-    q, as_np = to_device(Q)
+    if _is_host(Q):
+        # host in, host out (the reference's contract): streamed through host.py
+        o, lse, o_hp = attn_forward_host(*(_host_f32(x) for x in (Q, K, V)), causal=cfg.causal, train=True,
+                                         out_dtype=torch.float32)
+        return AttnOutputs(O=o.numpy(), L=lse.numpy().astype(np.float64), O_prime=o_hp.numpy())
+    q, _ = to_device(Q)
     k, _ = to_device(K)
     v, _ = to_device(V)
-    out_dt = torch.float32 if as_np else None
-    o, lse, o_hp, _ = attn_forward(q, k, v, causal=cfg.causal, train=True, out_dtype=out_dt)
-    return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=_np_out(o_hp, as_np))
+    o, lse, o_hp, _ = attn_forward(q, k, v, causal=cfg.causal, train=True)
+    return AttnOutputs(O=o, L=lse, O_prime=o_hp)
 
 
 def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
     """Inference forward on real FP4 codes: O, L (flash.py:249-314)."""
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
     _check_cfg(cfg, n_q, n_k, d, True)
-    q, as_np = to_device(Q)
+    if _is_host(Q):
+        o, lse, _ = attn_forward_host(*(_host_f32(x) for x in (Q, K, V)), causal=cfg.causal, train=False,
+                                      out_dtype=torch.float32)
+        return AttnOutputs(O=o.numpy(), L=lse.numpy().astype(np.float64), O_prime=None)
+    q, _ = to_device(Q)
     k, _ = to_device(K)
     v, _ = to_device(V)
-    out_dt = torch.float32 if as_np else None
-    o, lse, _, _ = attn_forward(q, k, v, causal=cfg.causal, train=False, out_dtype=out_dt)
-    return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=None)
+    o, lse, _, _ = attn_forward(q, k, v, causal=cfg.causal, train=False)
+    return AttnOutputs(O=o, L=lse, O_prime=None)
 
 
 def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized=True, instrument=None):
