@@ -343,12 +343,22 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     const float sl2 = p.scale_log2;
     uint8_t* p_h = smem + L::P_H;
     uint8_t* ds_h = smem + L::DS_H;
+    // per-row L and D of the next query tile are loaded one tile ahead, so the
+    // global-load latency never sits between S_FULL and the exponentials
+    auto row_stats = [&](int t, float& l2, float& dq) {
+      const int64_t qq = static_cast<int64_t>(i_begin + t) * TILE + row;
+      l2 = (t < ni && qq < p.n_q) ? p.lse[head * p.n_q + qq] : 0.f;
+      dq = t < ni ? p.delta[head * (q_tiles * TILE) + qq] : 0.f;
+    };
+    float L_next, D_next;
+    row_stats(0, L_next, D_next);
     for (int ii = 0; ii < ni; ++ii) {
       const uint32_t ph = ii & 1;
       const int64_t q = static_cast<int64_t>(i_begin + ii) * TILE + row;
       const bool qvalid = q < p.n_q;
-      const float L2 = qvalid ? p.lse[head * p.n_q + q] * 1.44269504088896340736f : 0.f;
-      const float Dq = p.delta[head * (q_tiles * TILE) + q];
+      const float L2 = L_next * 1.44269504088896340736f;
+      const float Dq = D_next;
+      row_stats(ii + 1, L_next, D_next);
       int64_t kmax = p.n_k - 1;
       if (p.causal) kmax = min(kmax, q + offset);
       const int64_t lim = qvalid ? kmax - (k0 + kb) : -1;  // visible keys: c <= lim

@@ -367,18 +367,23 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
           return s4.x + s4.y;
         };
         float sum = expsum(m == -INFINITY ? 0.f : m);
-        // row max on the raw scores (the scale is positive)
-        float mx[8];
+        // A rebase needs a term above 2^8, hence sum > 240 (or inf): only then (and
+        // while no column is visible yet) is the tile max needed. Same m sequence,
+        // hence the same bits, as taking the max of every tile.
+        if (!(sum <= 240.0f) || m == -INFINITY) {
+          // row max on the raw scores (the scale is positive)
+          float mx[8];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) mx[a] = x[a];
+          for (int a = 0; a < 8; ++a) mx[a] = x[a];
 #pragma unroll
-        for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
-        const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
-        if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
-          l = (m == -INFINITY) ? 0.f : l * ex2(m - mloc);
-          m = mloc;
-          sum = expsum(m);
+          for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+          const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                   fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+          if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
+            l = (m == -INFINITY) ? 0.f : l * ex2(m - mloc);
+            m = mloc;
+            sum = expsum(m);
+          }
         }
         l += sum;
         AQ_PROF(prof_p1 += clock64() - tp1;)
