@@ -90,6 +90,17 @@ int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int
 /* Replaces flash_forward_training / flash_forward_inference (flash.py:176-314). */
 int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 
+/* FP4 KV cache: inference forward (flash_forward_inference, flash.py:249-314)
+ * over K and V already quantized in the reference QuantTensor layout -- the
+ * payload of ATQ4 files (tensors.py:173-188):
+ *   K   = quantize(K)            codes [heads][n_k][d/2],   scales [heads][n_k][d/16]
+ *   V^T = quantize_padded(V.T)   codes [heads][d][n16/2],   scales [heads][d][n16/16]
+ * (n16 = ceil(n_k/16)*16, codec.py:359-361). args->k / args->v are ignored,
+ * args->train must be 0; Q is quantized on the fly. Bit-identical to aq_attn_fwd
+ * on the K / V these caches were quantized from. */
+int aq_attn_fwd_kv4(const AqFwdArgs* args, const uint8_t* k_codes, const uint8_t* k_scales,
+                    const uint8_t* vt_codes, const uint8_t* vt_scales, void* stream);
+
 typedef struct {
   const void* q; const void* k; const void* v; /* original operands, in_dtype */
   int in_dtype;

@@ -223,6 +223,41 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   return cuda_status(launch_attn_fwd(p, st));
 }
 
+int aq_attn_fwd_kv4(const AqFwdArgs* a, const uint8_t* k_codes, const uint8_t* k_scales, const uint8_t* vt_codes,
+                    const uint8_t* vt_scales, void* stream) {
+  if (!a || !a->q || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;
+  if (!k_codes || !k_scales || !vt_codes || !vt_scales) return AQ_E_INVALID;
+  if (a->train) return AQ_E_INVALID;  // a KV cache serves inference (no O', no backward)
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->o_dtype)) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d % 16) return AQ_E_SHAPE;
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 0);
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  RowsArgs r{};
+  r.x = a->q;
+  r.x_dt = a->in_dtype;
+  r.heads = a->heads;
+  r.n = a->n_q;
+  r.cols = a->d;
+  r.ld = a->d;
+  r.hs = a->n_q * a->d;
+  r.codes_t = ws + w.q_codes;
+  r.sf_t = ws + w.q_sf;
+  if (launch_quantize_rows(r, st) != cudaSuccess) return AQ_E_CUDA;
+  if (launch_pack_kv4(k_codes, k_scales, vt_codes, vt_scales, a->heads, a->n_k, static_cast<int>(a->d),
+                      ws + w.k_codes, ws + w.k_sf, ws + w.v_codes, ws + w.v_sf, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  AqFwdArgs b = *a;
+  b.operands_staged = 1;
+  b.keep_for_bwd = 0;
+  b.k = b.q;  // unused once staged
+  b.v = b.q;
+  return aq_attn_fwd(&b, stream);
+}
+
 int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d) {
   if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128)) return 0;
   return bwd_ws(heads, n_q, n_k, d).total;

@@ -73,6 +73,9 @@ cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
+cudaError_t launch_pack_kv4(const uint8_t* k_codes, const uint8_t* k_scales, const uint8_t* vt_codes,
+                            const uint8_t* vt_scales, int64_t heads, int64_t n, int d, uint8_t* k_codes_t,
+                            uint8_t* k_sf_t, uint8_t* v_codes_t, uint8_t* v_sf_t, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
                            int d, float* delta, uint8_t* do_h, cudaStream_t st);
 
