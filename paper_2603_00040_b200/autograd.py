@@ -17,21 +17,24 @@ from .flash import BwdVariant, attn_backward, attn_forward
 
 class AttnQATFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT):
-        o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True)
+    def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True):
+        o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True, quantized=quantized)
         ctx.save_for_backward(q, k, v, o, o_hp, lse, ws)
         ctx.causal = causal
         ctx.variant = variant
+        ctx.quantized = quantized
         return o
 
     @staticmethod
     def backward(ctx, d_o):
         q, k, v, o, o_hp, lse, ws = ctx.saved_tensors
         dq, dk, dv = attn_backward(q, k, v, d_o.contiguous(), o, o_hp, lse, causal=ctx.causal,
-                                   variant=ctx.variant, grad_dtype=q.dtype, fwd_workspace=ws)
-        return dq, dk, dv, None, None
+                                   variant=ctx.variant, grad_dtype=q.dtype, fwd_workspace=ws,
+                                   quantized=ctx.quantized)
+        return dq, dk, dv, None, None, None
 
 
-def attn_qat(q, k, v, causal=False, variant=BwdVariant.CORRECT):
-    """NVFP4 QAT attention: O = softmax_fq(Q^F K^F^T / sqrt(d)) V^F with the Attn-QAT backward."""
-    return AttnQATFunction.apply(q, k, v, causal, variant)
+def attn_qat(q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True):
+    """NVFP4 QAT attention: O = softmax_fq(Q^F K^F^T / sqrt(d)) V^F with the Attn-QAT backward.
+    ``quantized=False`` is the reference's bf16 mode (plain attention, plain.py)."""
+    return AttnQATFunction.apply(q, k, v, causal, variant, quantized)

@@ -24,6 +24,7 @@ import torch
 from . import _lib
 from .codec import NVFP4, BlockSpec, to_device
 from .host import default_chunk, run_pipelined
+from .plain import plain_backward, plain_forward
 from .errors import InvalidValue, MissingOPrime, ShapeError, TileError
 
 
@@ -98,13 +99,16 @@ def _heads_view(t):
 
 
 def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd=False, lse_out=None,
-                 workspace=None, operands_staged=False, out=None, o_hp_out=None):
+                 workspace=None, operands_staged=False, out=None, o_hp_out=None, quantized=True):
     """Fused forward on CUDA tensors [..., N, d] -> (O, L, O_hp or None, workspace).
 
     ``train=True`` is flash_forward_training (O, L, O'), ``False`` is
     flash_forward_inference (O, L). O is the FP4-path output, O' the
-    high-precision output the QAT backward needs (flash.py:176-246)."""
+    high-precision output the QAT backward needs (flash.py:176-246).
+    ``quantized=False`` is plain attention (O' = O; plain.py)."""
     _lib.require_cuda()
+    if not quantized:
+        return _plain_forward(q, k, v, causal, train, out_dtype)
     q3, n_q, d = _heads_view(q)
     k3, n_k, dk = _heads_view(k)
     v3, n_v, dv = _heads_view(v)
@@ -151,7 +155,7 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
 
 
 def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.CORRECT, grad_dtype=None,
-                  fwd_workspace=None, workspace=None, grads_out=None):
+                  fwd_workspace=None, workspace=None, grads_out=None, quantized=True):
     """Fused QAT backward on CUDA tensors -> (dQ, dK, dV) (flash.py:317-390)."""
     _lib.require_cuda()
     q3, n_q, d = _heads_view(q)
@@ -168,6 +172,12 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
     if lse.numel() != heads * n_q:
         raise ShapeError("outs.L has the wrong shape")
     grad_dtype = grad_dtype or q.dtype
+    if not quantized:
+        # every variant reduces to the plain backward (flash.py:344-349, 357)
+        g = plain_backward(q3.contiguous(), k3.contiguous(), v3.contiguous(), d_o.reshape(heads, n_q, d),
+                           o_ref.reshape(heads, n_q, d), lse.reshape(heads, n_q), causal, grad_dtype)
+        return (g[0].reshape(q.shape[:-2] + (n_q, d)), g[1].reshape(k.shape[:-2] + (n_k, d)),
+                g[2].reshape(v.shape[:-2] + (n_k, d)))
     lib = _lib.load()
     ws_bytes = lib.aq_attn_bwd_workspace_bytes(heads, n_q, n_k, d)
     if workspace is not None:
@@ -203,6 +213,20 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
     _lib.check(lib.aq_attn_bwd(args, _lib.stream_ptr()))
     return (dq.reshape(q.shape[:-2] + (n_q, d)), dk.reshape(k.shape[:-2] + (n_k, d)),
             dv.reshape(v.shape[:-2] + (n_k, d)))
+
+
+def _plain_forward(q, k, v, causal, train, out_dtype):
+    q3, n_q, d = _heads_view(q)
+    k3, n_k, dk = _heads_view(k)
+    v3, n_v, dv = _heads_view(v)
+    if dk != d or dv != d or n_v != n_k or k3.shape[0] != q3.shape[0] or v3.shape[0] != q3.shape[0]:
+        raise ShapeError(f"inconsistent shapes Q{tuple(q.shape)} K{tuple(k.shape)} V{tuple(v.shape)}")
+    o, lse = plain_forward(q3.contiguous(), k3.contiguous(), v3.contiguous(), causal)
+    if out_dtype is not None:
+        o = o.to(out_dtype)
+    lead = q.shape[:-2]
+    o = o.reshape(*lead, n_q, d)
+    return o, lse.reshape(*lead, n_q), (o.clone() if train else None), None
 
 
 # ----------------------------------------------------------------------------
@@ -319,10 +343,8 @@ def _check_cfg(cfg, n_q, n_k, d, quantized):
         raise InvalidValue("the B200 path accumulates in fp32 (tensor cores); accum_width=64 is CPU-only")
     if cfg.spec != NVFP4:
         raise InvalidValue("the B200 path implements NVFP4 only")
-    if d % cfg.spec.block_size:
+    if quantized and d % cfg.spec.block_size:
         raise ShapeError("d must be a multiple of the block size when quantizing")
-    if not quantized:
-        raise InvalidValue("quantized=False (plain attention) is not implemented on the B200 path yet")
     if cfg.causal and n_q > n_k:
         raise ShapeError("causal attention requires N_q <= N_k")
 
@@ -344,6 +366,12 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     """Training forward: O, L and the auxiliary O' (flash.py:176-246)."""
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
     _check_cfg(cfg, n_q, n_k, d, quantized)
+    if not quantized:
+        q, as_np = to_device(Q)
+        k, _ = to_device(K)
+        v, _ = to_device(V)
+        o, lse, o_hp, _ = attn_forward(q, k, v, causal=cfg.causal, train=True, quantized=False)
+        return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=_np_out(o_hp, as_np))
     if _is_host(Q):
         # host in, host out (the reference's contract): streamed through host.py
         o, lse, o_hp = attn_forward_host(*(_host_f32(x) for x in (Q, K, V)), causal=cfg.causal, train=True,
@@ -390,5 +418,6 @@ def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized
     lse = to_device(outs.L)[0]
     g_dt = torch.float32 if as_np else None
     dq, dk, dv = attn_backward(q, k, v, d_o.to(q.dtype) if d_o.dtype != q.dtype and not as_np else d_o,
-                               o, o_hp, lse, causal=cfg.causal, variant=variant, grad_dtype=g_dt)
+                               o, o_hp, lse, causal=cfg.causal, variant=variant, grad_dtype=g_dt,
+                               quantized=quantized)
     return AttnGrads(dQ=_np_out(dq, as_np), dK=_np_out(dk, as_np), dV=_np_out(dv, as_np))

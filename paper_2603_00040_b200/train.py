@@ -31,12 +31,13 @@ from .autograd import attn_qat
 from .errors import InvalidValue, StabilityError
 from .flash import BwdVariant
 
-# attention modes of the reference harness (harness.py:39-45)
+# attention modes of the reference harness (harness.py:39-45): (quantized, variant)
 ATTN_MODES = {
-    "fp4-qat": BwdVariant.CORRECT,
-    "fp4-qat/lowpreco": BwdVariant.LOW_PREC_O,
-    "fp4-qat/nofqp": BwdVariant.NO_FAKE_QUANT_P,
-    "fp4-qat/naive-bf16-bwd": BwdVariant.NAIVE_BF16_BWD,
+    "bf16": (False, BwdVariant.CORRECT),
+    "fp4-qat": (True, BwdVariant.CORRECT),
+    "fp4-qat/lowpreco": (True, BwdVariant.LOW_PREC_O),
+    "fp4-qat/nofqp": (True, BwdVariant.NO_FAKE_QUANT_P),
+    "fp4-qat/naive-bf16-bwd": (True, BwdVariant.NAIVE_BF16_BWD),
 }
 TASK_COMMON_GAIN = 12.0  # harness.py:37
 DIVERGENCE_LOSS = 1e6
@@ -129,14 +130,18 @@ class AttnLayer(torch.nn.Module):
         self.n_heads, self.head_dim = n_heads, head_dim
         self.attn_fn = attn_fn or attn_qat   # tests inject a CPU reference attention
 
-    def forward(self, x, causal=False, variant=BwdVariant.CORRECT, dtype=torch.bfloat16):
+    def forward(self, x, causal=False, variant=BwdVariant.CORRECT, dtype=torch.bfloat16, quantized=True):
         B, N, _ = x.shape
         H, d = self.n_heads, self.head_dim
         xc = x.to(dtype)
 
         def proj(w):
             return (xc @ w.to(dtype)).view(B, N, H, d).transpose(1, 2)
-        o = self.attn_fn(proj(self.w_q), proj(self.w_k), proj(self.w_v), causal, variant)
+        qkv = (proj(self.w_q), proj(self.w_k), proj(self.w_v))
+        if quantized:
+            o = self.attn_fn(*qkv, causal, variant)
+        else:   # the harness's "bf16" mode: plain attention (flash.py quantized=False)
+            o = self.attn_fn(*qkv, causal, variant, False)
         o = o.transpose(1, 2).reshape(B, N, H * d)
         return o @ self.w_o.to(dtype).t()
 
@@ -183,7 +188,7 @@ def train(cfg: TrainConfig, device=None, attn_fn=None, log_every=0):
     opt = torch.optim.AdamW(layer.parameters(), lr=cfg.lr, betas=(cfg.beta1, cfg.beta2),
                             weight_decay=cfg.weight_decay)
     ar = GradAllReduce(layer.parameters(), world)
-    variant = ATTN_MODES[cfg.attn_mode]
+    quantized, variant = ATTN_MODES[cfg.attn_mode]
     log = TrainLog()
     for step in range(cfg.steps):
         t0 = time.perf_counter()
@@ -193,7 +198,7 @@ def train(cfg: TrainConfig, device=None, attn_fn=None, log_every=0):
         t = torch.from_numpy(T).to(device)
         opt.zero_grad(set_to_none=True)
         y = layer(x, cfg.causal, variant,
-                  dtype=torch.bfloat16 if cfg.compute_dtype == "bf16" else torch.float32)
+                  dtype=torch.bfloat16 if cfg.compute_dtype == "bf16" else torch.float32, quantized=quantized)
         loss = torch.mean((y[:, -1].float() - t) ** 2)
         loss.backward()
         ar.wait()
