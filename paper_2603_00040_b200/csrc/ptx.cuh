@@ -33,19 +33,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 #ifndef AQ_WAIT_MODE
 #define AQ_WAIT_MODE 2
 #endif
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+// Non-blocking probe of the phase.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
-#if AQ_WAIT_MODE == 2
-  // no suspend-time hint: the hardware's default time limit
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-#elif AQ_WAIT_MODE == 3
-  // non-blocking probe (busy spin)
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -53,23 +43,42 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
-#else
-  // suspend-time hint (ns): a waiting warp sleeps until the phase completes
-  // (or the hint elapses) instead of re-issuing the probe, so idle waiters do
-  // not steal issue slots from the softmax warps on the same SMSP
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-      : "memory");
-#endif
   return ok != 0;
 }
+// Potentially blocking probe: with a suspend-time hint (ns) a waiting warp
+// sleeps until the phase completes (or the hint elapses) instead of
+// re-issuing the probe, so idle waiters do not steal issue slots from the
+// softmax warps on the same SMSP.
+template <bool kHint>
+__device__ __forceinline__ bool mbar_try_wait_t(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  if (kHint) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  return mbar_try_wait_t<AQ_WAIT_MODE != 2>(bar, parity);
+}
 // Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
-// The first probe is inline; the retry loop (and its trap counter) only runs
-// when the phase is not complete yet, so the common case costs one TRYWAIT.
+//   mode 0: inline sleeping loop with a retry counter
+//   mode 1: inline sleeping loop, no counter (no hang protection; tuning only)
+//   mode 2: inline blocking probe, out-of-line retry loop with counter
+//   mode 5: inline non-blocking probe, out-of-line sleeping loop with counter
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
@@ -85,6 +94,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #elif AQ_WAIT_MODE == 1
   while (!mbar_try_wait(bar, parity)) {
   }
+#elif AQ_WAIT_MODE == 5
+  if (!mbar_test_wait(bar, parity)) mbar_wait_slow(bar, parity);
 #else
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 #endif
