@@ -63,9 +63,24 @@ int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64
                      int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite,
                      void* stream);
 
+/* Replaces attnqat.codec.round_to_fp4 (format 0, codec.py:76-88) and
+ * round_to_e4m3 (format 1, codec.py:101-112): one code per element of x
+ * (x_dtype 0 = fp32, 3 = fp64; exact in that precision, ties to even).
+ * *invalid is set for non-finite input (and negative input for E4M3). */
+int aq_round_codes(const void* x, int x_dtype, int64_t n, int format, uint8_t* codes, int* invalid, void* stream);
+
 /* Replaces attnqat.codec.dequantize (codec.py:327-333). rows x cols. */
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
                   int out_dtype, void* stream);
+
+/* Replaces attnqat.tensors.fp4mm (tensors.py:54-86): C = A B^T from two NVFP4
+ * QuantTensors blocked along the shared contraction axis K (K % 16 == 0):
+ * A codes [M][K/2] + scales [M][K/16], B^T codes [N][K/2] + scales [N][K/16];
+ * C [M][N] fp32 with row stride ldc. Block-scaled tcgen05 MMAs (exact block
+ * products, fp32 accumulation). workspace: aq_fp4mm_workspace_bytes(M, N, K). */
+int64_t aq_fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int aq_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
+             const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, void* workspace, void* stream);
 
 /* ---- fused attention ----------------------------------------------------- */
 typedef struct {

@@ -7,13 +7,14 @@ a C ABI); there is no CPU fallback.
 """
 
 from .autograd import AttnQATFunction, attn_qat
-from .codec import (MXFP4, NVFP4, BlockSpec, QuantTensor, ScaleFormat, dequantize, fake_quantize,
-                    fake_quantize_cols, fake_quantize_padded, quantize, quantize_cols, quantize_padded)
+from .codec import (MXFP4, NVFP4, BlockSpec, Fp4Block, QuantTensor, ScaleFormat, decode_e4m3, decode_fp4, dequantize,
+                    dequantize_block, encode_fp4, fake_quantize, fake_quantize_cols, fake_quantize_padded, quantize,
+                    quantize_block, quantize_cols, quantize_padded, round_to_e4m3, round_to_fp4)
 from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, ShapeError, StabilityError,
                      TileError)
 from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward, attn_forward_host,
                     attn_qat_host, flash_backward, flash_forward_inference, flash_forward_training)
 from .kvcache import KV4Cache, attn_forward_kv4, kv4_quantize, load_kv4, save_kv4
-from .tensors import load_quant_tensor, load_tensor, save_quant_tensor, save_tensor
+from .tensors import Rng, fp4mm, load_quant_tensor, load_tensor, matmul, randn, save_quant_tensor, save_tensor
 
 __version__ = "0.1.0"

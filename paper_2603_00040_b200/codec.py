@@ -210,3 +210,118 @@ def quantize_cols(x, spec=NVFP4) -> QuantTensor:
         _lib.ptr(codes), _lib.ptr(scales), None, 0, _lib.ptr(flag), _lib.stream_ptr()))
     _nonfinite_check(flag)
     return QuantTensor(cols, n16, spec, _out(codes, was_np), _out(scales, was_np))
+
+
+# ----------------------------------------------------------------------------
+# element-wise codes and single blocks (codec.py:63-138, 225-258)
+# ----------------------------------------------------------------------------
+
+def _round_codes(x, fmt, what):
+    was_np = not isinstance(x, torch.Tensor)
+    if was_np:
+        arr = np.asarray(x, dtype=np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1)))
+    else:
+        arr = None
+        t = x.reshape(-1)
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float32)
+    _lib.require_cuda()
+    t = t.to("cuda").contiguous()
+    codes = torch.empty(t.numel(), dtype=torch.uint8, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_round_codes(_lib.ptr(t), 3 if t.dtype == torch.float64 else 0, t.numel(), fmt,
+                                          _lib.ptr(codes), _lib.ptr(flag), _lib.stream_ptr()))
+    if int(flag.item()):
+        raise InvalidValue(f"{what} requires finite{' non-negative' if fmt == 1 else ''} input")
+    if not was_np:
+        return codes.reshape(x.shape)
+    out = codes.cpu().numpy().reshape(arr.shape)
+    return out if arr.ndim else out[()]
+
+
+def round_to_fp4(x):
+    """Nearest FP4 (E2M1) code, ties to even, saturating at +-6; -0.0 -> 0x0,
+    a small negative that rounds to zero keeps the sign (codec.py:76-88).
+    Exact in the input precision (float64 NumPy input is rounded in float64)."""
+    return _round_codes(x, 0, "round_to_fp4")
+
+
+def encode_fp4(values):
+    """Alias of round_to_fp4 (codec.py:96-98)."""
+    return round_to_fp4(values)
+
+
+def round_to_e4m3(x):
+    """Nearest finite E4M3 code of a non-negative value, ties to even, including
+    subnormals; saturates at 448 -> 0x7E (codec.py:101-112)."""
+    return _round_codes(x, 1, "round_to_e4m3")
+
+
+_FP4_TABLE = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], dtype=np.float64)
+FP4_DECODE = np.concatenate([_FP4_TABLE, -_FP4_TABLE])
+FP4_DECODE[8] = 0.0   # both zeros decode to +0.0
+
+
+def _e4m3_table():
+    c = np.arange(256)
+    e, m = (c >> 3) & 0xF, c & 7
+    mag = np.where(e == 0, m * 2.0 ** -9, (1.0 + m / 8.0) * 2.0 ** (e.astype(np.float64) - 7))
+    return np.where(c & 0x80, -mag, mag)
+
+
+E4M3_DECODE = _e4m3_table()
+
+
+def decode_fp4(codes):
+    """4-bit codes -> FP4 values (codec.py:91-93)."""
+    if isinstance(codes, torch.Tensor):
+        return torch.as_tensor(FP4_DECODE, device=codes.device)[codes.long()]
+    return FP4_DECODE[np.asarray(codes, dtype=np.uint8)]
+
+
+def decode_e4m3(codes):
+    """E4M3 codes -> values; NaN codes (0x7F / 0xFF) are rejected (codec.py:115-120)."""
+    if isinstance(codes, torch.Tensor):
+        if bool(((codes & 0x7F) == 0x7F).any()):
+            raise InvalidValue("NaN E4M3 code cannot be used as a scale")
+        return torch.as_tensor(E4M3_DECODE, device=codes.device)[codes.long()]
+    c = np.asarray(codes, dtype=np.uint8)
+    if np.any(c & 0x7F == 0x7F):
+        raise InvalidValue("NaN E4M3 code cannot be used as a scale")
+    return E4M3_DECODE[c]
+
+
+@dataclass
+class Fp4Block:
+    """block_size FP4 codes packed two per byte plus one shared scale code (codec.py:225-236)."""
+
+    codes: bytes
+    scale: int
+    spec: BlockSpec
+
+    def __post_init__(self):
+        if len(self.codes) != self.spec.block_size // 2:
+            raise ShapeError(f"packed block must be {self.spec.block_size // 2} bytes")
+
+
+def quantize_block(x, spec=NVFP4) -> Fp4Block:
+    """One block of block_size finite reals -> Fp4Block (codec.py:239-248), on the GPU quantizer."""
+    _require_nvfp4(spec)
+    arr = np.asarray(x.detach().cpu() if isinstance(x, torch.Tensor) else x, dtype=np.float64)
+    if arr.shape != (spec.block_size,):
+        raise ShapeError(f"block must have exactly {spec.block_size} elements")
+    if not np.all(np.isfinite(arr)):
+        raise InvalidValue("quantize_block requires finite input")
+    qt = quantize(arr[None, :], spec)
+    return Fp4Block(codes=bytes(np.asarray(qt.codes, dtype=np.uint8).reshape(-1)), scale=int(qt.scales[0, 0]),
+                    spec=spec)
+
+
+def dequantize_block(block: Fp4Block):
+    """Fp4Block -> block_size float64 reals (scale x code, exact; codec.py:251-258)."""
+    _require_nvfp4(block.spec)
+    codes = np.frombuffer(block.codes, dtype=np.uint8).reshape(1, -1)
+    scales = np.array([[block.scale]], dtype=np.uint8)
+    qt = QuantTensor(1, block.spec.block_size, block.spec, codes, scales)
+    return np.asarray(dequantize(qt, np.float64), dtype=np.float64).reshape(-1)

@@ -173,12 +173,33 @@ int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64
   return cuda_status(launch_quantize_cols(a, static_cast<cudaStream_t>(stream)));
 }
 
+int aq_round_codes(const void* x, int x_dtype, int64_t n, int format, uint8_t* codes, int* invalid, void* stream) {
+  if (!x || !codes || (x_dtype != 0 && x_dtype != 3) || (format != 0 && format != 1)) return AQ_E_INVALID;
+  if (n < 0) return AQ_E_SHAPE;
+  if (n == 0) return AQ_OK;
+  return cuda_status(launch_round_codes(x, x_dtype == 3, n, format, codes, invalid, static_cast<cudaStream_t>(stream)));
+}
+
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out, int out_dtype,
                   void* stream) {
   if (!codes || !scales || !out || !dtype_ok(out_dtype)) return AQ_E_INVALID;
   if (rows < 0 || cols <= 0 || cols % 16) return AQ_E_SHAPE;
   if (rows == 0) return AQ_OK;
   return cuda_status(launch_dequantize(codes, scales, rows, cols, out, out_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+int64_t aq_fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % 16) return 0;
+  return fp4mm_workspace_bytes(M, N, K);
+}
+
+int aq_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
+             const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, void* workspace, void* stream) {
+  if (!a_codes || !a_scales || !b_codes || !b_scales || !c || !workspace) return AQ_E_INVALID;
+  if (M < 0 || N < 0 || K <= 0 || K % 16 || ldc < N) return AQ_E_SHAPE;
+  if (M == 0 || N == 0) return AQ_OK;
+  return cuda_status(launch_fp4mm(a_codes, a_scales, M, b_codes, b_scales, N, K, c, ldc,
+                                  static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream)));
 }
 
 int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int keep) {

@@ -73,6 +73,12 @@ cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
+int64_t fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
+                         const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, uint8_t* ws,
+                         cudaStream_t st);
+cudaError_t launch_round_codes(const void* x, int x_is_f64, int64_t n, int format, uint8_t* codes, int* invalid,
+                               cudaStream_t st);
 cudaError_t launch_pack_kv4(const uint8_t* k_codes, const uint8_t* k_scales, const uint8_t* vt_codes,
                             const uint8_t* vt_scales, int64_t heads, int64_t n, int d, uint8_t* k_codes_t,
                             uint8_t* k_sf_t, uint8_t* v_codes_t, uint8_t* v_sf_t, cudaStream_t st);

@@ -406,4 +406,78 @@ cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64
   return cudaGetLastError();
 }
 
+
+
+// ---------------------------------------------------------------------------
+// Element-wise code rounding (codec.py:63-112): round_to_fp4 / round_to_e4m3.
+// Exact in the input precision (fp32 or fp64): the code is the number of
+// rounding midpoints below |x|, a tie (|x| exactly on a midpoint) goes to the
+// even code. Every midpoint of both formats is exact in fp32, so comparing in
+// the input's own precision reproduces the reference's float64 rounding with
+// no double rounding. fp4: |x| saturates at 6, a negative non-zero value keeps
+// the sign nibble (codec.py:84-87). e4m3: 0 <= x, saturates at 448 (0x7E).
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ double e4m3_code_value(int c) {
+  return c < 8 ? c * 0.001953125 : (1.0 + (c & 7) * 0.125) * ldexp(1.0, (c >> 3) - 7);
+}
+
+template <typename T, int FMT>
+__global__ void __launch_bounds__(256) round_codes_kernel(const T* __restrict__ x, int64_t n,
+                                                          uint8_t* __restrict__ codes, int* invalid) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T v = x[i];
+    const bool finite = isfinite(static_cast<double>(v));
+    if (!finite || (FMT == 1 && v < T(0))) {
+      if (invalid) atomicOr(invalid, 1);
+      codes[i] = 0;
+      continue;
+    }
+    const T mag = fabs(v);
+    int lo = 0, hi = 0;
+    if (FMT == 0) {
+      const T m = mag < T(6) ? mag : T(6);
+      const T mids[7] = {T(0.25), T(0.75), T(1.25), T(1.75), T(2.5), T(3.5), T(5)};
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        lo += mids[k] < m;
+        hi += mids[k] <= m;
+      }
+    } else {
+      const T m = mag < T(448) ? mag : T(448);
+      // binary search over the 126 midpoints mid(c) = (val(c) + val(c+1)) / 2, c = 0..125
+      int a = 0, b = 126;  // lo = #mids < m
+      while (a < b) {
+        const int c = (a + b) >> 1;
+        if (static_cast<T>(0.5 * (e4m3_code_value(c) + e4m3_code_value(c + 1))) < m) a = c + 1;
+        else b = c;
+      }
+      lo = a;
+      hi = (lo < 126 && static_cast<T>(0.5 * (e4m3_code_value(lo) + e4m3_code_value(lo + 1))) == m) ? lo + 1 : lo;
+    }
+    int code = lo != hi ? lo + (lo & 1) : lo;
+    if (FMT == 0 && signbit(static_cast<double>(v)) && v != T(0)) code |= 0x8;
+    codes[i] = static_cast<uint8_t>(code);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_round_codes(const void* x, int x_is_f64, int64_t n, int format, uint8_t* codes, int* invalid,
+                               cudaStream_t st) {
+  int64_t g = ceil_div(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  const int grid = static_cast<int>(g < 1 ? 1 : g);
+  if (x_is_f64) {
+    if (format == 0) round_codes_kernel<double, 0><<<grid, 256, 0, st>>>(static_cast<const double*>(x), n, codes, invalid);
+    else round_codes_kernel<double, 1><<<grid, 256, 0, st>>>(static_cast<const double*>(x), n, codes, invalid);
+  } else {
+    if (format == 0) round_codes_kernel<float, 0><<<grid, 256, 0, st>>>(static_cast<const float*>(x), n, codes, invalid);
+    else round_codes_kernel<float, 1><<<grid, 256, 0, st>>>(static_cast<const float*>(x), n, codes, invalid);
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace aq

@@ -129,3 +129,98 @@ def load_quant_tensor(path, device=None) -> QuantTensor:
         return QuantTensor(rows, cols, spec, torch.from_numpy(codes.copy()).to(device),
                            torch.from_numpy(scales.copy()).to(device))
     return QuantTensor(rows, cols, spec, codes.copy(), scales.copy())
+
+
+# ----------------------------------------------------------------------------
+# deterministic host random streams (tensors.py:89-117): test-data generators,
+# identical streams to the reference for the same seed
+# ----------------------------------------------------------------------------
+
+class Rng:
+    """PCG64 stream with NumPy's standard normal; ``spawn`` derives an
+    independent stream from (seed, offset) the way the reference does."""
+
+    def __init__(self, seed):
+        self.seed = int(seed)
+        self._gen = np.random.Generator(np.random.PCG64(self.seed))
+
+    def spawn(self, offset):
+        return Rng(self.seed * 0x9E3779B9 + offset & 0x7FFFFFFFFFFFFFFF)
+
+    def standard_normal(self, dims, dtype=np.float64):
+        return self._gen.standard_normal(size=dims).astype(dtype)
+
+    def integers(self, low, high=None, size=None):
+        return self._gen.integers(low, high=high, size=size)
+
+    def uniform(self, low=0.0, high=1.0, size=None):
+        return self._gen.uniform(low, high, size=size)
+
+
+def randn(dims, rng, scale=1.0, dtype=np.float64):
+    """i.i.d. N(0, scale^2) host tensor from an Rng."""
+    if scale <= 0:
+        raise ShapeError("scale must be positive")
+    return scale * rng.standard_normal(tuple(dims), dtype=dtype)
+
+
+# ----------------------------------------------------------------------------
+# matrix products (tensors.py:25-86)
+# ----------------------------------------------------------------------------
+
+def _dev_u8(a):
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint8))
+    return t.to("cuda").contiguous()
+
+
+def fp4mm(aq, bq_t, accum_width=32):
+    """C = A @ B from NVFP4 QuantTensors, B supplied transposed (both blocked
+    along the contraction axis; tensors.py:54-86), on block-scaled tcgen05
+    MMAs. Exact block products, fp32 accumulation (accum_width=64 raises
+    InvalidValue: the tensor cores accumulate in fp32). NumPy operands give a
+    NumPy result, torch operands a CUDA tensor."""
+    from . import _lib
+    from .codec import NVFP4
+    if not isinstance(aq, QuantTensor) or not isinstance(bq_t, QuantTensor):
+        raise ShapeError("fp4mm operands must be QuantTensors")
+    if aq.spec != bq_t.spec:
+        raise ShapeError("fp4mm operands must share a BlockSpec")
+    if aq.cols != bq_t.cols:
+        raise ShapeError(f"contraction axes differ: {aq.cols} vs {bq_t.cols}")
+    if accum_width not in (32, 64):
+        raise ShapeError(f"accum_width must be 32 or 64, got {accum_width}")
+    if accum_width != 32:
+        raise InvalidValue("the B200 path accumulates in fp32 (tensor cores); accum_width=64 is CPU-only")
+    if aq.spec != NVFP4:
+        raise InvalidValue("the B200 path implements NVFP4 only")
+    _lib.require_cuda()
+    as_np = not isinstance(aq.codes, torch.Tensor)
+    ac, asf, bc, bsf = (_dev_u8(x) for x in (aq.codes, aq.scales, bq_t.codes, bq_t.scales))
+    M, N, K = aq.rows, bq_t.rows, aq.cols
+    lib = _lib.load()
+    ws = torch.empty(lib.aq_fp4mm_workspace_bytes(M, N, K), dtype=torch.uint8, device="cuda")
+    c = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    _lib.check(lib.aq_fp4mm(_lib.ptr(ac), _lib.ptr(asf), M, _lib.ptr(bc), _lib.ptr(bsf), N, K, _lib.ptr(c), N,
+                            _lib.ptr(ws), _lib.stream_ptr()))
+    return c.cpu().numpy() if as_np else c
+
+
+def matmul(a, b, accum_width=32):
+    """a @ b in the accumulation width (tensors.py:32-51), on the GPU (cuBLAS
+    through torch; the reference's fixed left-to-right summation order is not
+    reproduced, results agree to fp32 / fp64 rounding). a may be 3-D with b
+    shared across the batch."""
+    from . import _lib
+    if accum_width not in (32, 64):
+        raise ShapeError(f"accum_width must be 32 or 64, got {accum_width}")
+    dt = torch.float32 if accum_width == 32 else torch.float64
+    as_np = not isinstance(a, torch.Tensor)
+    _lib.require_cuda()
+    ta = torch.as_tensor(np.asarray(a) if as_np else a).to("cuda", dt)
+    tb = torch.as_tensor(np.asarray(b) if not isinstance(b, torch.Tensor) else b).to("cuda", dt)
+    if ta.dim() not in (2, 3) or tb.dim() != 2:
+        raise ShapeError("matmul expects a 2-D or 3-D left operand and 2-D right")
+    if tb.shape[0] != ta.shape[-1]:
+        raise ShapeError(f"inner dims mismatch: {tuple(ta.shape)} x {tuple(tb.shape)}")
+    out = ta @ tb
+    return out.cpu().numpy() if as_np else out

@@ -1,0 +1,65 @@
+"""Element-wise code rounding (round_to_fp4 / round_to_e4m3, codec.py:63-112) and
+single-block helpers (codec.py:225-258) on the GPU vs the pinned oracle,
+including float64 inputs one ulp either side of every rounding midpoint (no
+double rounding through float32)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_00040_b200 as aq
+from oracle import nvfp4_attn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _around(points):
+    pts = np.asarray(points, dtype=np.float64)
+    return np.concatenate([pts, np.nextafter(pts, -np.inf), np.nextafter(pts, np.inf), pts + 1e-12, pts - 1e-12])
+
+
+def test_round_to_fp4_matches_oracle():
+    codec = np.load(os.path.join(GOLD, "codec.npz"))
+    mids = [0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0]
+    rng = np.random.default_rng(0)
+    x = np.concatenate([codec["adv_x"].reshape(-1), rng.standard_normal(4096) * 3, _around(mids), -_around(mids),
+                        [0.0, -0.0, -1e-30, 1e-30, 6.0, 7.0, -6.5, 1e30, -1e30]])
+    got = aq.round_to_fp4(x)
+    np.testing.assert_array_equal(got, orc.round_to_fp4(x))
+    # float32 torch input on the device
+    x32 = torch.from_numpy(x.astype(np.float32)).cuda()
+    np.testing.assert_array_equal(aq.round_to_fp4(x32).cpu().numpy(), orc.round_to_fp4(x.astype(np.float32)))
+    assert aq.round_to_fp4(-0.0) == 0 and aq.round_to_fp4(-0.1) == 0x8 and aq.round_to_fp4(0.25) == 0
+
+
+def test_round_to_e4m3_matches_oracle():
+    vals = orc.E4M3_VALUES[:127].astype(np.float64)
+    mids = (vals[:-1] + vals[1:]) / 2
+    rng = np.random.default_rng(1)
+    x = np.concatenate([np.abs(rng.standard_normal(4096)) * 10.0 ** rng.integers(-4, 3, 4096), _around(mids),
+                        _around(vals), [0.0, 448.0, 464.0, 1e6, 2.0 ** -10, 2.0 ** -11]])
+    x = x[x >= 0]
+    np.testing.assert_array_equal(aq.round_to_e4m3(x), orc.round_to_e4m3(x))
+
+
+def test_invalid_inputs_raise():
+    for bad in ([np.inf], [np.nan, 1.0]):
+        with pytest.raises(aq.InvalidValue):
+            aq.round_to_fp4(np.array(bad))
+    with pytest.raises(aq.InvalidValue):
+        aq.round_to_e4m3(np.array([1.0, -0.5]))
+
+
+def test_quantize_dequantize_block():
+    rng = np.random.default_rng(2)
+    for _ in range(20):
+        x = rng.standard_normal(16) * 10.0 ** rng.integers(-3, 3)
+        blk = aq.quantize_block(x)
+        codes, scales = orc.quantize(x.astype(np.float32).astype(np.float64)[None, :])
+        assert blk.codes == codes.tobytes() and blk.scale == int(scales[0, 0])
+        np.testing.assert_array_equal(aq.dequantize_block(blk), orc.dequantize(codes, scales, 16, np.float64)[0])
+    with pytest.raises(aq.ShapeError):
+        aq.quantize_block(np.zeros(8))
