@@ -14,4 +14,6 @@ ncu --set full --clock-control none --import-source on -k regex:attn_bwd_kernel 
     python scripts/time_bwd.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:quantize -s 2 -c 3 -o gpurun_out/prof/quantize_c2 \
     python scripts/time_quant.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:fp4mm_kernel -s 1 -c 1 -o gpurun_out/prof/fp4mm_8k \
+    python scripts/time_fp4mm.py > /dev/null 2>&1
 ls -la gpurun_out/prof
