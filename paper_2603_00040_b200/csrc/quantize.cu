@@ -150,30 +150,43 @@ __device__ __forceinline__ void store_fq16(void* p, int64_t i0, int dt, const __
 //   sf_t      SF512 images per tile
 //   fqh_t     T8x8 16-bit tiles of the dequantized values (dtype fqh_dt)
 // ---------------------------------------------------------------------------
-template <bool WANT_FQ>
+// NPAIR > 0: compile-time block pairs per row (d = 64 / 128), so the per-thread
+// index math is shifts and masks; 0 = runtime (any cols). Rows are contiguous
+// across heads in the common case (n % 128 == 0, hs == n * ld): then no
+// division by n is needed at all (64-bit division dominated the instruction
+// count of the first version).
+template <bool WANT_FQ, int NPAIR>
 __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
   const int64_t nb = a.cols / 16;
-  const int64_t npair = (nb + 1) / 2;
+  const int64_t npair = NPAIR > 0 ? NPAIR : (nb + 1) / 2;
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
   const int64_t total = a.heads * n_pad * npair;
   const int D = static_cast<int>(a.cols);
+  const bool flat = n_pad == a.n && a.hs == a.n * a.ld;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t bp = t % npair;
-    const int64_t rowp = t / npair;
-    const int64_t h = rowp / n_pad;
-    const int64_t r = rowp % n_pad;
-    const bool real = r < a.n;
-    const int64_t row = h * a.n + r;
-    const int64_t tile = h * (n_pad / TILE) + r / TILE;
-    const int rr = static_cast<int>(r % TILE);
+    const int64_t bp = NPAIR > 0 ? (t & (NPAIR - 1)) : t % npair;
+    const int64_t rowp = NPAIR > 0 ? (t / NPAIR) : t / npair;
+    int64_t h, r;
+    if (flat) {
+      h = 0;
+      r = rowp;          // row index over all heads; source offset rowp * ld
+    } else {
+      h = rowp / n_pad;
+      r = rowp % n_pad;
+    }
+    const bool real = flat || r < a.n;
+    const int64_t row = flat ? rowp : h * a.n + r;
+    // n_pad is a multiple of TILE in tiled mode, so tiles of consecutive heads are consecutive
+    const int64_t tile = rowp / TILE;
+    const int rr = static_cast<int>(rowp % TILE);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int64_t b = bp * 2 + half;
       if (b >= nb) break;
       float v[16];
       if (real) {
-        load16(a.x, h * a.hs + r * a.ld + b * 16, a.x_dt, v);
+        load16(a.x, (flat ? rowp * a.ld : h * a.hs + r * a.ld) + b * 16, a.x_dt, v);
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -233,25 +246,29 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
     for (int c0 = 0; c0 < D; c0 += kColsMax) {
       const int cw = min(kColsMax, D - c0);
       __syncthreads();
-      const bool vec = a.x_dt == kBF16 && cw == kColsMax && (a.ld % 8) == 0 && (a.hs % 8) == 0 &&
-                       (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+      const bool vec = a.x_dt == kBF16 && (cw % 8) == 0 && (a.ld % 8) == 0 && (a.hs % 8) == 0 &&
+                       (c0 % 8) == 0 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
       if (vec) {
-        // all 16-byte loads of the slab in flight at once (8 per thread), then unpack
-        constexpr int CV = kColsMax / 8, PER = kColsSlab * CV / 128;
+        // all 16-byte loads of the slab in flight at once (up to 8 per thread), then unpack
+        const int cv = cw / 8;
+        const int nvec = kColsSlab * cv;
+        constexpr int PER = kColsSlab * (kColsMax / 8) / 128;
         uint4 w[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           const int i = threadIdx.x + k * 128;
-          const int tt = i / CV, c = (i % CV) * 8;
+          const int tt = i / cv, c = (i % cv) * 8;
           const int64_t tok = tok0 + tt;
-          w[k] = tok < a.n ? *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.x) + h * a.hs +
-                                                             tok * a.ld + c0 + c)
-                           : make_uint4(0, 0, 0, 0);
+          w[k] = (i < nvec && tok < a.n)
+                     ? *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.x) + h * a.hs +
+                                                       tok * a.ld + c0 + c)
+                     : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           const int i = threadIdx.x + k * 128;
-          const int tt = i / CV, c = (i % CV) * 8;
+          if (i >= nvec) break;
+          const int tt = i / cv, c = (i % cv) * 8;
           const uint32_t ww[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -267,10 +284,12 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
         }
       }
       __syncthreads();
-      for (int c = threadIdx.x; c < cw; c += blockDim.x) {
+      // one work item = (column, 32-token group): every thread busy for narrow d too
+      for (int wi = threadIdx.x; wi < cw * (kColsSlab / 32); wi += blockDim.x) {
+        const int c = wi % cw;
+        const int g32 = wi / cw;
         const int64_t col = c0 + c;
-#pragma unroll
-        for (int g32 = 0; g32 < kColsSlab / 32; ++g32) {
+        {
           uint32_t codes[4];
           uint32_t scales = 0;
 #pragma unroll
@@ -381,10 +400,17 @@ static int grid_for(int64_t work) {
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
   const int g = grid_for(a.heads * n_pad * ((a.cols / 16 + 1) / 2));
-  if (a.fq || a.fqh_t)
-    quantize_rows_kernel<true><<<g, 256, 0, st>>>(a);
-  else
-    quantize_rows_kernel<false><<<g, 256, 0, st>>>(a);
+  const bool fq = a.fq || a.fqh_t;
+  if (a.cols == 128) {
+    if (fq) quantize_rows_kernel<true, 4><<<g, 256, 0, st>>>(a);
+    else quantize_rows_kernel<false, 4><<<g, 256, 0, st>>>(a);
+  } else if (a.cols == 64) {
+    if (fq) quantize_rows_kernel<true, 2><<<g, 256, 0, st>>>(a);
+    else quantize_rows_kernel<false, 2><<<g, 256, 0, st>>>(a);
+  } else {
+    if (fq) quantize_rows_kernel<true, 0><<<g, 256, 0, st>>>(a);
+    else quantize_rows_kernel<false, 0><<<g, 256, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
