@@ -410,13 +410,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           tc_fence_before();
           mbar_arrive(&bars[C::B_SB_EMPTY]);
           const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
-#ifndef AQ_DBG_NOEXP2
-          p_from_s<CW / 2>(x, cbase, sl2, L2);
-#endif
-          if (lim < CW - 1) {
-#pragma unroll
-            for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
-          }
+          // claim the P^F buffer first, so P = exp(S - L), its quantization and the
+          // stores form one straight-line block per 32 keys that the scheduler can
+          // interleave (MUFU work of one group overlaps ALU work of the previous)
           const int pb = pc % C::NP;
           if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
           ++pc;
@@ -425,8 +421,14 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           uint32_t scw[(CW + 63) / 64];
 #pragma unroll
           for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
+          auto group32 = [&](int blk, bool masked) {
+#ifndef AQ_DBG_NOEXP2
+            p_from_s<16>(x + blk * 16, cbase + blk * 16, sl2, L2);
+#endif
+            if (masked) {
 #pragma unroll
-          for (int blk = 0; blk < CW / 16; blk += 2) {
+              for (int c = 0; c < 32; ++c) x[blk * 16 + c] = (blk * 16 + c <= lim) ? x[blk * 16 + c] : 0.f;
+            }
 #ifdef AQ_DBG_NOQ2
             PBlock qa, qb;
             qa.scale = __float_as_uint(x[blk * 16]) & 0xff; qa.codes[0] = __float_as_uint(x[blk * 16 + 1]); qa.codes[1] = __float_as_uint(x[blk * 16 + 2]);
@@ -438,6 +440,13 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
                 make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
             scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+          };
+          if (lim >= CW - 1) {
+#pragma unroll
+            for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, false);
+          } else {
+#pragma unroll
+            for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, true);
           }
 #pragma unroll
           for (int s = 0; s < CW / 64; ++s)
