@@ -394,6 +394,32 @@ def main():
            "api": "attn_forward_host (inference)" if mode == "fwd" else "attn_qat_host (fwd+bwd)",
            "pcie_gbs": (h2d_b + d2h_b) / (float(et.item()) * 1e-3) / 1e9}
 
+    # ---- the same inference step serving from a stored FP4 KV cache (kvcache.py):
+    # only Q (bf16) and the 4-bit K / V^T cross PCIe; the cache is built once,
+    # outside the timed region, like a serving KV cache
+    e2e_kv4 = None
+    if mode == "fwd":
+        hcache = aq.kv4_quantize(k, v).pin_memory()
+
+        def kv4_step():
+            aq.attn_forward_kv4_host(hq, hcache, causal=causal, out=ho, lse_out=hl)
+        for _ in range(2):
+            kv4_step()
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(st)
+        for _ in range(args.steps):
+            kv4_step()
+        b1.record(st)
+        barrier()
+        kms = b0.elapsed_time(b1) / args.steps
+        kt_ = torch.tensor([kms], device=dev)
+        if world > 1:
+            dist.all_reduce(kt_, op=dist.ReduceOp.MAX)
+        e2e_kv4 = {"value": world * flops_rank / (float(kt_.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "ms_per_step": float(kt_.item()), "api": "attn_forward_kv4_host (NVFP4 KV cache)",
+                   "h2d_bytes_per_step": q.numel() * 2 + hcache.nbytes(), "d2h_bytes_per_step": d2h_b}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ref = CpuReference(cfg)
@@ -413,7 +439,7 @@ def main():
                        "global_batch": world * B, "parallelism": f"dp{world} over B*H (no comms)",
                        "l2": "inputs larger than L2 (3 x %.0f MB bf16)" % (q.numel() * 2 / 1e6)},
             "tokens_per_s": tokens_s,
-            "roofline": roof, "mma_peaks_tflops": peaks, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "mma_peaks_tflops": peaks, "cpu_baseline": cpu, "e2e": e2e, "e2e_fp4_kv_cache": e2e_kv4,
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
         }), flush=True)
     if world > 1:

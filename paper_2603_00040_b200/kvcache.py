@@ -46,6 +46,10 @@ class KV4Cache:
         return KV4Cache(self.heads, self.n, self.d, *(t.to(device) for t in
                                                       (self.k_codes, self.k_scales, self.vt_codes, self.vt_scales)))
 
+    def pin_memory(self):
+        return KV4Cache(self.heads, self.n, self.d, *(t.cpu().pin_memory() for t in
+                                                      (self.k_codes, self.k_scales, self.vt_codes, self.vt_scales)))
+
     def nbytes(self):
         return sum(t.numel() for t in (self.k_codes, self.k_scales, self.vt_codes, self.vt_scales))
 
@@ -155,3 +159,38 @@ def load_kv4(prefix, device="cuda") -> KV4Cache:
         raise ShapeError("V^T columns do not match the padded token count")
     return KV4Cache(heads, n, d, kq.codes.reshape(heads, n, d // 2), kq.scales.reshape(heads, n, d // 16),
                     vq.codes.reshape(heads, d, vq.cols // 2), vq.scales.reshape(heads, d, vq.cols // 16))
+
+
+def attn_forward_kv4_host(q, cache: KV4Cache, causal=False, out=None, lse_out=None, out_dtype=None,
+                          chunk_heads=None):
+    """FP4-KV-cache inference from host memory: q [..., n_q, d] and a KV4Cache
+    on the host (pinned for overlap) -> host (O, L). Only Q (16-bit) and the
+    4-bit cache cross PCIe -- 0.5625 B per cached K/V element instead of 2 --
+    streamed over head chunks like attn_forward_host (host.py)."""
+    from .host import default_chunk, run_pipelined
+    _lib.require_cuda()
+    if q.device.type != "cpu" or cache.k_codes.device.type != "cpu":
+        raise InvalidValue("host entry points take CPU tensors (pinned for overlapped copies)")
+    n_q, d = q.shape[-2:]
+    q3 = q.reshape(-1, n_q, d)
+    heads = q3.shape[0]
+    if heads != cache.heads or d != cache.d:
+        raise ShapeError(f"q {tuple(q.shape)} does not match the cache (heads {cache.heads}, d {cache.d})")
+    out_dtype = out_dtype or q.dtype
+    o = out.reshape(heads, n_q, d) if out is not None else torch.empty((heads, n_q, d), dtype=out_dtype,
+                                                                         pin_memory=True)
+    lse = lse_out.reshape(heads, n_q) if lse_out is not None else torch.empty((heads, n_q), dtype=torch.float32,
+                                                                              pin_memory=True)
+    per_head = q3[0].numel() * q3.element_size() + cache.nbytes() // heads
+    chunk = chunk_heads or default_chunk(heads, per_head)
+    lib = _lib.load()
+    ws = (lambda h: (lib.aq_attn_fwd_workspace_bytes(h, n_q, cache.n, d, 0, 0),), torch.uint8)
+
+    def fn(dev, res, scr):
+        part = KV4Cache(dev[1].shape[0], cache.n, d, *dev[1:])
+        attn_forward_kv4(dev[0], part, causal=causal, out=res[0], lse_out=res[1], workspace=scr[0],
+                         out_dtype=out_dtype)
+    run_pipelined(fn, [q3, cache.k_codes, cache.k_scales, cache.vt_codes, cache.vt_scales], [o, lse], chunk,
+                  scratch=[("kv4_ws", *ws)])
+    lead = q.shape[:-2]
+    return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)

@@ -66,3 +66,13 @@ def test_kv4_errors():
         aq.attn_forward_kv4(torch.randn(2, 256, 64, device="cuda"), cache, causal=True)
     with pytest.raises(aq.ShapeError):
         aq.kv4_quantize(k, v[:, :64])
+
+
+def test_kv4_host_pipeline_equals_device():
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn(2, 5, 384, 128, generator=g, device="cuda").bfloat16() for _ in range(3))
+    cache = aq.kv4_quantize(k, v)
+    o_d, l_d = aq.attn_forward_kv4(q, cache, causal=True)
+    o_h, l_h = aq.attn_forward_kv4_host(q.cpu().pin_memory(), cache.pin_memory(), causal=True, chunk_heads=3)
+    torch.cuda.synchronize()
+    assert o_h.device.type == "cpu" and torch.equal(o_h, o_d.cpu()) and torch.equal(l_h, l_d.cpu())
