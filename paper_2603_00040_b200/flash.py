@@ -264,7 +264,7 @@ def attn_forward_host(q, k, v, causal=False, train=False, out=None, lse_out=None
         o_hp = o_hp_out.reshape(heads, n_q, d) if o_hp_out is not None else _host_empty((heads, n_q, d), out_dtype)
         outs.append(o_hp)
     per_head = (q3[0].numel() + 2 * k3[0].numel()) * q3.element_size()
-    chunk = chunk_heads or default_chunk(heads, per_head)
+    chunk = chunk_heads or default_chunk(heads, per_head, items_per_head=-(-n_q // 128))
     lib = _lib.load()
     ws_bytes = lambda h: (lib.aq_attn_fwd_workspace_bytes(h, n_q, n_k, d, int(train), 0),)  # noqa: E731
     if ws_bytes(1)[0] <= 0:
@@ -298,7 +298,7 @@ def attn_qat_host(q, k, v, d_o, causal=False, variant=BwdVariant.CORRECT, out=No
         dq = _host_empty((heads, n_q, d), dt)
         dk, dv = (_host_empty((heads, n_k, d), dt) for _ in range(2))
     per_head = (2 * q3[0].numel() + 2 * k3[0].numel()) * q3.element_size()
-    chunk = chunk_heads or default_chunk(heads, per_head)
+    chunk = chunk_heads or default_chunk(heads, per_head, items_per_head=-(-n_q // 128))
     lib = _lib.load()
     if lib.aq_attn_fwd_workspace_bytes(1, n_q, n_k, d, 1, 1) <= 0:
         raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")

@@ -131,10 +131,17 @@ def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device
     comp.wait_stream(h2d)
 
 
-def default_chunk(heads, per_head_bytes):
-    """~16 chunks (the first upload and the last download are not overlapped,
-    so smaller chunks shorten the exposed ends), but at least 16 MB per chunk
-    so the copies stay near the PCIe rate."""
+def default_chunk(heads, per_head_bytes, items_per_head=None, sms=None):
+    """Heads per chunk: ~16 chunks (the first upload and the last download are
+    not overlapped, so smaller chunks shorten the exposed ends), at least 16 MB
+    per chunk so the copies stay near the PCIe rate, and -- when the kernels
+    are persistent over (head, 128-row tile) items -- at least ~8 waves of
+    items per chunk so a compute-heavy chunk does not end in a mostly idle
+    wave."""
     target = max(1, heads // 16)
     min_heads = max(1, (16 << 20) // max(1, per_head_bytes))
+    if items_per_head:
+        if sms is None:
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        min_heads = max(min_heads, -(-8 * sms // items_per_head))
     return min(heads, max(target, min_heads))

@@ -182,7 +182,7 @@ def attn_forward_kv4_host(q, cache: KV4Cache, causal=False, out=None, lse_out=No
     lse = lse_out.reshape(heads, n_q) if lse_out is not None else torch.empty((heads, n_q), dtype=torch.float32,
                                                                               pin_memory=True)
     per_head = q3[0].numel() * q3.element_size() + cache.nbytes() // heads
-    chunk = chunk_heads or default_chunk(heads, per_head)
+    chunk = chunk_heads or default_chunk(heads, per_head, items_per_head=-(-n_q // 128))
     lib = _lib.load()
     ws = (lambda h: (lib.aq_attn_fwd_workspace_bytes(h, n_q, cache.n, d, 0, 0),), torch.uint8)
 

@@ -32,7 +32,7 @@ def run(B, H, N, d, causal, train, reps=10):
 
 
 CASES = [(4, 32, 8192, 128, True, False), (1, 40, 32760, 128, False, False), (8, 32, 4096, 128, True, True),
-         (4, 32, 8192, 64, True, False)]
+         (4, 32, 8192, 64, True, False), (8, 32, 4096, 128, True, False), (4, 32, 8192, 128, True, True)]
 
 if __name__ == "__main__":
     sel = [int(a) for a in sys.argv[1:]] or range(len(CASES))
