@@ -50,8 +50,9 @@ __device__ unsigned long long g_prof[16];
 template <int D, bool TRAIN, int CS>
 struct Cfg {
   static constexpr int NSW = 4 * CS;                 // softmax warps
-  static constexpr int NUM_THREADS = 32 * (NSW + 2);
-  static constexpr int PRODUCER = NSW, MMA = NSW + 1;
+  static constexpr int NUM_THREADS = 32 * (NSW + 3);
+  static constexpr int PRODUCER = NSW, PRODUCER1 = NSW + 1, MMA = NSW + 2;
+  static constexpr int NK1 = 4;                      // K ring (K codes + SF only), both passes
   static constexpr int CW = TILE / CS;               // key columns per softmax thread
   static constexpr int NS = TRAIN ? 2 : 5;           // K/V stages
   static constexpr int NB1 = 3;                      // S buffers in pass 1 (1 and 2 alias O / O')
@@ -59,14 +60,14 @@ struct Cfg {
   static constexpr int NP = TRAIN ? 2 : 3;           // P^F (and P^) buffers
   // TMEM columns: S buffer b at 128*b
   static constexpr uint32_t T_O = TRAIN ? 128 : 256, T_OP = 256;
-  static constexpr uint32_t T_QSF = 384, T_KSF = 392, T_PSF = T_KSF + 8 * NS, T_VSF = T_PSF + 8 * NP;
+  static constexpr uint32_t T_QSF = 384, T_PSF = T_QSF + 8, T_VSF = T_PSF + 8 * NP, T_KSF1 = T_VSF + 8 * NS;
   // shared memory
   static constexpr int Q_CODES = 0;
   static constexpr int Q_SF = Q_CODES + TILE * D / 2;
   static constexpr int STAGE0 = Q_SF + (D / 64) * 512;
-  static constexpr int ST_K = 0;
-  static constexpr int ST_KSF = ST_K + TILE * D / 2;
-  static constexpr int ST_V = ST_KSF + (D / 64) * 512;
+  // pass-2 stage: V^T codes + scale factors (+ V^F fp16); K tiles of both
+  // passes come through the small K ring of producer 1
+  static constexpr int ST_V = 0;
   static constexpr int ST_VSF = ST_V + TILE * D / 2;
   static constexpr int ST_VH = ST_VSF + 1024;
   static constexpr int STAGE_BYTES = ST_VH + (TRAIN ? TILE * D * 2 : 0);
@@ -74,8 +75,10 @@ struct Cfg {
   static constexpr int PB_CODES = 0, PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024;
   static constexpr int P_BYTES = PB_H + (TRAIN ? TILE * TILE * 2 : 0);
   static constexpr int ML = P0 + NP * P_BYTES;       // pass-1 (m, l) partials
-  static constexpr int BARS = ML + 2 * CS * TILE * 4;
-  static constexpr int NUM_BARS = 32;
+  static constexpr int K1_0 = ML + 2 * CS * TILE * 4; // pass-1 K ring
+  static constexpr int K1_BYTES = TILE * D / 2 + (D / 64) * 512;
+  static constexpr int BARS = K1_0 + NK1 * K1_BYTES;
+  static constexpr int NUM_BARS = 40;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int USED = TMEM_SLOT + 16;
   // one CTA per SM (the kernel owns all 512 TMEM columns)
@@ -86,10 +89,11 @@ struct Cfg {
   // barrier slots
   static constexpr int B_Q_FULL = 0, B_Q_EMPTY = 1, B_O_FULL = 2, B_O_EMPTY = 3, B_KV_FULL = 4,
                        B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS, B_S_EMPTY = B_S_FULL + NB1,
-                       B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP, B_END = B_P_EMPTY + NP;
+                       B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP, B_K1_FULL = B_P_EMPTY + NP,
+                       B_K1_EMPTY = B_K1_FULL + NK1, B_END = B_K1_EMPTY + NK1;
   static_assert(B_END <= NUM_BARS, "barrier slots");
   static_assert(USED <= 227 * 1024, "shared memory");
-  static_assert(T_VSF + 8 * NS <= 512, "TMEM columns");
+  static_assert(T_KSF1 + 8 * NK1 <= 512, "TMEM columns");
 };
 
 // Work item w -> (head, query tile, key tiles). Causal items are ordered by
@@ -157,6 +161,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       mbar_init(&bars[C::B_P_FULL + b], 32 * C::NSW);
       mbar_init(&bars[C::B_P_EMPTY + b], 1);
     }
+    for (int s = 0; s < C::NK1; ++s) {
+      mbar_init(&bars[C::B_K1_FULL + s], 1);
+      mbar_init(&bars[C::B_K1_EMPTY + s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -178,25 +186,42 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q_FULL]);
       }
       __syncwarp();
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < item.nt; ++j, ++it) {
-          const int st = it % C::NS;
-          if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
-          uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
-          const int64_t kt_idx = item.head * k_tiles + j;
-          uint64_t* fb = &bars[C::B_KV_FULL + st];
-          if (elect_one()) {
-            mbar_expect_tx(fb, C::K_BYTES + (pass ? C::V_BYTES : 0));
-            bulk_g2s(sb + C::ST_K, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-            bulk_g2s(sb + C::ST_KSF, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
-            if (pass) {
-              bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-              bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
-              if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
-            }
-          }
-          __syncwarp();
+      // pass-2 stages (V [+ V^F]); the K tiles of both passes come from producer 1's ring
+      for (int j = 0; j < item.nt; ++j, ++it) {
+        const int st = it % C::NS;
+        if (it >= C::NS) mbar_wait(&bars[C::B_KV_EMPTY + st], ((it / C::NS) - 1) & 1);
+        uint8_t* sb = smem + C::STAGE0 + st * C::STAGE_BYTES;
+        const int64_t kt_idx = item.head * k_tiles + j;
+        uint64_t* fb = &bars[C::B_KV_FULL + st];
+        if (elect_one()) {
+          mbar_expect_tx(fb, C::V_BYTES);
+          bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+          bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
+          if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
         }
+        __syncwarp();
+      }
+    }
+  } else if (warp == C::PRODUCER1) {
+    // ------------------------------------------------------------ producer 1: K ring
+    // K codes + scale factors only (9 KB per tile), NK1 deep, for the S MMAs of
+    // both passes, running ahead independently of the large pass-2 stages
+    int i1 = 0;
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item item = work_item(p, w, q_tiles, k_tiles);
+      for (int jp = 0; jp < 2 * item.nt; ++jp, ++i1) {
+        const int j = jp % item.nt;  // pass 1 then pass 2 re-read the same K tiles
+        const int st = i1 % C::NK1;
+        if (i1 >= C::NK1) mbar_wait(&bars[C::B_K1_EMPTY + st], ((i1 / C::NK1) - 1) & 1);
+        uint8_t* sb = smem + C::K1_0 + st * C::K1_BYTES;
+        const int64_t kt_idx = item.head * k_tiles + j;
+        uint64_t* fb = &bars[C::B_K1_FULL + st];
+        if (elect_one()) {
+          mbar_expect_tx(fb, C::K_BYTES);
+          bulk_g2s(sb, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+          bulk_g2s(sb + TILE * D / 2, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == C::MMA) {
@@ -213,26 +238,28 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
     const uint32_t q_base = s0 + C::Q_CODES;
     int it = 0, pc = 0, k = 0;
     SUses su;
-    // S(it) into buffer b
-    auto issue_s = [&](int it_, int b) {
+    // S(i1) into buffer b, K from producer 1's ring (both passes, in order)
+    int i1 = 0;
+    auto issue_s1 = [&](int b) {
       const int u = su.take(b);
-      const int st = it_ % C::NS;
-      mbar_wait(&bars[C::B_KV_FULL + st], (it_ / C::NS) & 1);
+      const int st = i1 % C::NK1;
+      mbar_wait(&bars[C::B_K1_FULL + st], (i1 / C::NK1) & 1);
       if (u > 0) mbar_wait(&bars[C::B_S_EMPTY + b], (u - 1) & 1);
       tc_fence_after();
-      const uint32_t kb = s0 + C::STAGE0 + st * C::STAGE_BYTES + C::ST_K;
-      const uint32_t ksf = s0 + C::STAGE0 + st * C::STAGE_BYTES + C::ST_KSF;
+      const uint32_t kb = s0 + C::K1_0 + st * C::K1_BYTES;
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + C::T_KSF + 8 * st + 4 * ks, desc_at(t_sf, ksf + ks * 512));
+          tmem_cp_32x128_x4(tmem + C::T_KSF1 + 8 * st + 4 * ks, desc_at(t_sf, kb + TILE * D / 2 + ks * 512));
 #pragma unroll
         for (int ks = 0; ks < D / 64; ++ks)
           mma_nvf4_ss(tmem + 128 * b, desc_at(t_k, q_base + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
-                      tmem + C::T_QSF + 4 * ks, tmem + C::T_KSF + 8 * st + 4 * ks, ks > 0);
+                      tmem + C::T_QSF + 4 * ks, tmem + C::T_KSF1 + 8 * st + 4 * ks, ks > 0);
         tc_commit(&bars[C::B_S_FULL + b]);
+        tc_commit(&bars[C::B_K1_EMPTY + st]);
       }
       __syncwarp();
+      ++i1;
     };
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
@@ -245,11 +272,9 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       __syncwarp();
       // pass 1: S tiles round-robin over NB1 buffers; buffers 1 and 2 alias
       // the O (/O') columns, so they wait for the previous item's epilogue
-      for (int jj = 0; jj < nt; ++jj, ++it) {
+      for (int jj = 0; jj < nt; ++jj) {
         if (jj == 1 && k > 0) mbar_wait(&bars[C::B_O_EMPTY], (k - 1) & 1);
-        issue_s(it, jj % C::NB1);
-        if (elect_one()) tc_commit(&bars[C::B_KV_EMPTY + it % C::NS]);
-        __syncwarp();
+        issue_s1(jj % C::NB1);
       }
       if (nt == 1 && k > 0) mbar_wait(&bars[C::B_O_EMPTY], (k - 1) & 1);
       // pass 2: S tiles run up to NB2 ahead of the PV MMAs (S(ns) reuses the
@@ -257,7 +282,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       const int it2 = it;
       for (int ns = 0, np = 0; np < nt;) {
         if (ns < nt && ns <= np + C::NB2) {
-          issue_s(it2 + ns, ns % C::NB2);
+          issue_s1(ns % C::NB2);
           if (ns == nt - 1 && elect_one()) tc_commit(&bars[C::B_Q_EMPTY]);  // last read of Q
           __syncwarp();
           ++ns;
@@ -266,6 +291,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         const int pj = np++;
         const int pb = pc % C::NP;
         const int st = (it2 + pj) % C::NS;
+        mbar_wait(&bars[C::B_KV_FULL + st], ((it2 + pj) / C::NS) & 1);  // V^T (+ V^F) of this tile landed
         mbar_wait(&bars[C::B_P_FULL + pb], (pc / C::NP) & 1);
         ++pc;
         tc_fence_after();

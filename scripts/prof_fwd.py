@@ -7,13 +7,15 @@ from paper_2603_00040_b200 import _lib  # noqa: E402
 lib = _lib.load()
 fn = lib.aq_debug_fwd_profile
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-B, H, N, d, causal = 4, 32, 8192, 128, True
+B, H, N, d = (int(x) for x in sys.argv[1:5]) if len(sys.argv) > 4 else (4, 32, 8192, 128)
+causal = True
+train = os.environ.get("AQ_PROF_TRAIN", "0") == "1"
 q, k, v = (torch.randn(B, H, N, d, device="cuda").bfloat16() for _ in range(3))
-o, lse, _, ws = aq.attn_forward(q, k, v, causal=causal, train=False)
+o, lse, _, ws = aq.attn_forward(q, k, v, causal=causal, train=train)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
 fn(buf, 1)
-aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, operands_staged=True)
+aq.attn_forward(q, k, v, causal=causal, train=train, workspace=ws, operands_staged=True)
 torch.cuda.synchronize()
 fn(buf, 0)
 v = list(buf)
