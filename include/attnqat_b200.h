@@ -147,6 +147,9 @@ double aq_probe_mma_flops(int kind, int ctas, int rounds);
 /* Cycle counters of the forward softmax warps (filled when the environment
  * sets AQ_FWD_DEBUG bit 32; tuning aid). out: 16 counters. */
 int aq_debug_fwd_profile(unsigned long long* out, int reset);
+/* Cycle counters of the backward compute warps (library built with
+ * -DAQ_BWD_PROFILE; tuning aid). out: 16 counters. */
+int aq_debug_bwd_profile(unsigned long long* out, int reset);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,15 @@ namespace aq {
 
 namespace bwd {
 
+// Tuning aid (-DAQ_BWD_PROFILE): cycle sums per compute-warp segment, lane 0
+// of every compute warp; [0..7] KV role, [8..13] Q role, [14] KV tiles, [15] Q tiles.
+__device__ unsigned long long g_bprof[16];
+#ifdef AQ_BWD_PROFILE
+#define AQ_BPROF(...) __VA_ARGS__
+#else
+#define AQ_BPROF(...)
+#endif
+
 // Compute warps: 4 TMEM row groups x NKG key groups. 16 warps hide more
 // latency but cap registers at 96/thread: d=64 gains 9%, d=128 loses 2%
 // (spills), so the count is per head dim.
@@ -343,6 +352,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     const float sl2 = p.scale_log2;
     uint8_t* p_h = smem + L::P_H;
     uint8_t* ds_h = smem + L::DS_H;
+    AQ_BPROF(unsigned long long pr_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long tq_ = clock64();)
     // per-row L and D of the next query tile are loaded one tile ahead, so the
     // global-load latency never sits between S_FULL and the exponentials
     auto row_stats = [&](int t, float& l2, float& dq) {
@@ -363,35 +373,46 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       if (p.causal) kmax = min(kmax, q + offset);
       const int64_t lim = qvalid ? kmax - (k0 + kb) : -1;  // visible keys: c <= lim
       float pr[KPT];
+      AQ_BPROF(tq_ = clock64();)
       mbar_wait(&bars[KV_B_S_FULL], ph);
       tc_fence_after();
       tmem_load_f<KPT>(t_lane + KV_T_S + kb, pr);
       tc_fence_before();
       mbar_arrive(&bars[KV_B_S_EMPTY]);
+      AQ_BPROF(long long tn_ = clock64(); pr_[0] += tn_ - tq_; tq_ = tn_;)
       // P = exp(S - L) exactly as the forward computes it
       p_from_s<KPT / 2>(pr, kb, sl2, L2);
       if (lim < KPT - 1) {
 #pragma unroll
         for (int c = 0; c < KPT; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
+      AQ_BPROF(tn_ = clock64(); pr_[1] += tn_ - tq_; tq_ = tn_;)
       if (ii > 0) mbar_wait(&bars[KV_B_PF_FREE], (ii - 1) & 1);
+      AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       // P^F (or P) -> bf16 [query][key] T8x8
 #pragma unroll
       for (int blk = 0; blk < KPT / 16; ++blk) {
         uint4 w[2];
         if (p.fq_p) {
           const PBlock qb = quantize_p16(pr + blk * 16);
-          __half2 c[4];
-          const __half sh = __float2half_rn(qb.sv);
-          const __half2 s2 = __halves2half2(sh, sh);
+          // P^F in bf16 straight from the codes: byte-permute lookups of the
+          // E2M1 values' bf16 bytes, then one exact bf16x2 multiply by the
+          // decoded scale (code x E4M3 has <= 5 significant bits)
+          const __nv_bfloat16 sb = __float2bfloat16_rn(qb.sv);
+          const __nv_bfloat162 s2 = __halves2bfloat162(sb, sb);
 #pragma unroll
           for (int h8 = 0; h8 < 2; ++h8) {
-            e2m1x8_to_h2(qb.codes[h8], c);
             uint32_t o[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __half22float2(__hmul2(c[e], s2));
-              o[e] = pack_bf16(f.x, f.y);
+            for (int q4 = 0; q4 < 2; ++q4) {
+              const uint32_t sel = (qb.codes[h8] >> (16 * q4)) & 0xFFFFu;
+              const uint32_t lo = __byte_perm(0xC0800000u, 0xC0804000u, sel);  // low bytes of 0,.5,1,1.5 | 2,3,4,6
+              const uint32_t hi = __byte_perm(0x3F3F3F00u, 0x40404040u, sel);  // high bytes
+              uint32_t v01 = __byte_perm(lo, hi, 0x5140), v23 = __byte_perm(lo, hi, 0x7362);
+              const __nv_bfloat162 p01 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v01), s2);
+              const __nv_bfloat162 p23 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v23), s2);
+              o[2 * q4] = *reinterpret_cast<const uint32_t*>(&p01);
+              o[2 * q4 + 1] = *reinterpret_cast<const uint32_t*>(&p23);
             }
             w[h8] = make_uint4(o[0], o[1], o[2], o[3]);
           }
@@ -408,6 +429,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       }
       fence_async_smem();
       mbar_arrive(&bars[KV_B_PF_FULL]);
+      AQ_BPROF(tn_ = clock64(); pr_[3] += tn_ - tq_; tq_ = tn_;)
       // dS = (dP - D) . P / sqrt(d) -> bf16
       mbar_wait(&bars[KV_B_DP_FULL + dph], ph);
       tc_fence_after();
@@ -415,11 +437,15 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       tmem_load_f<KPT>(t_lane + KV_T_DP + kb % HALF, dp);
       tc_fence_before();
       mbar_arrive(&bars[KV_B_DP_EMPTY + dph]);
+      AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
       if (ii > 0) mbar_wait(&bars[KV_B_DS_FREE], (ii - 1) & 1);
+      AQ_BPROF(tn_ = clock64(); pr_[5] += tn_ - tq_; tq_ = tn_;)
       store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
       fence_async_smem();
       mbar_arrive(&bars[KV_B_DS_FULL]);
+      AQ_BPROF(tn_ = clock64(); pr_[6] += tn_ - tq_; tq_ = tn_;)
     }
+    AQ_BPROF(if (lane == 0) { for (int e = 0; e < 7; ++e) atomicAdd(&g_bprof[e], pr_[e]); atomicAdd(&g_bprof[14], static_cast<unsigned long long>(ni)); })
     // epilogue: dK, dV rows (thread = key row, D/NKG columns)
     if (ni > 0) {
       mbar_wait(&bars[KV_B_DONE], 0);
@@ -640,31 +666,39 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     int64_t kmax = p.n_k - 1;
     if (p.causal) kmax = min(kmax, q + offset);
     uint8_t* ds_h = smem + L::DS_H;
+    AQ_BPROF(unsigned long long pr_[6] = {0, 0, 0, 0, 0, 0}; long long tq_ = clock64();)
     for (int j = 0; j < nt; ++j) {
       const uint32_t ph = j & 1;
       const int64_t lim = qvalid ? kmax - (static_cast<int64_t>(j) * TILE + kb) : -1;
       float pr[KPT];
+      AQ_BPROF(tq_ = clock64();)
       mbar_wait(&bars[Q_B_S_FULL], ph);
       tc_fence_after();
       tmem_load_f<KPT>(t_lane + Q_T_S + kb, pr);
       tc_fence_before();
       mbar_arrive(&bars[Q_B_S_EMPTY]);
+      AQ_BPROF(long long tn_ = clock64(); pr_[0] += tn_ - tq_; tq_ = tn_;)
       p_from_s<KPT / 2>(pr, kb, sl2, L2);
       if (lim < KPT - 1) {
 #pragma unroll
         for (int c = 0; c < KPT; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
+      AQ_BPROF(tn_ = clock64(); pr_[1] += tn_ - tq_; tq_ = tn_;)
       mbar_wait(&bars[Q_B_DP_FULL], ph);
       tc_fence_after();
       float dp[KPT];
       tmem_load_f<KPT>(t_lane + Q_T_DP + kb, dp);
       tc_fence_before();
       mbar_arrive(&bars[Q_B_DP_EMPTY]);
+      AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       if (j > 0) mbar_wait(&bars[Q_B_DS_EMPTY], (j - 1) & 1);
+      AQ_BPROF(tn_ = clock64(); pr_[3] += tn_ - tq_; tq_ = tn_;)
       store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
       fence_async_smem();
       mbar_arrive(&bars[Q_B_DS_FULL]);
+      AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
     }
+    AQ_BPROF(if (lane == 0) { for (int e = 0; e < 5; ++e) atomicAdd(&g_bprof[8 + e], pr_[e]); atomicAdd(&g_bprof[15], static_cast<unsigned long long>(nt)); })
     // epilogue: dQ rows (thread = query row, D/NKG columns), written once in the output dtype
     if (nt > 0) {
       mbar_wait(&bars[Q_B_DONE], 0);
@@ -785,6 +819,15 @@ cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st) {
   if (p.d == 64) return bwd::launch<64>(p, st);
   if (p.d == 128) return bwd::launch<128>(p, st);
   return cudaErrorInvalidValue;
+}
+
+extern "C" int aq_debug_bwd_profile(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, bwd::g_bprof, sizeof(bwd::g_bprof)) != cudaSuccess) return 5;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(bwd::g_bprof, z, sizeof(z)) != cudaSuccess) return 5;
+  }
+  return 0;
 }
 
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
