@@ -33,7 +33,10 @@ namespace aq {
 namespace gemm {
 
 constexpr int BM = 128, BN = 128, BK = 128;  // output tile, K slab
-constexpr int NST = 6;                         // ring stages
+#ifndef AQ_FP4MM_STAGES
+#define AQ_FP4MM_STAGES 11
+#endif
+constexpr int NST = AQ_FP4MM_STAGES;           // ring stages (bytes in flight per SM = NST x 18 KB)
 constexpr int CODE_SLAB = TILE * BK / 2;       // 8 KB: 4 K-chunks of a 128-row T8x32 tile
 constexpr int SF_SLAB = (BK / 64) * 512;       // 1 KB: 2 SF512 images
 constexpr int STAGE = 2 * (CODE_SLAB + SF_SLAB);
