@@ -39,6 +39,7 @@ class HostPipeline:
         self.bufs = {}                  # name -> [slot0, slot1]
         self.in_free = [None, None]     # compute finished reading input slot s
         self.out_free = [None, None]    # download finished reading output slot s
+        self.lock = threading.Lock()    # one pipelined call at a time per device (shared slots)
 
     def slots(self, name, shape, dtype):
         """Two device buffers of at least ``shape``; reallocated (after a device
@@ -84,6 +85,11 @@ def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device
     if any(t.shape[0] != heads for t in list(host_inputs) + list(host_outputs)):
         raise ValueError("all host buffers need the same leading (head) dimension")
     pipe = pipeline(device)
+    with pipe.lock:
+        _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch)
+
+
+def _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch):
     chunk_heads = max(1, min(int(chunk_heads), heads))
     host_inputs = [_pinned(t.contiguous()) for t in host_inputs]
     comp = torch.cuda.current_stream(pipe.device)
