@@ -70,17 +70,21 @@ struct Block16 {
   bool finite;
 };
 
-template <bool WANT_FQ>
+template <bool WANT_FQ, bool CHECK_FINITE = true>
 __device__ __forceinline__ void quantize_block16(const float (&v)[16], Block16& out) {
   float a[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) a[j] = fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1]));
   const float amax = fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
   // fmaxf drops NaN, so test finiteness separately: x * 0 is NaN for NaN / inf
-  float2 z = make_float2(0.f, 0.f);
+  if (CHECK_FINITE) {
+    float2 z = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < 16; j += 2) z = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(0.f, 0.f), z);
-  out.finite = (z.x + z.y == 0.f);
+    for (int j = 0; j < 16; j += 2) z = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(0.f, 0.f), z);
+    out.finite = (z.x + z.y == 0.f);
+  } else {
+    out.finite = true;
+  }
   const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);  // = fl(amax / 6)
   uint32_t sc = cvt_e4m3(raw);
   if (sc == 0 && amax > 0.f) sc = 1;  // tiny non-zero block keeps 2^-9 (codec.py:175-176)
@@ -217,6 +221,45 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
   }
 }
 
+// K1 fast path: the attention staging case only -- bf16 rows, whole 128-row
+// tiles (n % 128 == 0, contiguous heads), MMA tile outputs only. No per-block
+// output-pointer branches, no reference-layout or fake-quant stores: one
+// thread = 32 columns (two blocks) of one row, one 16-byte code store and one
+// 2-byte scale store.
+template <int D>
+__global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                                  uint8_t* __restrict__ codes_t,
+                                                                  uint8_t* __restrict__ sf_t) {
+  constexpr int NPAIR = D / 32;
+  const int64_t total = rows * NPAIR;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int bp = static_cast<int>(t & (NPAIR - 1));
+    const int64_t row = t / NPAIR;
+    const int64_t tile = row / TILE;
+    const int rr = static_cast<int>(row % TILE);
+    const uint4* src = reinterpret_cast<const uint4*>(x + row * D + bp * 32);
+    const uint4 w[4] = {src[0], src[1], src[2], src[3]};
+    Block16 q[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t ww[8] = {w[2 * h].x, w[2 * h].y, w[2 * h].z, w[2 * h].w,
+                              w[2 * h + 1].x, w[2 * h + 1].y, w[2 * h + 1].z, w[2 * h + 1].w};
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[2 * j] = __uint_as_float(ww[j] << 16);
+        v[2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
+      }
+      quantize_block16<false, false>(v, q[h]);
+    }
+    *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, bp * 32, TILE)) =
+        make_uint4(q[0].packed[0], q[0].packed[1], q[1].packed[0], q[1].packed[1]);
+    *reinterpret_cast<uint16_t*>(sf_t + tile * sf_tile_bytes_qk(D) + sf512_off(rr, 2 * bp)) =
+        static_cast<uint16_t>(q[0].scale | (q[1].scale << 8));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: blocks along the token axis (the V operand, quantized as V^T with the
 // token tail zero-padded to a multiple of 16; codec.py:359-381). x is
@@ -232,6 +275,60 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kColsSlab = 64;   // tokens per CTA step (4 blocks of 16)
 constexpr int kColsMax = 128;   // columns staged per pass
+
+// K2 fast path: the attention staging case only -- bf16 V, whole 128-token
+// tiles, contiguous heads, MMA tile outputs (V^T codes + scales) only. A CTA
+// stages 64 tokens x D columns as bf16 in shared memory (16-byte loads); a
+// thread then owns a column pair x 32 tokens: 32 four-byte shared loads give
+// both columns' 32 values, four blocks are quantized, and each column's 32
+// codes leave as one 16-byte store (plus one 2-byte scale store).
+template <int D>
+__global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads,
+                                                                  int64_t n, uint8_t* __restrict__ codes_t,
+                                                                  uint8_t* __restrict__ sf_t) {
+  constexpr int SLAB = 64, PITCH = D + 8;  // tokens per CTA step; padded row (bf16 elements)
+  __shared__ __align__(16) __nv_bfloat16 slab[SLAB][PITCH];
+  const int64_t tiles = n / TILE;
+  const int64_t nslabs = heads * tiles * (TILE / SLAB);
+  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
+    const int64_t tok0 = sidx * SLAB;  // flat token index over all heads (tiles never straddle heads)
+    __syncthreads();
+    constexpr int CV = D / 8;           // 16-byte vectors per token row
+#pragma unroll
+    for (int k = 0; k < SLAB * CV / 128; ++k) {
+      const int i = threadIdx.x + k * 128;
+      const int tt = i / CV, c = (i % CV) * 8;
+      *reinterpret_cast<uint4*>(&slab[tt][c]) = *reinterpret_cast<const uint4*>(x + (tok0 + tt) * D + c);
+    }
+    __syncthreads();
+    const int64_t tile = tok0 / TILE;
+    const int kt0 = static_cast<int>(tok0 % TILE);
+    for (int wi = threadIdx.x; wi < (D / 2) * (SLAB / 32); wi += blockDim.x) {
+      const int cp = wi % (D / 2);     // column pair
+      const int g32 = wi / (D / 2);    // 32-token group
+      float v0[32], v1[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(&slab[g32 * 32 + j][2 * cp]);
+        v0[j] = __uint_as_float(w << 16);
+        v1[j] = __uint_as_float(w & 0xFFFF0000u);
+      }
+      const int kt = kt0 + g32 * 32;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const float* v = cc ? v1 : v0;
+        Block16 qa, qb;
+        quantize_block16<false, false>(*reinterpret_cast<const float(*)[16]>(v), qa);
+        quantize_block16<false, false>(*reinterpret_cast<const float(*)[16]>(v + 16), qb);
+        const int col = 2 * cp + cc;
+        *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(col, kt, D)) =
+            make_uint4(qa.packed[0], qa.packed[1], qb.packed[0], qb.packed[1]);
+        *reinterpret_cast<uint16_t*>(sf_t + tile * kSfTileBytesV + sf512_off(col, kt / 16)) =
+            static_cast<uint16_t>(qa.scale | (qb.scale << 8));
+      }
+    }
+  }
+}
 
 template <bool WANT_FQ>
 __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
@@ -399,6 +496,17 @@ static int grid_for(int64_t work) {
 
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
+  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fqh_t && !a.fq && !a.codes_ref &&
+                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+  if (fast) {
+    const int64_t rows = a.heads * a.n;
+    const int g = grid_for(rows * (a.cols / 32));
+    const auto* x = static_cast<const __nv_bfloat16*>(a.x);
+    if (a.cols == 128) quantize_rows_tiled_kernel<128><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t);
+    else quantize_rows_tiled_kernel<64><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t);
+    return cudaGetLastError();
+  }
   const int g = grid_for(a.heads * n_pad * ((a.cols / 16 + 1) / 2));
   const bool fq = a.fq || a.fqh_t;
   if (a.cols == 128) {
@@ -415,6 +523,17 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
+  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fqh_t && !a.fqh2_t && !a.fq && !a.codes_ref &&
+                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+  if (fast) {
+    int64_t g = a.heads * (a.n / 64);
+    if (g > 148 * 64) g = 148 * 64;
+    const auto* x = static_cast<const __nv_bfloat16*>(a.x);
+    if (a.cols == 128) quantize_cols_tiled_kernel<128><<<static_cast<int>(g), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+    else quantize_cols_tiled_kernel<64><<<static_cast<int>(g), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+    return cudaGetLastError();
+  }
   const bool tiled = a.codes_t || a.sf_t || a.fqh_t || a.fqh2_t;
   const int64_t nslabs = tiled ? ceil_div(a.n, TILE) * (TILE / kColsSlab) : ceil_div(a.n, kColsSlab);
   int64_t g = a.heads * nslabs;

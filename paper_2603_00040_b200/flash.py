@@ -245,7 +245,7 @@ def _host_empty(shape, dtype, like=None):
 
 
 def attn_forward_host(q, k, v, causal=False, train=False, out=None, lse_out=None, o_hp_out=None,
-                      out_dtype=None, chunk_heads=None):
+                      out_dtype=None, chunk_heads=None, sync=True):
     """Forward from host tensors [..., N, d] into host outputs -> (O, L, O' or None).
 
     Same math as ``attn_forward`` (train selects flash_forward_training vs
@@ -273,14 +273,14 @@ def attn_forward_host(q, k, v, causal=False, train=False, out=None, lse_out=None
     def fn(dev, res, scr):
         attn_forward(dev[0], dev[1], dev[2], causal=causal, train=train, out_dtype=out_dtype, out=res[0],
                      lse_out=res[1], o_hp_out=res[2] if train else None, workspace=scr[0])
-    run_pipelined(fn, [q3, k3, v3], outs, chunk, scratch=[("fwd_ws", ws_bytes, torch.uint8)])
+    run_pipelined(fn, [q3, k3, v3], outs, chunk, scratch=[("fwd_ws", ws_bytes, torch.uint8)], sync=sync)
     lead = q.shape[:-2]
     return (o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q),
             outs[2].reshape(*lead, n_q, d) if train else None)
 
 
 def attn_qat_host(q, k, v, d_o, causal=False, variant=BwdVariant.CORRECT, out=None, grads_out=None,
-                  chunk_heads=None):
+                  chunk_heads=None, sync=True):
     """One QAT attention training step from host tensors: forward (O, O', L) and
     backward (dQ, dK, dV) per head chunk, H2D / kernels / D2H overlapped.
     Returns (O, dQ, dK, dV) in host memory."""
@@ -314,7 +314,7 @@ def attn_qat_host(q, k, v, d_o, causal=False, variant=BwdVariant.CORRECT, out=No
                      lse_out=lse_d, workspace=scr[0])
         attn_backward(qd, kd, vd, dod, res[0], o_hp_d, lse_d, causal=causal, variant=variant, grad_dtype=dt,
                       fwd_workspace=scr[0], workspace=scr[1], grads_out=res[1:])
-    run_pipelined(fn, [q3, k3, v3, do3], [o, dq, dk, dv], chunk, scratch=scratch)
+    run_pipelined(fn, [q3, k3, v3, do3], [o, dq, dk, dv], chunk, scratch=scratch, sync=sync)
     lead = q.shape[:-2]
     return (o.reshape(*lead, n_q, d), dq.reshape(*lead, n_q, d), dk.reshape(*lead, n_k, d),
             dv.reshape(*lead, n_k, d))

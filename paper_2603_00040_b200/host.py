@@ -14,9 +14,10 @@ kernels, so a call costs about max(H2D, D2H, compute) plus one chunk of each
 instead of their sum. All device memory is owned by a per-device
 ``HostPipeline``: two input slots, two output slots and two kernel workspaces,
 allocated once and recycled under events (no allocator traffic per chunk, no
-host synchronisation inside or between calls). The call returns once the last
-download is queued; the caller's current stream is made to wait for it, so
-stream-ordered timing and ``synchronize`` both see the whole transfer.
+host synchronisation inside or between calls). By default the call returns
+once the host outputs are complete (host memory in, host memory out, like the
+reference); with ``sync=False`` it returns once the last download is queued
+and the caller's current stream is made to wait for it.
 """
 
 from __future__ import annotations
@@ -69,7 +70,7 @@ def _pinned(t):
     return t if t.is_pinned() else t.pin_memory()
 
 
-def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device=None):
+def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device=None, sync=True):
     """Run ``fn`` over head chunks of host tensors with overlapped transfers.
 
     host_inputs:  CPU tensors whose dim 0 is the head index (same length H).
@@ -80,6 +81,10 @@ def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device
                   double-buffered like the slots.
     fn(dev_inputs, dev_outputs, dev_scratch) writes chunk results into
                   dev_outputs (views shaped like host_output[lo:hi]).
+    sync:         wait for the last download before returning, so the host
+                  outputs can be read at once (the reference contract). With
+                  sync=False the caller's current stream is only made to wait
+                  for it: read the outputs after synchronising that stream.
     """
     heads = host_inputs[0].shape[0]
     if any(t.shape[0] != heads for t in list(host_inputs) + list(host_outputs)):
@@ -87,6 +92,8 @@ def run_pipelined(fn, host_inputs, host_outputs, chunk_heads, scratch=(), device
     pipe = pipeline(device)
     with pipe.lock:
         _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch)
+    if sync:
+        torch.cuda.current_stream(pipe.device).synchronize()
 
 
 def _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch):

@@ -162,7 +162,7 @@ def load_kv4(prefix, device="cuda") -> KV4Cache:
 
 
 def attn_forward_kv4_host(q, cache: KV4Cache, causal=False, out=None, lse_out=None, out_dtype=None,
-                          chunk_heads=None):
+                          chunk_heads=None, sync=True):
     """FP4-KV-cache inference from host memory: q [..., n_q, d] and a KV4Cache
     on the host (pinned for overlap) -> host (O, L). Only Q (16-bit) and the
     4-bit cache cross PCIe -- 0.5625 B per cached K/V element instead of 2 --
@@ -191,6 +191,6 @@ def attn_forward_kv4_host(q, cache: KV4Cache, causal=False, out=None, lse_out=No
         attn_forward_kv4(dev[0], part, causal=causal, out=res[0], lse_out=res[1], workspace=scr[0],
                          out_dtype=out_dtype)
     run_pipelined(fn, [q3, cache.k_codes, cache.k_scales, cache.vt_codes, cache.vt_scales], [o, lse], chunk,
-                  scratch=[("kv4_ws", *ws)])
+                  scratch=[("kv4_ws", *ws)], sync=sync)
     lead = q.shape[:-2]
     return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)
