@@ -226,10 +226,11 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 // output-pointer branches, no reference-layout or fake-quant stores: one
 // thread = 32 columns (two blocks) of one row, one 16-byte code store and one
 // 2-byte scale store.
-template <int D>
+template <int D, bool FQH>
 __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
                                                                   uint8_t* __restrict__ codes_t,
-                                                                  uint8_t* __restrict__ sf_t) {
+                                                                  uint8_t* __restrict__ sf_t,
+                                                                  uint8_t* __restrict__ fqh_t, int fqh_dt) {
   constexpr int NPAIR = D / 32;
   const int64_t total = rows * NPAIR;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -251,7 +252,18 @@ __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const __nv_bfl
         v[2 * j] = __uint_as_float(ww[j] << 16);
         v[2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
       }
-      quantize_block16<false, false>(v, q[h]);
+      quantize_block16<FQH, false>(v, q[h]);
+    }
+    if (FQH) {
+      // the 16-bit fake-quantized operand tile the backward reuses (T8x8)
+      uint8_t* base = fqh_t + tile * h_tile_bytes(D);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8)
+          *reinterpret_cast<uint4*>(base + t8x8_off(rr, bp * 32 + h * 16 + h8 * 8)) =
+              make_uint4(h2_to(q[h].fq[4 * h8], fqh_dt), h2_to(q[h].fq[4 * h8 + 1], fqh_dt),
+                         h2_to(q[h].fq[4 * h8 + 2], fqh_dt), h2_to(q[h].fq[4 * h8 + 3], fqh_dt));
     }
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, bp * 32, TILE)) =
         make_uint4(q[0].packed[0], q[0].packed[1], q[1].packed[0], q[1].packed[1]);
@@ -282,12 +294,16 @@ constexpr int kColsMax = 128;   // columns staged per pass
 // thread then owns a column pair x 32 tokens: 32 four-byte shared loads give
 // both columns' 32 values, four blocks are quantized, and each column's 32
 // codes leave as one 16-byte store (plus one 2-byte scale store).
-template <int D>
+template <int D, bool FQH>
 __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads,
                                                                   int64_t n, uint8_t* __restrict__ codes_t,
-                                                                  uint8_t* __restrict__ sf_t) {
-  constexpr int SLAB = 64, PITCH = D + 8;  // tokens per CTA step; padded row (bf16 elements)
+                                                                  uint8_t* __restrict__ sf_t, uint8_t* __restrict__ fqh_t,
+                                                                  int fqh_dt, uint8_t* __restrict__ fqh2_t,
+                                                                  int fqh2_dt) {
+  constexpr int SLAB = 64, PITCH = D + 8;  // tokens per CTA step; padded row (16-bit elements)
   __shared__ __align__(16) __nv_bfloat16 slab[SLAB][PITCH];
+  // training: the dequantized values, as f16 pairs, for the T8x8 operand tiles
+  __shared__ __align__(16) __half slab_h[FQH ? SLAB : 1][FQH ? PITCH : 8];
   const int64_t tiles = n / TILE;
   const int64_t nslabs = heads * tiles * (TILE / SLAB);
   for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
@@ -314,17 +330,46 @@ __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfl
         v1[j] = __uint_as_float(w & 0xFFFF0000u);
       }
       const int kt = kt0 + g32 * 32;
+      Block16 q[2][2];  // [column][16-token block]
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         const float* v = cc ? v1 : v0;
-        Block16 qa, qb;
-        quantize_block16<false, false>(*reinterpret_cast<const float(*)[16]>(v), qa);
-        quantize_block16<false, false>(*reinterpret_cast<const float(*)[16]>(v + 16), qb);
+        quantize_block16<FQH, false>(*reinterpret_cast<const float(*)[16]>(v), q[cc][0]);
+        quantize_block16<FQH, false>(*reinterpret_cast<const float(*)[16]>(v + 16), q[cc][1]);
         const int col = 2 * cp + cc;
         *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(col, kt, D)) =
-            make_uint4(qa.packed[0], qa.packed[1], qb.packed[0], qb.packed[1]);
+            make_uint4(q[cc][0].packed[0], q[cc][0].packed[1], q[cc][1].packed[0], q[cc][1].packed[1]);
         *reinterpret_cast<uint16_t*>(sf_t + tile * kSfTileBytesV + sf512_off(col, kt / 16)) =
-            static_cast<uint16_t>(qa.scale | (qb.scale << 8));
+            static_cast<uint16_t>(q[cc][0].scale | (q[cc][1].scale << 8));
+      }
+      if (FQH) {
+        // token-major f16 pairs (column 2cp, 2cp+1) of the dequantized values
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t a0 = *reinterpret_cast<const uint32_t*>(&q[0][b].fq[j]);
+            const uint32_t a1 = *reinterpret_cast<const uint32_t*>(&q[1][b].fq[j]);
+            const int tt = g32 * 32 + b * 16 + 2 * j;
+            *reinterpret_cast<uint32_t*>(&slab_h[tt][2 * cp]) = __byte_perm(a0, a1, 0x5410);
+            *reinterpret_cast<uint32_t*>(&slab_h[tt + 1][2 * cp]) = __byte_perm(a0, a1, 0x7632);
+          }
+      }
+    }
+    if (FQH) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < SLAB * CV; i += blockDim.x) {
+        const int tt = i % SLAB, c8 = (i / SLAB) * 8;
+        const uint4 w = *reinterpret_cast<const uint4*>(&slab_h[tt][c8]);
+        const __half2 h[4] = {*reinterpret_cast<const __half2*>(&w.x), *reinterpret_cast<const __half2*>(&w.y),
+                              *reinterpret_cast<const __half2*>(&w.z), *reinterpret_cast<const __half2*>(&w.w)};
+        const uint32_t off = static_cast<uint32_t>(tile * h_tile_bytes(D)) + t8x8_off(kt0 + tt, c8);
+        if (fqh_t)
+          *reinterpret_cast<uint4*>(fqh_t + off) =
+              make_uint4(h2_to(h[0], fqh_dt), h2_to(h[1], fqh_dt), h2_to(h[2], fqh_dt), h2_to(h[3], fqh_dt));
+        if (fqh2_t)
+          *reinterpret_cast<uint4*>(fqh2_t + off) =
+              make_uint4(h2_to(h[0], fqh2_dt), h2_to(h[1], fqh2_dt), h2_to(h[2], fqh2_dt), h2_to(h[3], fqh2_dt));
       }
     }
   }
@@ -496,15 +541,21 @@ static int grid_for(int64_t work) {
 
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
-  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fqh_t && !a.fq && !a.codes_ref &&
-                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
+                    !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
   if (fast) {
     const int64_t rows = a.heads * a.n;
     const int g = grid_for(rows * (a.cols / 32));
     const auto* x = static_cast<const __nv_bfloat16*>(a.x);
-    if (a.cols == 128) quantize_rows_tiled_kernel<128><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t);
-    else quantize_rows_tiled_kernel<64><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t);
+    uint8_t* fqh = static_cast<uint8_t*>(a.fqh_t);
+    if (a.cols == 128) {
+      if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt);
+      else quantize_rows_tiled_kernel<128, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0);
+    } else {
+      if (fqh) quantize_rows_tiled_kernel<64, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt);
+      else quantize_rows_tiled_kernel<64, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0);
+    }
     return cudaGetLastError();
   }
   const int g = grid_for(a.heads * n_pad * ((a.cols / 16 + 1) / 2));
@@ -523,15 +574,24 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
-  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fqh_t && !a.fqh2_t && !a.fq && !a.codes_ref &&
-                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
+                    !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
   if (fast) {
     int64_t g = a.heads * (a.n / 64);
     if (g > 148 * 64) g = 148 * 64;
     const auto* x = static_cast<const __nv_bfloat16*>(a.x);
-    if (a.cols == 128) quantize_cols_tiled_kernel<128><<<static_cast<int>(g), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
-    else quantize_cols_tiled_kernel<64><<<static_cast<int>(g), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+    const bool fqh = a.fqh_t || a.fqh2_t;
+    auto* h1 = static_cast<uint8_t*>(a.fqh_t);
+    auto* h2 = static_cast<uint8_t*>(a.fqh2_t);
+    const int gg = static_cast<int>(g);
+    if (a.cols == 128) {
+      if (fqh) quantize_cols_tiled_kernel<128, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt);
+      else quantize_cols_tiled_kernel<128, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0);
+    } else {
+      if (fqh) quantize_cols_tiled_kernel<64, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt);
+      else quantize_cols_tiled_kernel<64, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0);
+    }
     return cudaGetLastError();
   }
   const bool tiled = a.codes_t || a.sf_t || a.fqh_t || a.fqh2_t;
