@@ -749,49 +749,73 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
 }
 
 // K6: D = rowsum(dO . O_ref) (fp32) and dO -> bf16 T8x8 tiles (pad rows zero).
-// One thread per 8 columns of a row.
+// A warp owns 8 consecutive rows (one T8x8 core row group): lane = (row % 8,
+// column group c8 = lane / 8 + 4 i), so every 16-byte tile store of a warp
+// fills four contiguous 128-byte runs; the row sum is closed with two
+// shuffles over the four lanes that share a row.
+template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt, const void* o_ref, int o_dt,
-                                                      int64_t heads, int64_t n_q, int d, float* delta,
-                                                      uint8_t* do_h) {
-  const int per_row = d / 8;
+                                                      int64_t heads, int64_t n_q, float* delta, uint8_t* do_h) {
+  constexpr int NCG = D / 8;  // 16-byte column groups per row
   const int64_t q_tiles = ceil_div(n_q, TILE);
-  const int64_t rows = heads * q_tiles * TILE;
-  const int64_t total = rows * per_row;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c8 = static_cast<int>(t % per_row);
-    const int64_t rp = t / per_row;
+  const int64_t row_groups = heads * q_tiles * (TILE / 8);
+  const int lane = threadIdx.x % 32;
+  const int r8 = lane % 8, cg = lane / 8;
+  for (int64_t wg = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; wg < row_groups;
+       wg += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const int64_t rp = wg * 8 + r8;              // padded row over all heads
     const int64_t h = rp / (q_tiles * TILE);
     const int64_t q = rp % (q_tiles * TILE);
     const bool valid = q < n_q;
-    float g[8], o[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      g[e] = 0.f;
-      o[e] = 0.f;
-    }
-    if (valid) {
-      const int64_t base = (h * n_q + q) * d + c8 * 8;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (do_dt == 1) g[e] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d_o)[base + e]);
-        else if (do_dt == 2) g[e] = __half2float(reinterpret_cast<const __half*>(d_o)[base + e]);
-        else g[e] = reinterpret_cast<const float*>(d_o)[base + e];
-        if (o_dt == 1) o[e] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(o_ref)[base + e]);
-        else if (o_dt == 2) o[e] = __half2float(reinterpret_cast<const __half*>(o_ref)[base + e]);
-        else o[e] = reinterpret_cast<const float*>(o_ref)[base + e];
-      }
-    }
+    const int64_t base_row = (h * n_q + q) * D;
+    const int64_t tile = h * q_tiles + q / TILE;
+    uint8_t* tdst = do_h + tile * h_tile_bytes(D);
     float acc = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc = fmaf(g[e], o[e], acc);
-    // reduce across the per_row (8 or 16) consecutive lanes of this row
-    for (int off = per_row / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (c8 == 0) delta[rp] = acc;
-    const int64_t tile = h * q_tiles + q / TILE;
-    const uint4 w = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]),
-                               pack_bf16(g[6], g[7]));
-    *reinterpret_cast<uint4*>(do_h + tile * h_tile_bytes(d) + t8x8_off(static_cast<int>(q % TILE), c8 * 8)) = w;
+    for (int i = 0; i < NCG / 4; ++i) {
+      const int c8 = cg + 4 * i;
+      float g[8], o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] = o[e] = 0.f;
+      if (valid) {
+        const int64_t base = base_row + c8 * 8;
+        if (do_dt == 1) {
+          const uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(d_o) + base);
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            g[2 * e] = __uint_as_float(ww[e] << 16);
+            g[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            g[e] = do_dt == 2 ? __half2float(reinterpret_cast<const __half*>(d_o)[base + e])
+                              : reinterpret_cast<const float*>(d_o)[base + e];
+        }
+        if (o_dt == 1) {
+          const uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(o_ref) + base);
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            o[2 * e] = __uint_as_float(ww[e] << 16);
+            o[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            o[e] = o_dt == 2 ? __half2float(reinterpret_cast<const __half*>(o_ref)[base + e])
+                             : reinterpret_cast<const float*>(o_ref)[base + e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(g[e], o[e], acc);
+      *reinterpret_cast<uint4*>(tdst + t8x8_off(static_cast<int>(q % TILE), c8 * 8)) =
+          make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+    if (cg == 0) delta[rp] = acc;
   }
 }
 
@@ -833,9 +857,10 @@ extern "C" int aq_debug_bwd_profile(unsigned long long* out, int reset) {
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
                            int d, float* delta, uint8_t* do_h, cudaStream_t st) {
   const int64_t rows = heads * ceil_div(n_q, TILE) * TILE;
-  // per_row threads of a row must sit in one warp: 256-thread blocks, d/8 in {8, 16}
-  bwd::bwd_pre_kernel<<<bwd::grid_for(rows * (d / 8)), 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, d, delta,
-                                                                     do_h);
+  const int g = bwd::grid_for(rows * 4);  // 4 threads per row
+  if (d == 128) bwd::bwd_pre_kernel<128><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h);
+  else if (d == 64) bwd::bwd_pre_kernel<64><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
