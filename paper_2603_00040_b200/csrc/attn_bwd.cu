@@ -152,7 +152,7 @@ constexpr uint32_t KV_T_S = 0, KV_T_DK = 128, KV_T_DV = 256, KV_T_DP = 384, KV_T
 enum KvBar {
   KV_B_K = 0, KV_B_QC_FULL = 1, KV_B_QC_EMPTY = 3, KV_B_DO_FULL = 5, KV_B_DO_EMPTY = 7, KV_B_QH_FULL = 9,
   KV_B_QH_EMPTY, KV_B_S_FULL, KV_B_S_EMPTY, KV_B_DP_FULL, KV_B_DP_EMPTY = KV_B_DP_FULL + 2,
-  KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE
+  KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE, KV_B_V
 };
 
 // Schedule per query tile i (MMA warp, in issue order):
@@ -182,6 +182,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[KV_B_K], 1);
+    mbar_init(&bars[KV_B_V], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars[KV_B_QC_FULL + s], 1);
       mbar_init(&bars[KV_B_QC_EMPTY + s], 1);
@@ -211,10 +212,13 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     // ------------------------------------------------------------ producer
     const int64_t kidx = head * k_tiles + kt;
     if (elect_one()) {
-      mbar_expect_tx(&bars[KV_B_K], L::K_BYTES);
+      // K (needed by the first S) and V^F (needed by the first dP) on separate
+      // barriers, so the first S does not wait for the 32 KB V^F tile
+      mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
       bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
       bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
-      bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_K]);
+      mbar_expect_tx(&bars[KV_B_V], TILE * D * 2);
+      bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_V]);
     }
     __syncwarp();
     auto load_qc = [&](int t) {
@@ -312,6 +316,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       // dP = dO V^F^T, one 64-key half at a time, with S_{i+1} in between
       mbar_wait(&bars[KV_B_DO_FULL + s], (ii >> 1) & 1);
       if (ii > 0) mbar_wait(&bars[KV_B_DP_EMPTY + 1], ph ^ 1);
+      else mbar_wait(&bars[KV_B_V], 0);
       issue_dp(ii, 0, do_h);
       if (ii + 1 < ni) issue_s(ii + 1);
       mbar_wait(&bars[KV_B_DP_EMPTY + 0], ph);
@@ -500,7 +505,8 @@ constexpr uint32_t Q_T_S = 0, Q_T_DP = 128, Q_T_DQ = 256, Q_T_QSF = 384, Q_T_KSF
 
 enum QBar {
   Q_B_Q = 0, Q_B_KC_FULL = 1, Q_B_KC_EMPTY = 3, Q_B_VH_FULL = 5, Q_B_VH_EMPTY = 7, Q_B_KH_FULL = 9,
-  Q_B_KH_EMPTY = 11, Q_B_S_FULL = 13, Q_B_S_EMPTY, Q_B_DP_FULL, Q_B_DP_EMPTY, Q_B_DS_FULL, Q_B_DS_EMPTY, Q_B_DONE
+  Q_B_KH_EMPTY = 11, Q_B_S_FULL = 13, Q_B_S_EMPTY, Q_B_DP_FULL, Q_B_DP_EMPTY, Q_B_DS_FULL, Q_B_DS_EMPTY, Q_B_DONE,
+  Q_B_DOH
 };
 
 // MMA issue order: S_0 dP_0 | S_1 dP_1 dQ_0 | S_2 dP_2 dQ_1 | ... so S_{j+1} and
@@ -526,6 +532,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[Q_B_Q], 1);
+    mbar_init(&bars[Q_B_DOH], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars[Q_B_KC_FULL + s], 1);
       mbar_init(&bars[Q_B_KC_EMPTY + s], 1);
@@ -553,10 +560,11 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     // ------------------------------------------------------------ producer
     const int64_t qidx = head * q_tiles + qt;
     if (elect_one()) {
-      mbar_expect_tx(&bars[Q_B_Q], L::Q_BYTES);
+      mbar_expect_tx(&bars[Q_B_Q], TILE * D / 2 + (D / 64) * 512);
       bulk_g2s(smem + L::Q_CODES, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_Q]);
       bulk_g2s(smem + L::Q_SF, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_Q]);
-      bulk_g2s(smem + L::DO_H, p.do_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_Q]);
+      mbar_expect_tx(&bars[Q_B_DOH], TILE * D * 2);
+      bulk_g2s(smem + L::DO_H, p.do_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_DOH]);
     }
     __syncwarp();
     for (int j = 0; j < nt; ++j) {
@@ -623,6 +631,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       __syncwarp();
       mbar_wait(&bars[Q_B_VH_FULL + st], pf);
       if (j > 0) mbar_wait(&bars[Q_B_DP_EMPTY], (j - 1) & 1);
+      else mbar_wait(&bars[Q_B_DOH], 0);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t vh = s0 + L::VH0 + st * TILE * D * 2;
