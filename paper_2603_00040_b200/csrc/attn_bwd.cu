@@ -180,7 +180,8 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   }
   const int ni = q_tiles > i_begin ? q_tiles - i_begin : 0;
 
-  if (threadIdx.x == 0) {
+  const int64_t kidx = head * k_tiles + kt;
+  if (threadIdx.x == 32 * PRODUCER) {
     mbar_init(&bars[KV_B_K], 1);
     mbar_init(&bars[KV_B_V], 1);
     for (int s = 0; s < 2; ++s) {
@@ -201,6 +202,26 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     mbar_init(&bars[KV_B_DS_FREE], 1);
     mbar_init(&bars[KV_B_DONE], 1);
     fence_mbar_init();
+    // the stationary K / V^F tiles and the first query tile are requested
+    // before the CTA-wide sync, so their latency overlaps TMEM allocation.
+    // K (first S) and V^F (first dP) on separate barriers.
+    mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
+    bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
+    bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
+    if (ni > 0) {
+      const int64_t qidx = head * q_tiles + i_begin;
+      mbar_expect_tx(&bars[KV_B_QC_FULL], L::QC_BYTES);
+      bulk_g2s(smem + L::QC0, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_QC_FULL]);
+      bulk_g2s(smem + L::QC0 + TILE * D / 2, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512,
+               &bars[KV_B_QC_FULL]);
+    }
+    mbar_expect_tx(&bars[KV_B_V], TILE * D * 2);
+    bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_V]);
+    if (ni > 0) {
+      const int64_t qidx = head * q_tiles + i_begin;
+      mbar_expect_tx(&bars[KV_B_DO_FULL], TILE * D * 2);
+      bulk_g2s(smem + L::DO_H0, p.do_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_DO_FULL]);
+    }
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -210,17 +231,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
 
   if (warp == PRODUCER) {
     // ------------------------------------------------------------ producer
-    const int64_t kidx = head * k_tiles + kt;
-    if (elect_one()) {
-      // K (needed by the first S) and V^F (needed by the first dP) on separate
-      // barriers, so the first S does not wait for the 32 KB V^F tile
-      mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
-      bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
-      bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
-      mbar_expect_tx(&bars[KV_B_V], TILE * D * 2);
-      bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_V]);
-    }
-    __syncwarp();
+    // (K, V^F and query tile 0 were requested before the CTA-wide sync)
     auto load_qc = [&](int t) {
       const int s = t & 1;
       if (t >= 2) mbar_wait(&bars[KV_B_QC_EMPTY + s], ((t >> 1) - 1) & 1);
@@ -244,10 +255,6 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       }
       __syncwarp();
     };
-    if (ni > 0) {
-      load_qc(0);
-      load_do(0);
-    }
     for (int t = 0; t < ni; ++t) {
       if (t + 1 < ni) {
         load_qc(t + 1);
@@ -530,7 +537,8 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     nt = last < 0 ? 0 : min(nt, static_cast<int>(last / TILE) + 1);
   }
 
-  if (threadIdx.x == 0) {
+  const int64_t qidx0 = head * q_tiles + qt;
+  if (threadIdx.x == 32 * PRODUCER) {
     mbar_init(&bars[Q_B_Q], 1);
     mbar_init(&bars[Q_B_DOH], 1);
     for (int s = 0; s < 2; ++s) {
@@ -549,6 +557,19 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     mbar_init(&bars[Q_B_DS_EMPTY], 1);
     mbar_init(&bars[Q_B_DONE], 1);
     fence_mbar_init();
+    // stationary Q codes / dO and key tile 0 requested before the CTA-wide sync
+    mbar_expect_tx(&bars[Q_B_Q], TILE * D / 2 + (D / 64) * 512);
+    bulk_g2s(smem + L::Q_CODES, p.q_codes + qidx0 * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_Q]);
+    bulk_g2s(smem + L::Q_SF, p.q_sf + qidx0 * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_Q]);
+    if (nt > 0) {
+      const int64_t kidx = head * k_tiles;
+      mbar_expect_tx(&bars[Q_B_KC_FULL], L::KC_BYTES);
+      bulk_g2s(smem + L::KC0, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL]);
+      bulk_g2s(smem + L::KC0 + TILE * D / 2, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512,
+               &bars[Q_B_KC_FULL]);
+    }
+    mbar_expect_tx(&bars[Q_B_DOH], TILE * D * 2);
+    bulk_g2s(smem + L::DO_H, p.do_h + qidx0 * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_DOH]);
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -558,21 +579,13 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 
   if (warp == PRODUCER) {
     // ------------------------------------------------------------ producer
-    const int64_t qidx = head * q_tiles + qt;
-    if (elect_one()) {
-      mbar_expect_tx(&bars[Q_B_Q], TILE * D / 2 + (D / 64) * 512);
-      bulk_g2s(smem + L::Q_CODES, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_Q]);
-      bulk_g2s(smem + L::Q_SF, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_Q]);
-      mbar_expect_tx(&bars[Q_B_DOH], TILE * D * 2);
-      bulk_g2s(smem + L::DO_H, p.do_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_DOH]);
-    }
-    __syncwarp();
+    // (Q codes, dO and key tile 0's codes were requested before the CTA-wide sync)
     for (int j = 0; j < nt; ++j) {
       const int st = j & 1;
       const uint32_t pe = ((j >> 1) - 1) & 1;
       const int64_t kidx = head * k_tiles + j;
       if (j >= 2) mbar_wait(&bars[Q_B_KC_EMPTY + st], pe);
-      if (elect_one()) {
+      if (j > 0 && elect_one()) {
         uint8_t* dst = smem + L::KC0 + st * L::KC_BYTES;
         mbar_expect_tx(&bars[Q_B_KC_FULL + st], L::KC_BYTES);
         bulk_g2s(dst, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL + st]);
