@@ -330,6 +330,11 @@ def main():
                 "peak_source": "measured live: tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak)",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                 "path_ceiling_frac": achieved / (peaks["nvfp4"] * 2.0 / 3.0),
+                # the binding unit is the SFU: 2 exponentials per score (7/8 on MUFU.EX2) plus one
+                # reciprocal per 16-key block = 1.81 MUFU ops per score (ncu: 1.87 incl. merges),
+                # at 16 MUFU/clk/SM; the algorithmic FLOPs per score are 4 d
+                "sfu_ceiling_tflops": _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch),
+                "sfu_frac": achieved / _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch),
                 "traffic": _traffic_from_profiles(args.config)}
     else:
         roof = {"bound": "tensor", "kernel": "attn_fwd+attn_bwd", "achieved": value / world,
@@ -532,6 +537,14 @@ def run_layer_mode(args, cfg, rank, world, local):
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _sfu_ceiling(d, sm_mhz, torch):
+    """Forward TFLOP/s at which the MUFU (SFU) pipe saturates: 4 d algorithmic FLOPs per
+    score over 1.87 MUFU ops per score (ncu, profiles/) at 16 MUFU results / clk / SM."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mufu_per_s = 16.0 * sms * sm_mhz * 1e6
+    return 4.0 * d * mufu_per_s / 1.87 / 1e12
 
 
 def _traffic_from_profiles(config):
