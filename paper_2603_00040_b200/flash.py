@@ -107,6 +107,10 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
     high-precision output the QAT backward needs (flash.py:176-246).
     ``quantized=False`` is plain attention (O' = O; plain.py)."""
     _lib.require_cuda()
+    if q.device.type == "cuda" and q.device.index is not None and q.device.index != torch.cuda.current_device():
+        with torch.cuda.device(q.device):  # launch on (and with the current stream of) q's device
+            return attn_forward(q, k, v, causal, train, out_dtype, keep_for_bwd, lse_out, workspace,
+                                operands_staged, out, o_hp_out, quantized)
     if not quantized:
         return _plain_forward(q, k, v, causal, train, out_dtype)
     q3, n_q, d = _heads_view(q)
@@ -158,6 +162,10 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
                   fwd_workspace=None, workspace=None, grads_out=None, quantized=True):
     """Fused QAT backward on CUDA tensors -> (dQ, dK, dV) (flash.py:317-390)."""
     _lib.require_cuda()
+    if q.device.type == "cuda" and q.device.index is not None and q.device.index != torch.cuda.current_device():
+        with torch.cuda.device(q.device):
+            return attn_backward(q, k, v, d_o, o, o_hp, lse, causal, variant, grad_dtype, fwd_workspace,
+                                 workspace, grads_out, quantized)
     q3, n_q, d = _heads_view(q)
     k3, n_k, _ = _heads_view(k)
     v3, _, _ = _heads_view(v)
