@@ -69,6 +69,18 @@ int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64
  * *invalid is set for non-finite input (and negative input for E4M3). */
 int aq_round_codes(const void* x, int x_dtype, int64_t n, int format, uint8_t* codes, int* invalid, void* stream);
 
+/* MXFP4 (BlockSpec(32, E8M0), codec.py:123-203): quantize(x, MXFP4) /
+ * fake_quantize(x, MXFP4) / dequantize of an MXFP4 QuantTensor. x [rows][cols]
+ * (cols % 32 == 0); codes [rows][cols/2], scales [rows][cols/32] (E8M0). */
+int aq_quantize_mx(const void* x, int x_dtype, int64_t rows, int64_t cols, uint8_t* codes, uint8_t* scales,
+                   void* fq, int fq_dtype, int* nonfinite, void* stream);
+int aq_dequantize_mx(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
+                     int out_dtype, void* stream);
+/* Replaces attnqat.codec.round_to_e8m0 (codec.py:123-136): nearest power of two,
+ * ties up, code clamped to 0..254; x_dtype 0 = fp32, 3 = fp64; *invalid set for
+ * non-finite or non-positive input. */
+int aq_e8m0_codes(const void* x, int x_dtype, int64_t n, uint8_t* codes, int* invalid, void* stream);
+
 /* Replaces attnqat.codec.dequantize (codec.py:327-333). rows x cols. */
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
                   int out_dtype, void* stream);

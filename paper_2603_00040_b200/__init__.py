@@ -9,7 +9,8 @@ a C ABI); there is no CPU fallback.
 from .autograd import AttnQATFunction, attn_qat
 from .codec import (MXFP4, NVFP4, BlockSpec, Fp4Block, QuantTensor, ScaleFormat, decode_e4m3, decode_fp4, dequantize,
                     dequantize_block, encode_fp4, fake_quantize, fake_quantize_cols, fake_quantize_padded, quantize,
-                    quantize_block, quantize_cols, quantize_padded, round_to_e4m3, round_to_fp4)
+                    quantize_block, quantize_cols, quantize_padded, round_to_e4m3, round_to_e8m0, round_to_fp4,
+                    decode_e8m0)
 from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, ShapeError, StabilityError,
                      TileError)
 from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward, attn_forward_host,

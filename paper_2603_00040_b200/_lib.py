@@ -57,6 +57,9 @@ PROTOTYPES = {
     "aq_dequantize": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_vp]),
     "aq_fp4mm_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
     "aq_fp4mm": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "aq_quantize_mx": (c_int, [c_vp, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
+    "aq_dequantize_mx": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_vp]),
+    "aq_e8m0_codes": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_vp]),
     "aq_round_codes": (c_int, [c_vp, c_int, c_i64, c_int, c_vp, c_vp, c_vp]),
     "aq_attn_fwd_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_int, c_int]),
     "aq_attn_fwd": (c_int, [ctypes.POINTER(AqFwdArgs), c_vp]),

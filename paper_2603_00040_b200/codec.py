@@ -100,8 +100,29 @@ def _nonfinite_check(flag):
         raise InvalidValue("quantize requires finite input")
 
 
+def _quantize_mx(t, codes=None, scales=None, fq=None):
+    rows, cols = t.shape
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_quantize_mx(_lib.ptr(t), _lib.DT_CODE[t.dtype], rows, cols, _lib.ptr(codes),
+                                          _lib.ptr(scales), _lib.ptr(fq), _lib.DT_CODE[fq.dtype] if fq is not None else 0,
+                                          _lib.ptr(flag), _lib.stream_ptr()))
+    _nonfinite_check(flag)
+
+
 def quantize(x, spec=NVFP4) -> QuantTensor:
-    """Block-row-wise NVFP4 quantization (codec.py:302-324)."""
+    """Block-row-wise NVFP4 / MXFP4 quantization (codec.py:302-324)."""
+    if spec == MXFP4:
+        t, was_np = to_device(x)
+        if t.dim() != 2:
+            raise ShapeError("quantize expects a 2-D tensor")
+        rows, cols = t.shape
+        if cols % 32:
+            raise ShapeError(f"cols ({cols}) must be a multiple of block_size (32);"
+                             " padding is the caller's responsibility")
+        codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=t.device)
+        scales = torch.empty((rows, cols // 32), dtype=torch.uint8, device=t.device)
+        _quantize_mx(t, codes=codes, scales=scales)
+        return QuantTensor(rows, cols, spec, _out(codes, was_np), _out(scales, was_np))
     _require_nvfp4(spec)
     t, was_np = to_device(x)
     if t.dim() != 2:
@@ -130,6 +151,10 @@ def dequantize(qt: QuantTensor, dtype=np.float32):
     scales = torch.as_tensor(np.ascontiguousarray(qt.scales) if was_np else qt.scales).to("cuda").contiguous()
     tdt = dtype if isinstance(dtype, torch.dtype) else _NP2T.get(np.dtype(dtype).type, torch.float32)
     out = torch.empty((qt.rows, qt.cols), dtype=tdt, device="cuda")
+    if qt.spec == MXFP4:
+        _lib.check(_lib.load().aq_dequantize_mx(_lib.ptr(codes), _lib.ptr(scales), qt.rows, qt.cols, _lib.ptr(out),
+                                                _lib.DT_CODE[tdt], _lib.stream_ptr()))
+        return _out(out, was_np, None if isinstance(dtype, torch.dtype) else dtype)
     _lib.check(_lib.load().aq_dequantize(_lib.ptr(codes), _lib.ptr(scales), qt.rows, qt.cols,
                                          _lib.ptr(out), _lib.DT_CODE[tdt], _lib.stream_ptr()))
     return _out(out, was_np, None if isinstance(dtype, torch.dtype) else dtype)
@@ -137,6 +162,15 @@ def dequantize(qt: QuantTensor, dtype=np.float32):
 
 def fake_quantize(x, spec=NVFP4):
     """Quantize-then-dequantize, shape and dtype preserved (codec.py:336-340)."""
+    if spec == MXFP4:
+        t, was_np = to_device(x)
+        if t.dim() != 2:
+            raise ShapeError("quantize expects a 2-D tensor")
+        if t.shape[1] % 32:
+            raise ShapeError(f"cols ({t.shape[1]}) must be a multiple of block_size (32)")
+        out = torch.empty_like(t)
+        _quantize_mx(t, fq=out)
+        return _out(out, was_np, np.asarray(x).dtype if was_np else None)
     _require_nvfp4(spec)
     t, was_np = to_device(x)
     if t.dim() != 2:
@@ -181,6 +215,11 @@ def fake_quantize_padded(x, spec=NVFP4):
 
 def fake_quantize_cols(x, spec=NVFP4):
     """Blocks along the token (row) axis, ragged tail zero-padded (codec.py:373-381)."""
+    if spec == MXFP4:
+        t, was_np = to_device(x)
+        n = t.shape[0]
+        out = fake_quantize_padded(t.t().contiguous(), MXFP4)[:, :n].t().contiguous()
+        return _out(out, was_np, np.asarray(x).dtype if was_np else None)
     _require_nvfp4(spec)
     t, was_np = to_device(x)
     if t.dim() != 2:
@@ -307,7 +346,8 @@ class Fp4Block:
 
 def quantize_block(x, spec=NVFP4) -> Fp4Block:
     """One block of block_size finite reals -> Fp4Block (codec.py:239-248), on the GPU quantizer."""
-    _require_nvfp4(spec)
+    if spec not in (NVFP4, MXFP4):
+        raise InvalidValue(f"unsupported block spec {spec}")
     arr = np.asarray(x.detach().cpu() if isinstance(x, torch.Tensor) else x, dtype=np.float64)
     if arr.shape != (spec.block_size,):
         raise ShapeError(f"block must have exactly {spec.block_size} elements")
@@ -320,8 +360,45 @@ def quantize_block(x, spec=NVFP4) -> Fp4Block:
 
 def dequantize_block(block: Fp4Block):
     """Fp4Block -> block_size float64 reals (scale x code, exact; codec.py:251-258)."""
-    _require_nvfp4(block.spec)
     codes = np.frombuffer(block.codes, dtype=np.uint8).reshape(1, -1)
     scales = np.array([[block.scale]], dtype=np.uint8)
     qt = QuantTensor(1, block.spec.block_size, block.spec, codes, scales)
     return np.asarray(dequantize(qt, np.float64), dtype=np.float64).reshape(-1)
+
+
+def round_to_e8m0(x):
+    """Nearest power of two of a positive value, ties up -> E8M0 code clamped to
+    0..254 (codec.py:123-136). Exact in the input precision."""
+    was_np = not isinstance(x, torch.Tensor)
+    arr = np.asarray(x, dtype=np.float64) if was_np else None
+    t = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1))) if was_np else x.reshape(-1)
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float32)
+    _lib.require_cuda()
+    t = t.to("cuda").contiguous()
+    codes = torch.empty(t.numel(), dtype=torch.uint8, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.check(_lib.load().aq_e8m0_codes(_lib.ptr(t), 3 if t.dtype == torch.float64 else 0, t.numel(),
+                                         _lib.ptr(codes), _lib.ptr(flag), _lib.stream_ptr()))
+    if int(flag.item()):
+        raise InvalidValue("round_to_e8m0 requires finite positive input")
+    if not was_np:
+        return codes.reshape(x.shape)
+    out = codes.cpu().numpy().reshape(arr.shape)
+    return out if arr.ndim else out[()]
+
+
+E8M0_DECODE = np.ldexp(1.0, np.arange(256) - 127)
+E8M0_DECODE[255] = np.nan
+
+
+def decode_e8m0(codes):
+    """E8M0 codes -> 2^(code - 127); the NaN code 0xFF is rejected (codec.py:138-142)."""
+    if isinstance(codes, torch.Tensor):
+        if bool((codes == 0xFF).any()):
+            raise InvalidValue("NaN E8M0 code cannot be used as a scale")
+        return torch.as_tensor(E8M0_DECODE, device=codes.device)[codes.long()]
+    c = np.asarray(codes, dtype=np.uint8)
+    if np.any(c == 0xFF):
+        raise InvalidValue("NaN E8M0 code cannot be used as a scale")
+    return E8M0_DECODE[c]

@@ -180,6 +180,30 @@ int aq_round_codes(const void* x, int x_dtype, int64_t n, int format, uint8_t* c
   return cuda_status(launch_round_codes(x, x_dtype == 3, n, format, codes, invalid, static_cast<cudaStream_t>(stream)));
 }
 
+int aq_quantize_mx(const void* x, int x_dtype, int64_t rows, int64_t cols, uint8_t* codes, uint8_t* scales,
+                   void* fq, int fq_dtype, int* nonfinite, void* stream) {
+  if (!x || !dtype_ok(x_dtype) || (fq && !dtype_ok(fq_dtype))) return AQ_E_INVALID;
+  if (rows < 0 || cols <= 0 || cols % 32) return AQ_E_SHAPE;
+  if (rows == 0) return AQ_OK;
+  return cuda_status(launch_quantize_mx(x, x_dtype, rows, cols, codes, scales, fq, fq_dtype, nonfinite,
+                                        static_cast<cudaStream_t>(stream)));
+}
+
+int aq_dequantize_mx(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
+                     int out_dtype, void* stream) {
+  if (!codes || !scales || !out || !dtype_ok(out_dtype)) return AQ_E_INVALID;
+  if (rows < 0 || cols <= 0 || cols % 32) return AQ_E_SHAPE;
+  if (rows == 0) return AQ_OK;
+  return cuda_status(launch_dequantize_mx(codes, scales, rows, cols, out, out_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+int aq_e8m0_codes(const void* x, int x_dtype, int64_t n, uint8_t* codes, int* invalid, void* stream) {
+  if (!x || !codes || (x_dtype != 0 && x_dtype != 3)) return AQ_E_INVALID;
+  if (n < 0) return AQ_E_SHAPE;
+  if (n == 0) return AQ_OK;
+  return cuda_status(launch_e8m0_codes(x, x_dtype == 3, n, codes, invalid, static_cast<cudaStream_t>(stream)));
+}
+
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out, int out_dtype,
                   void* stream) {
   if (!codes || !scales || !out || !dtype_ok(out_dtype)) return AQ_E_INVALID;

@@ -685,4 +685,119 @@ cudaError_t launch_round_codes(const void* x, int x_is_f64, int64_t n, int forma
   return cudaGetLastError();
 }
 
+
+
+// ---------------------------------------------------------------------------
+// MXFP4 (32-element blocks, E8M0 power-of-two scales; codec.py:123-142,
+// 169-203): scale code = round-to-nearest power of two of amax / 6 with ties
+// up (0 for an all-zero block), elements = E2M1_RNE(x / 2^(code-127)). The
+// division by a power of two is exact, so x * 2^(127-code) feeds the hardware
+// E2M1 convert directly; amax / 6 is IEEE-rounded (its E8M0 rounding cannot
+// straddle the 1.5 * 2^e midpoint for fp32-representable inputs).
+// ---------------------------------------------------------------------------
+namespace {
+
+template <typename T>
+__device__ __forceinline__ uint32_t e8m0_code(T raw) {  // raw > 0, finite (codec.py:123-136)
+  int e;
+  const T m = frexp(raw, &e);                  // raw = m 2^e, m in [0.5, 1)
+  const int ex = (T(2) * m < T(1.5)) ? e - 1 : e;
+  const int c = ex + 127;
+  return static_cast<uint32_t>(c < 0 ? 0 : (c > 254 ? 254 : c));
+}
+
+__device__ __forceinline__ float e8m0_value(uint32_t code) { return ldexpf(1.0f, static_cast<int>(code) - 127); }
+
+__global__ void __launch_bounds__(256) quantize_mx_kernel(const void* x, int x_dt, int64_t rows, int64_t cols,
+                                                          uint8_t* codes, uint8_t* scales, void* fq, int fq_dt,
+                                                          int* nonfinite) {
+  const int64_t nb = cols / 32;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < rows * nb;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / nb, b = t % nb;
+    const int64_t i0 = r * cols + b * 32;
+    float v[32];
+    float amax = 0.f;
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = load_elem(x, i0 + j, x_dt);
+      finite = finite && isfinite(v[j]);
+      amax = fmaxf(amax, fabsf(v[j]));
+    }
+    if (!finite && nonfinite) atomicOr(nonfinite, 1);
+    const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);
+    const uint32_t sc = raw > 0.f ? e8m0_code(raw) : 0u;
+    const float rs = __int_as_float(static_cast<int>((254u - sc) << 23));  // 2^(127 - code), exact
+    const float s = e8m0_value(sc);
+    float q[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) q[j] = v[j] * rs + 0.0f;  // + 0 maps -0.0 to +0 (codec.py:84)
+    uint32_t packed[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) packed[k] = cvt_e2m1x8(q + 8 * k);
+    if (codes)
+      *reinterpret_cast<uint4*>(codes + r * (cols / 2) + b * 16) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (scales) scales[t] = static_cast<uint8_t>(sc);
+    if (fq) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        store_elem(fq, i0 + j, fq_dt, e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) dequantize_mx_kernel(const uint8_t* codes, const uint8_t* scales, int64_t rows,
+                                                            int64_t cols, void* out, int out_dt) {
+  const int64_t nb = cols / 32;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < rows * nb;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / nb, b = t % nb;
+    const float s = e8m0_value(scales[t]);
+    const uint4 w = *reinterpret_cast<const uint4*>(codes + r * (cols / 2) + b * 16);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      store_elem(out, r * cols + b * 32 + j, out_dt, e2m1_to_f32((ww[j >> 3] >> (4 * (j & 7))) & 0xF) * s);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) e8m0_codes_kernel(const T* __restrict__ x, int64_t n, uint8_t* codes,
+                                                         int* invalid) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T v = x[i];
+    if (!isfinite(static_cast<double>(v)) || !(v > T(0))) {
+      if (invalid) atomicOr(invalid, 1);
+      codes[i] = 0;
+      continue;
+    }
+    codes[i] = static_cast<uint8_t>(e8m0_code(v));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_quantize_mx(const void* x, int x_dt, int64_t rows, int64_t cols, uint8_t* codes, uint8_t* scales,
+                               void* fq, int fq_dt, int* nonfinite, cudaStream_t st) {
+  quantize_mx_kernel<<<grid_for(rows * (cols / 32)), 256, 0, st>>>(x, x_dt, rows, cols, codes, scales, fq, fq_dt,
+                                                                    nonfinite);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_mx(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
+                                 int out_dt, cudaStream_t st) {
+  dequantize_mx_kernel<<<grid_for(rows * (cols / 32)), 256, 0, st>>>(codes, scales, rows, cols, out, out_dt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_e8m0_codes(const void* x, int x_is_f64, int64_t n, uint8_t* codes, int* invalid, cudaStream_t st) {
+  if (x_is_f64)
+    e8m0_codes_kernel<double><<<grid_for(n), 256, 0, st>>>(static_cast<const double*>(x), n, codes, invalid);
+  else
+    e8m0_codes_kernel<float><<<grid_for(n), 256, 0, st>>>(static_cast<const float*>(x), n, codes, invalid);
+  return cudaGetLastError();
+}
+
 }  // namespace aq
