@@ -1,0 +1,24 @@
+"""Small ragged cases of every GPU entry point, for compute-sanitizer (memcheck / racecheck)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_00040_b200 as aq  # noqa: E402
+
+g = torch.Generator(device="cuda").manual_seed(0)
+for n, d, causal in ((200, 64, True), (77, 128, False)):
+    q, k, v, do = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() for _ in range(4))
+    o = aq.attn_qat(q.requires_grad_(), k.requires_grad_(), v.requires_grad_(), causal=causal)
+    o.backward(do)
+    aq.attn_forward(q.detach(), k.detach(), v.detach(), causal=causal, train=False)
+    cache = aq.kv4_quantize(k.detach(), v.detach())
+    aq.attn_forward_kv4(q.detach(), cache, causal=causal)
+x = torch.randn(37, 48, generator=g, device="cuda")
+aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))
+aq.fake_quantize(torch.randn(5, 64, generator=g, device="cuda"), aq.MXFP4)
+aq.round_to_fp4(np.linspace(-7, 7, 101))
+torch.cuda.synchronize()
+print("sanitize cases ok")
