@@ -110,8 +110,7 @@ def _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch):
     for name, shape, dtype in scratch:
         shp = shape(chunk_heads) if callable(shape) else shape
         scr.append(pipe.slots(f"scratch_{name}", tuple(shp), dtype))
-    for c, lo in enumerate(range(0, heads, chunk_heads)):
-        hi = min(heads, lo + chunk_heads)
+    for c, (lo, hi) in enumerate(_chunks(heads, chunk_heads)):
         n = hi - lo
         s = c % 2
         if pipe.in_free[s] is not None:
@@ -142,6 +141,19 @@ def _run(pipe, fn, host_inputs, host_outputs, heads, chunk_heads, scratch):
         pipe.out_free[s] = fetched
     comp.wait_stream(d2h)
     comp.wait_stream(h2d)
+
+
+def _chunks(heads, chunk):
+    """[lo, hi) head ranges: full chunks, with the last full chunk cut into
+    quarters -- only the final chunk's kernels and download are not hidden
+    behind an upload, so a short tail shortens the exposed end."""
+    bounds = list(range(0, heads, chunk)) + [heads]
+    spans = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)]
+    if len(spans) > 1 and chunk >= 4:
+        lo, hi = spans.pop()
+        step = max(1, -(-(hi - lo) // 4))
+        spans += [(a, min(hi, a + step)) for a in range(lo, hi, step)]
+    return spans
 
 
 def default_chunk(heads, per_head_bytes, items_per_head=None, sms=None):
