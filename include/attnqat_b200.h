@@ -128,6 +128,31 @@ int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 int aq_attn_fwd_kv4(const AqFwdArgs* args, const uint8_t* k_codes, const uint8_t* k_scales,
                     const uint8_t* vt_codes, const uint8_t* vt_scales, void* stream);
 
+/* SageAttention3-style forward (sage3_forward, sage3.py:113-194): Q / K
+ * smoothing (per-b_q-tile Q means, global K mean, sage3.py:45-60), the score
+ * decomposition S = fp4(gamma_q) fp4(gamma_k)^T + q_bar gamma_k^T + bias
+ * (sage3.py:74-88) and two-level P (each row of each b_k key segment rescaled
+ * onto [0, 448*6] before NVFP4, the product divided back, sage3.py:98-110,
+ * 186-190). Every toggle is independent. Two-level P needs b_k in
+ * {16, 32, 64, 128} or b_k == n_k (AQ_E_TILE otherwise); b_q must divide n_q,
+ * b_k must divide n_k. Outputs O [heads][n_q][d] (o_dtype) and L. */
+typedef struct {
+  const void* q; const void* k; const void* v; /* [heads][n][d], in_dtype */
+  int in_dtype;
+  int64_t heads, n_q, n_k, d;
+  int causal;
+  int64_t b_q, b_k;
+  int smooth_q, smooth_k, two_level_p;
+  void* o;           /* [heads][n_q][d], o_dtype */
+  int o_dtype;
+  float* lse;        /* [heads][n_q] */
+  void* workspace;   /* aq_attn_fwd_sage3_workspace_bytes() */
+} AqSage3Args;
+
+int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q);
+/* Replaces sage3_forward (sage3.py:113-194) for quantized=True. */
+int aq_attn_fwd_sage3(const AqSage3Args* args, void* stream);
+
 typedef struct {
   const void* q; const void* k; const void* v; /* original operands, in_dtype */
   int in_dtype;

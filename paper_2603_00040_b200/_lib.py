@@ -33,6 +33,16 @@ class AqFwdArgs(ctypes.Structure):
     ]
 
 
+class AqSage3Args(ctypes.Structure):
+    _fields_ = [
+        ("q", c_vp), ("k", c_vp), ("v", c_vp), ("in_dtype", c_int),
+        ("heads", c_i64), ("n_q", c_i64), ("n_k", c_i64), ("d", c_i64),
+        ("causal", c_int), ("b_q", c_i64), ("b_k", c_i64),
+        ("smooth_q", c_int), ("smooth_k", c_int), ("two_level_p", c_int),
+        ("o", c_vp), ("o_dtype", c_int), ("lse", c_vp), ("workspace", c_vp),
+    ]
+
+
 class AqBwdArgs(ctypes.Structure):
     _fields_ = [
         ("q", c_vp), ("k", c_vp), ("v", c_vp), ("in_dtype", c_int),
@@ -64,6 +74,8 @@ PROTOTYPES = {
     "aq_attn_fwd_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_int, c_int]),
     "aq_attn_fwd": (c_int, [ctypes.POINTER(AqFwdArgs), c_vp]),
     "aq_attn_fwd_kv4": (c_int, [ctypes.POINTER(AqFwdArgs), c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "aq_attn_fwd_sage3_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
+    "aq_attn_fwd_sage3": (c_int, [ctypes.POINTER(AqSage3Args), c_vp]),
     "aq_attn_bwd_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "aq_attn_bwd": (c_int, [ctypes.POINTER(AqBwdArgs), c_vp]),
     "aq_probe_mma_peak": (c_int, [c_int, c_int, c_int, c_vp]),

@@ -268,6 +268,134 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   return cuda_status(launch_attn_fwd(p, st));
 }
 
+namespace {
+struct SageWs {
+  FwdWs f;
+  int64_t fwd, gamma_q, gamma_k, q_bar, k_bar, delta, bias, sums, total, kpad;
+};
+
+SageWs sage_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q) {
+  SageWs w{};
+  w.f = fwd_ws(heads, n_q, n_k, d, 1, 0);
+  w.kpad = ceil_div(n_k, TILE) * TILE;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.fwd = take(w.f.total);
+  w.gamma_q = take(heads * n_q * d * 4);
+  w.gamma_k = take(heads * n_k * d * 4);
+  w.q_bar = take(heads * (n_q / b_q) * d * 8);
+  w.k_bar = take(heads * d * 8);
+  w.delta = take(heads * (n_q / b_q) * w.kpad * 4);
+  w.bias = take(heads * n_q * 4);
+  const int64_t cq = n_q / sage_chunk_rows(b_q), ck = n_k / sage_chunk_rows(n_k);
+  w.sums = take(heads * (cq > ck ? cq : ck) * d * 8);  // chunk sums of the means
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q) {
+  if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128) || b_q <= 0 || n_q % b_q) return 0;
+  return sage_ws(heads, n_q, n_k, d, b_q).total;
+}
+
+int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
+  if (!a || !a->q || !a->k || !a->v || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->o_dtype)) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d % 16) return AQ_E_SHAPE;
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  // TileConfig.validate (flash.py:60-71) and smooth's b_q check (sage3.py:50-53)
+  if (a->b_q <= 0 || a->b_k <= 0 || a->n_q % a->b_q || a->n_k % a->b_k) return AQ_E_TILE;
+  if (a->n_k > a->b_k && a->b_k % 16) return AQ_E_TILE;
+  int seg = -1;
+  if (a->two_level_p) {
+    if (a->b_k >= a->n_k) seg = 0;
+    else if (a->b_k == 16 || a->b_k == 32 || a->b_k == 64 || a->b_k == 128) seg = static_cast<int>(a->b_k);
+    else return AQ_E_TILE;  // segments must sit inside one 128-key kernel tile
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int d = static_cast<int>(a->d);
+  const SageWs w = sage_ws(a->heads, a->n_q, a->n_k, a->d, a->b_q);
+  uint8_t* base = static_cast<uint8_t*>(a->workspace);
+  uint8_t* ws = base + w.fwd;
+  float* gq = reinterpret_cast<float*>(base + w.gamma_q);
+  float* gk = reinterpret_cast<float*>(base + w.gamma_k);
+  double* q_bar = a->smooth_q ? reinterpret_cast<double*>(base + w.q_bar) : nullptr;
+  double* k_bar = a->smooth_k ? reinterpret_cast<double*>(base + w.k_bar) : nullptr;
+  float* delta = a->smooth_q ? reinterpret_cast<float*>(base + w.delta) : nullptr;
+  float* bias = a->smooth_k ? reinterpret_cast<float*>(base + w.bias) : nullptr;
+  double* sums = reinterpret_cast<double*>(base + w.sums);
+  if (q_bar && launch_sage_means(a->q, a->in_dtype, a->heads, a->n_q, d, a->b_q, sums, q_bar, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  if (k_bar && launch_sage_means(a->k, a->in_dtype, a->heads, a->n_k, d, a->n_k, sums, k_bar, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  if (launch_sage_center(a->q, a->in_dtype, a->heads, a->n_q, d, a->b_q, q_bar, gq, st) != cudaSuccess ||
+      launch_sage_center(a->k, a->in_dtype, a->heads, a->n_k, d, a->n_k, k_bar, gk, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  if (delta && launch_sage_delta(q_bar, gk, a->heads, a->n_q / a->b_q, a->n_k, d, w.kpad, delta, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  if (bias && launch_sage_bias(q_bar, k_bar, gq, a->heads, a->n_q, d, a->b_q, bias, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  // gamma_q / gamma_k (fp32) and V into the attention tiles; V^F fp16 tiles feed
+  // the two-level accumulation
+  RowsArgs r{};
+  r.x_dt = 0;
+  r.heads = a->heads;
+  r.cols = a->d;
+  r.ld = a->d;
+  r.x = gq;
+  r.n = a->n_q;
+  r.hs = a->n_q * a->d;
+  r.codes_t = ws + w.f.q_codes;
+  r.sf_t = ws + w.f.q_sf;
+  if (launch_quantize_rows(r, st) != cudaSuccess) return AQ_E_CUDA;
+  r.x = gk;
+  r.n = a->n_k;
+  r.hs = a->n_k * a->d;
+  r.codes_t = ws + w.f.k_codes;
+  r.sf_t = ws + w.f.k_sf;
+  if (launch_quantize_rows(r, st) != cudaSuccess) return AQ_E_CUDA;
+  r.x = a->v;
+  r.x_dt = a->in_dtype;
+  r.codes_t = ws + w.f.v_codes;
+  r.sf_t = ws + w.f.v_sf;
+  r.fqh_t = a->two_level_p ? ws + w.f.v_h16 : nullptr;
+  r.fqh_dt = 2;
+  if (launch_quantize_cols(r, st) != cudaSuccess) return AQ_E_CUDA;
+  FwdParams p{};
+  p.q_codes = ws + w.f.q_codes;
+  p.q_sf = ws + w.f.q_sf;
+  p.k_codes = ws + w.f.k_codes;
+  p.k_sf = ws + w.f.k_sf;
+  p.v_codes = ws + w.f.v_codes;
+  p.v_sf = ws + w.f.v_sf;
+  p.v_h = a->two_level_p ? ws + w.f.v_h16 : nullptr;
+  p.o = a->two_level_p ? nullptr : a->o;  // two-level P: O comes out of the f16 accumulator
+  p.o_dt = a->o_dtype;
+  p.o_hp = a->two_level_p ? a->o : nullptr;
+  p.o_hp_dt = a->o_dtype;
+  p.lse = a->lse;
+  p.heads = a->heads;
+  p.n_q = a->n_q;
+  p.n_k = a->n_k;
+  p.d = d;
+  p.causal = a->causal;
+  p.train = a->two_level_p;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  p.sage_delta = delta;
+  p.sage_bias = bias;
+  p.sage_bq = a->b_q;
+  p.sage_kpad = w.kpad;
+  p.sage_seg = seg;
+  return cuda_status(launch_attn_fwd_sage(p, st));
+}
+
 int aq_attn_fwd_kv4(const AqFwdArgs* a, const uint8_t* k_codes, const uint8_t* k_scales, const uint8_t* vt_codes,
                     const uint8_t* vt_scales, void* stream) {
   if (!a || !a->q || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;

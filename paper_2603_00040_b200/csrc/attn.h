@@ -41,6 +41,11 @@ struct FwdParams {
   int train;
   float scale_log2;
   int debug;  // timing experiments only (0 in production): 1 skip P quant, 2 skip exp, 4 skip pass-1 math
+  // SageAttention3 toggles (sage3.py; read by the K4 SAGE instances only)
+  const float* sage_delta;  // [heads][n_q / sage_bq][sage_kpad]: q_bar gamma_k^T per query tile, or null
+  const float* sage_bias;   // [heads][n_q]: q_bar k_bar + gamma_q k_bar per row, or null
+  int64_t sage_bq, sage_kpad;
+  int sage_seg;             // two-level P segment (keys): 16 / 32 / 64 / 128, 0 = the whole row
 };
 
 struct BwdParams {
@@ -72,6 +77,23 @@ cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64
                               int out_dt, cudaStream_t st);
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
+// K4 with the sage3 score terms; p.train selects two-level P (O written from
+// the f16 accumulator into p.o_hp) vs plain NVFP4 P (O into p.o)
+cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st);
+// rows per partial-sum chunk of a mean over `seg` rows: the largest divisor of seg <= 128
+inline int64_t sage_chunk_rows(int64_t seg) {
+  int64_t c = seg < 128 ? seg : 128;
+  while (c > 1 && seg % c) --c;
+  return c;
+}
+cudaError_t launch_sage_means(const void* x, int x_dt, int64_t heads, int64_t n, int d, int64_t seg,
+                              double* scratch, double* mean, cudaStream_t st);
+cudaError_t launch_sage_center(const void* x, int x_dt, int64_t heads, int64_t n, int d, int64_t seg,
+                               const double* mean, float* gamma, cudaStream_t st);
+cudaError_t launch_sage_delta(const double* q_bar, const float* gamma_k, int64_t heads, int64_t t_q, int64_t n_k,
+                              int d, int64_t kpad, float* delta, cudaStream_t st);
+cudaError_t launch_sage_bias(const double* q_bar, const double* k_bar, const float* gamma_q, int64_t heads,
+                             int64_t n_q, int d, int64_t b_q, float* bias, cudaStream_t st);
 cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
 int64_t fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,

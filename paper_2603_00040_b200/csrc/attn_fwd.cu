@@ -47,7 +47,7 @@ __device__ unsigned long long g_prof[16];
 #define AQ_PROF(...)
 #endif
 
-template <int D, bool TRAIN, int CS>
+template <int D, bool TRAIN, int CS, bool SAGE = false>
 struct Cfg {
   static constexpr int NSW = 4 * CS;                 // softmax warps
   static constexpr int NUM_THREADS = 32 * (NSW + 3);
@@ -75,9 +75,12 @@ struct Cfg {
   static constexpr int PB_CODES = 0, PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024;
   static constexpr int P_BYTES = PB_H + (TRAIN ? TILE * TILE * 2 : 0);
   static constexpr int ML = P0 + NP * P_BYTES;       // pass-1 (m, l) partials
-  static constexpr int K1_0 = ML + 2 * CS * TILE * 4; // pass-1 K ring
+  // (m, l) partials (+ the exact row max and the two-level P exchange with SAGE)
+  static constexpr int K1_0 = ML + (SAGE ? 3 : 2) * CS * TILE * 4;  // pass-1 K ring
   static constexpr int K1_BYTES = TILE * D / 2 + (D / 64) * 512;
-  static constexpr int BARS = K1_0 + NK1 * K1_BYTES;
+  // SAGE: per softmax warp, two 512-byte delta buffers (up to two q_bar rows x 64 keys)
+  static constexpr int DL = K1_0 + NK1 * K1_BYTES;
+  static constexpr int BARS = DL + (SAGE ? NSW * 1024 : 0);
   static constexpr int NUM_BARS = 40;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int USED = TMEM_SLOT + 16;
@@ -131,9 +134,17 @@ struct SUses {
   }
 };
 
-template <int D, bool TRAIN, int CS>
-__global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
-  using C = Cfg<D, TRAIN, CS>;
+// SAGE (sage3.py:113-194): the scores gain the high-precision smoothing terms
+// S += delta[q tile][key] + bias[row] before the softmax (both passes); with
+// TRAIN the kernel runs two-level P instead of O' -- P^F is quantized from
+// P * r (r = 448*6 / max P over the row's key segment) and the f16 MMA
+// accumulates dequant(P^F) * l / r, so the 1/r of every segment is applied
+// before the accumulation (the FP4 PV MMA is skipped; O comes out of the O'
+// epilogue).
+template <int D, bool TRAIN, int CS, bool SAGE = false>
+__global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
+  using C = Cfg<D, TRAIN, CS, SAGE>;
+  static_assert(!SAGE || CS == 2, "the sage3 instances use 64 key columns per thread");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::TMEM_SLOT);
@@ -298,16 +309,18 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
         const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
         if (elect_one()) {
+          if (!(SAGE && TRAIN)) {
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
-            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
+            for (int ks = 0; ks < 2; ++ks) {
+              tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
+              tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::ST_VSF + ks * 512));
+            }
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
+                          desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
+                          tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
           }
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
-                        desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
-                        tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
           if (TRAIN) {
 #pragma unroll
             for (int ks = 0; ks < TILE / 16; ++ks)
@@ -363,6 +376,78 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       int64_t kmax = p.n_k - 1;  // last visible key of this row (inclusive)
       if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
       AQ_PROF(tiles += nt;)
+      // sage3 score terms of this row: S = (main + delta[key]) + bias (sage3.py:158-172).
+      // The delta row(s) of a warp's 32 rows (one, or two when b_q = 16) are
+      // staged through a warp-private double buffer in shared memory, loaded
+      // one S tile ahead (lane l: float4 l%16 of row l/16), so the global
+      // load latency hides behind the S wait; b_q < 16 reads global memory.
+      const float* dl_row = nullptr;
+      float brow = 0.f;
+      bool dl_fast = false, dl_lane = false;
+      int dl_r = 0;
+      const float* dl_src = nullptr;
+      float* dl_s = reinterpret_cast<float*>(smem + C::DL) + warp * 256;
+      float4 dl_next = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (SAGE) {
+        const int64_t gr = grow < p.n_q ? grow : p.n_q - 1;
+        const int64_t tq = p.n_q / p.sage_bq;
+        if (p.sage_delta) {
+          dl_row = p.sage_delta + (head * tq + gr / p.sage_bq) * p.sage_kpad + cbase;
+          if (p.sage_bq >= 16) {
+            dl_fast = true;
+            int64_t w0 = static_cast<int64_t>(item.qt) * TILE + 32 * (warp & 3);
+            w0 = (w0 < p.n_q ? w0 : p.n_q - 1) / p.sage_bq;
+            dl_r = static_cast<int>(gr / p.sage_bq - w0);
+            const int64_t src_row = w0 + (lane >> 4);
+            dl_lane = src_row < tq && src_row * p.sage_bq < static_cast<int64_t>(item.qt) * TILE + 32 * (warp & 3) + 32;
+            dl_src = p.sage_delta + (head * tq + (dl_lane ? src_row : w0)) * p.sage_kpad + cbase + (lane & 15) * 4;
+          }
+        }
+        if (p.sage_bias) brow = p.sage_bias[head * p.n_q + gr];
+      }
+      auto dl_fetch = [&](int jj) {
+        return dl_lane ? __ldg(reinterpret_cast<const float4*>(dl_src + static_cast<int64_t>(jj) * TILE))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      auto sage_pre = [&](int jj) {
+        if constexpr (SAGE) {
+          if (dl_fast) {
+            if (jj == 0) {
+              __syncwarp();
+              reinterpret_cast<float4*>(dl_s)[lane] = dl_fetch(0);
+              __syncwarp();
+            }
+            if (jj + 1 < nt) dl_next = dl_fetch(jj + 1);
+          }
+        }
+      };
+      auto sage_post = [&](int jj) {
+        if constexpr (SAGE) {
+          if (dl_fast && jj + 1 < nt) {
+            reinterpret_cast<float4*>(dl_s + ((jj + 1) & 1) * 128)[lane] = dl_next;
+            __syncwarp();
+          }
+        }
+      };
+      // The row-constant bias cancels in P = exp(S - L): the passes run on
+      // main + delta and only the stored L gains bias / sqrt(d).
+      auto sage_add = [&](int jj) {
+        if constexpr (SAGE) {
+          if (dl_row) {
+            const float4* d4 = dl_fast ? reinterpret_cast<const float4*>(dl_s + (jj & 1) * 128 + dl_r * 64)
+                                       : reinterpret_cast<const float4*>(dl_row + static_cast<int64_t>(jj) * TILE);
+#pragma unroll
+            for (int c = 0; c < CW; c += 4) {
+              const float4 dv = d4[c / 4];
+              x[c] = __fadd_rn(x[c], dv.x);
+              x[c + 1] = __fadd_rn(x[c + 1], dv.y);
+              x[c + 2] = __fadd_rn(x[c + 2], dv.z);
+              x[c + 3] = __fadd_rn(x[c + 3], dv.w);
+            }
+          }
+        }
+      };
+      float mtrue = -INFINITY;  // exact row max of S (two-level P over the whole row)
 
       // pass 1 -- online softmax statistics over this thread's columns (log2
       // domain). The exponentials use a reference max m that is only raised
@@ -370,12 +455,20 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       // they do not wait for the tile's max reduction; a raise recomputes.
       float m = -INFINITY, l = 0.f;
       for (int jj = 0; jj < nt; ++jj) {
+        sage_pre(jj);
         AQ_ACQUIRE_S(jj % C::NB1);
         AQ_PROF(const long long tp1 = clock64();)
+        sage_add(jj);
         const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);  // visible: c <= lim
         if (lim < CW - 1) {
 #pragma unroll
           for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
+        }
+        if constexpr (SAGE && TRAIN) {
+          if (p.sage_seg == 0) {
+#pragma unroll
+            for (int c = 0; c < CW; ++c) mtrue = fmaxf(mtrue, x[c]);
+          }
         }
         auto expsum = [&](float base) {
           float2 acc[4];
@@ -412,6 +505,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
           }
         }
         l += sum;
+        sage_post(jj);
         AQ_PROF(prof_p1 += clock64() - tp1;)
       }
       AQ_PROF(p1_wait = prof_wait; p1_ld = prof_ld;)
@@ -419,6 +513,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       float* ml = reinterpret_cast<float*>(smem + C::ML);
       ml[(half * 2 + 0) * TILE + row] = m;
       ml[(half * 2 + 1) * TILE + row] = l;
+      if constexpr (SAGE) ml[(2 * CS + half) * TILE + row] = mtrue;
       named_bar_sync(1, 32 * C::NSW);
       float mt = -INFINITY;
 #pragma unroll
@@ -426,24 +521,70 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
       float lt = 0.f;
 #pragma unroll
       for (int h = 0; h < CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
+      if constexpr (SAGE) {
+#pragma unroll
+        for (int h = 0; h < CS; ++h) mtrue = fmaxf(mtrue, ml[(2 * CS + h) * TILE + row]);
+      }
       named_bar_sync(1, 32 * C::NSW);  // the partials buffer is reused by the next item
       // natural-log L is what the reference stores (flash.py:217); pass 2 uses
       // L2 = L * log2(e) recomputed from the stored value so the backward, which
       // only sees L, rebuilds bit-identical P (and P^F).
       const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
-      if (half == 0 && grow < p.n_q) p.lse[head * p.n_q + grow] = L_nat;
+      if (half == 0 && grow < p.n_q)
+        p.lse[head * p.n_q + grow] = SAGE ? L_nat + brow * (sl2 * 0.69314718055994530942f) : L_nat;
       const float L2 = L_nat * 1.44269504088896340736f;
       const float l_scale = lt;  // P^ = exp(S - m) = P * l
 
       // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
       for (int jj = 0; jj < nt; ++jj) {
+        sage_pre(jj);
         AQ_ACQUIRE_S(jj % C::NB2);
         AQ_PROF(const long long tm0 = clock64();)
+        sage_add(jj);
         const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
         p_from_s<CW / 2>(x, cbase, sl2, L2);
         if (lim < CW - 1) {
 #pragma unroll
           for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
+        }
+        // two-level P (sage3.py:98-110, 186-190): per 16-key block, the factor
+        // l / r of its segment; P is rescaled onto [0, 448*6] before quantizing
+        float fr[CW / 16];
+        if constexpr (SAGE && TRAIN) {
+          float bm[CW / 16];
+#pragma unroll
+          for (int b = 0; b < CW / 16; ++b) {
+            float v = x[16 * b];
+#pragma unroll
+            for (int e = 1; e < 16; ++e) v = fmaxf(v, x[16 * b + e]);
+            bm[b] = v;
+          }
+          const int seg = p.sage_seg;
+          if (seg == 0) {  // the whole row: max P = exp(max S - L)
+            const float v = ex2(fmaf(mtrue, sl2, -L2));
+#pragma unroll
+            for (int b = 0; b < CW / 16; ++b) bm[b] = v;
+          } else if (seg == 32) {
+            bm[0] = bm[1] = fmaxf(bm[0], bm[1]);
+            bm[2] = bm[3] = fmaxf(bm[2], bm[3]);
+          } else if (seg >= 64) {
+            float v = fmaxf(fmaxf(bm[0], bm[1]), fmaxf(bm[2], bm[3]));
+            if (seg == 128) {  // the other column split holds the other 64 keys
+              float* pm = reinterpret_cast<float*>(smem + C::ML) + (jj & 1) * (CS * TILE);
+              pm[half * TILE + row] = v;
+              named_bar_sync(2, 32 * C::NSW);
+              v = fmaxf(pm[row], pm[TILE + row]);
+            }
+#pragma unroll
+            for (int b = 0; b < CW / 16; ++b) bm[b] = v;
+          }
+#pragma unroll
+          for (int b = 0; b < CW / 16; ++b) {
+            const float r = bm[b] > 0.f ? __fdiv_rn(2688.0f, bm[b]) : 1.0f;
+            fr[b] = __fdiv_rn(l_scale, r);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[16 * b + e] = fminf(x[16 * b + e] * r, 2688.0f);
+          }
         }
         const int pb = pc % C::NP;
         AQ_PROF(const long long tm1 = clock64();)
@@ -462,6 +603,28 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
           *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
               make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
           scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+          if constexpr (SAGE && TRAIN) {  // f16 dequant(P^F) * l / r for the accumulating MMA
+            uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const PBlock& q = t ? qb : qa;
+              const float f = q.sv * fr[blk + t];
+#pragma unroll
+              for (int h8 = 0; h8 < 2; ++h8) {
+                __half2 hh[4];
+                e2m1x8_to_h2(q.codes[h8], hh);
+                uint32_t h[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 v = __half22float2(hh[e]);
+                  const __half2 o2 = __floats2half2_rn(v.x * f, v.y * f);
+                  h[e] = *reinterpret_cast<const uint32_t*>(&o2);
+                }
+                *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + blk * 16 + 16 * t + 8 * h8)) =
+                    make_uint4(h[0], h[1], h[2], h[3]);
+              }
+            }
+          }
         }
         if (CW >= 64) {
 #pragma unroll
@@ -470,7 +633,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         } else {
           *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
         }
-        if (TRAIN) {
+        if (TRAIN && !SAGE) {
           uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
 #pragma unroll
           for (int c8 = 0; c8 < CW / 8; ++c8) {
@@ -488,6 +651,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
         AQ_PROF(const long long tm3 = clock64();)
         fence_async_smem();
         mbar_arrive(&bars[C::B_P_FULL + pb]);
+        sage_post(jj);
         AQ_PROF(const long long tm4 = clock64(); prof_p2m += tm1 - tm0; prof_pw += tm2 - tm1;)
         AQ_PROF(prof_q += tm3 - tm2; prof_f += tm4 - tm3;)
       }
@@ -581,10 +745,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS>::NUM_THREADS, 1) attn_fwd_ke
   }
 }
 
-template <int D, bool TRAIN, int CS>
+template <int D, bool TRAIN, int CS, bool SAGE = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
-  using C = Cfg<D, TRAIN, CS>;
-  auto kern = attn_fwd_kernel<D, TRAIN, CS>;
+  using C = Cfg<D, TRAIN, CS, SAGE>;
+  auto kern = attn_fwd_kernel<D, TRAIN, CS, SAGE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -624,6 +788,12 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
     if (cudaMemcpyToSymbol(fwd::g_prof, z, sizeof(z)) != cudaSuccess) return 5;
   }
   return 0;
+}
+
+cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st) {
+  if (p.d == 64) return p.train ? fwd::launch<64, true, 2, true>(p, st) : fwd::launch<64, false, 2, true>(p, st);
+  if (p.d == 128) return p.train ? fwd::launch<128, true, 2, true>(p, st) : fwd::launch<128, false, 2, true>(p, st);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {

@@ -1,0 +1,93 @@
+"""SageAttention3-style outlier heuristics as toggles (reference: attnqat/sage3.py).
+
+``sage3_forward`` is the reference's real-quant tiled attention with
+
+* Q / K smoothing: gamma_q = Q - (per-b_q-tile token mean), gamma_k = K -
+  (global token mean) (sage3.py:45-60); only the zero-mean residuals pass
+  through FP4;
+* the exact score decomposition S = fp4(gamma_q) fp4(gamma_k)^T + q_bar
+  gamma_k^T + [q_bar k_bar + gamma_q k_bar] (sage3.py:74-88), the two
+  correction terms added to the scores in fp32 and never quantized;
+* two-level P: every row of every b_k key segment is rescaled onto
+  [0, 448*6] before NVFP4 block quantization and the product divided back
+  (sage3.py:98-110, 186-190).
+
+On the B200 the pre-processing (means in fp64, centring, the delta / bias
+terms) runs in csrc/sage3.cu and the attention in the K4 kernel's SAGE
+instances (csrc/attn_fwd.cu): the delta / bias terms are added to the S tile
+after the FP4 MMA in both passes; two-level P quantizes P * r in registers and
+accumulates dequant(P^F) * l / r through the f16 MMA (the per-segment 1/r is
+applied before the accumulation). Two-level P needs b_k in {16, 32, 64, 128}
+(segments inside one 128-key kernel tile) or b_k == n_k (one segment per
+row). ``quantized=False`` is plain attention (the heuristics are exact no-ops
+in exact arithmetic, sage3.py:117-120) and runs on the plain path.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .codec import to_device
+from .errors import InvalidValue, ShapeError
+from .flash import AttnOutputs, _check_attention_shapes, _check_cfg, _heads_view, _np_out, _plain_forward
+
+P_RESCALE_MAX = 448.0 * 6.0  # sage3.py:27 (max E4M3 scale x max FP4 value)
+
+
+def attn_forward_sage3(q, k, v, causal=False, b_q=128, b_k=128, smooth_q=True, smooth_k=True, two_level_p=True,
+                       quantized=True, out_dtype=None, workspace=None):
+    """sage3_forward on CUDA tensors [..., N, d] -> (O, L)."""
+    _lib.require_cuda()
+    if not quantized:
+        o, lse, _, _ = _plain_forward(q, k, v, causal, False, out_dtype)
+        return o, lse
+    q3, n_q, d = _heads_view(q)
+    k3, n_k, dk = _heads_view(k)
+    v3, n_v, dv = _heads_view(v)
+    if dk != d or dv != d or n_v != n_k or k3.shape[0] != q3.shape[0] or v3.shape[0] != q3.shape[0]:
+        raise ShapeError(f"inconsistent shapes Q{tuple(q.shape)} K{tuple(k.shape)} V{tuple(v.shape)}")
+    dt = q.dtype
+    if k.dtype != dt or v.dtype != dt or dt not in _lib.DT_CODE:
+        raise InvalidValue("q, k, v must share a float32 / bfloat16 / float16 dtype")
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    heads = q3.shape[0]
+    out_dtype = out_dtype or dt
+    lib = _lib.load()
+    ws_bytes = lib.aq_attn_fwd_sage3_workspace_bytes(heads, n_q, n_k, d, b_q) if b_q > 0 and n_q % b_q == 0 else 0
+    if ws_bytes <= 0 and d in (64, 128) and n_q > 0 and n_k > 0:
+        ws_bytes = 256  # the entry point reports the tile error
+    if ws_bytes <= 0:
+        raise InvalidValue(f"unsupported shape (heads {heads}, n_q {n_q}, n_k {n_k}, d {d})")
+    ws = workspace if workspace is not None and workspace.numel() >= ws_bytes else \
+        torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    o = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
+    lse = torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
+    args = _lib.AqSage3Args(
+        q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
+        heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), b_q=b_q, b_k=b_k,
+        smooth_q=int(smooth_q), smooth_k=int(smooth_k), two_level_p=int(two_level_p),
+        o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype], lse=lse.data_ptr(), workspace=ws.data_ptr())
+    _lib.check(lib.aq_attn_fwd_sage3(args, _lib.stream_ptr()))
+    lead = q.shape[:-2]
+    return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)
+
+
+def sage3_forward(Q, K, V, cfg, smooth_q=True, smooth_k=True, two_level_p=True, quantized=True):
+    """Real-quant tiled attention with the outlier heuristics (sage3.py:113-194)
+    -> AttnOutputs(O, L, O_prime=None). NumPy in, NumPy out; CUDA tensors stay
+    on the device."""
+    n_q, n_k, d = _check_attention_shapes(Q, K, V)
+    _check_cfg(cfg, n_q, n_k, d, quantized)
+    if cfg.b_q <= 0 or n_q % cfg.b_q:
+        raise ShapeError(f"b_q ({cfg.b_q}) must divide N_q ({n_q})")  # sage3.py:50-53
+    q, as_np = to_device(Q)
+    k, _ = to_device(K)
+    v, _ = to_device(V)
+    o, lse = attn_forward_sage3(q, k, v, causal=cfg.causal, b_q=cfg.b_q, b_k=cfg.b_k, smooth_q=smooth_q,
+                                smooth_k=smooth_k, two_level_p=two_level_p, quantized=quantized,
+                                out_dtype=torch.float32 if as_np else None)
+    if as_np:
+        import numpy as np
+        return AttnOutputs(O=_np_out(o, True), L=_np_out(lse, True, np.float64), O_prime=None)
+    return AttnOutputs(O=o, L=lse, O_prime=None)

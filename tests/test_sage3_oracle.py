@@ -1,0 +1,57 @@
+"""The oracle's SageAttention3 restatement vs the reference goldens (CPU)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import nvfp4_attn_oracle as orc
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sg():
+    return np.load(os.path.join(GOLD, "sage3.npz"))
+
+
+def case(sg, name):
+    n_q, n_k, d, causal, b_q, b_k, sq, sk, tl, qz = (int(x) for x in sg[f"{name}_meta"])
+    return (sg[f"{name}_Q"], sg[f"{name}_K"], sg[f"{name}_V"],
+            dict(causal=bool(causal), b_q=b_q, b_k=b_k, smooth_q=bool(sq), smooth_k=bool(sk),
+                 two_level_p=bool(tl), quantized=bool(qz)))
+
+
+NAMES = ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_sage3_matches_reference(sg, name):
+    Q, K, V, kw = case(sg, name)
+    O, L = orc.sage3_forward(Q, K, V, width=32, **kw)
+    np.testing.assert_array_equal(O, sg[f"{name}_O"])
+    np.testing.assert_array_equal(L, sg[f"{name}_L"])
+
+
+def test_two_level_scale_properties():
+    # test_sage3.py:101-118
+    s, r = orc.two_level_scale(np.zeros((4, 16)))
+    assert np.all(r == 1.0) and np.all(s == 0)
+    P = np.zeros((1, 16))
+    P[0, 0] = orc.P_RESCALE_MAX
+    assert orc.two_level_scale(P)[1][0] == 1.0
+    P = np.random.default_rng(22).uniform(0, 1, (8, 32))
+    s, r = orc.two_level_scale(P)
+    assert np.all(s.max(axis=1) <= orc.P_RESCALE_MAX)
+
+
+def test_smooth_properties():
+    # test_sage3.py:26-63
+    g = np.random.default_rng(3)
+    Q, K = g.standard_normal((64, 32)), g.standard_normal((80, 32))
+    gq, gk, q_bar, k_bar = orc.smooth(Q, K, 16)
+    assert np.max(np.abs(gk.mean(axis=0))) <= 1e-6
+    assert np.max(np.abs(gq.reshape(4, 16, 32).mean(axis=1))) <= 1e-6
+    np.testing.assert_allclose(gq + np.repeat(q_bar, 16, axis=0), Q, rtol=0, atol=1e-15)
+    with pytest.raises(ValueError):
+        orc.smooth(np.zeros((10, 8)), np.zeros((10, 8)), 3)
