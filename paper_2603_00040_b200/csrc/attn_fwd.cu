@@ -439,10 +439,12 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
 #pragma unroll
             for (int c = 0; c < CW; c += 4) {
               const float4 dv = d4[c / 4];
-              x[c] = __fadd_rn(x[c], dv.x);
-              x[c + 1] = __fadd_rn(x[c + 1], dv.y);
-              x[c + 2] = __fadd_rn(x[c + 2], dv.z);
-              x[c + 3] = __fadd_rn(x[c + 3], dv.w);
+              const float2 a = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(dv.x, dv.y));
+              const float2 b = __fadd2_rn(make_float2(x[c + 2], x[c + 3]), make_float2(dv.z, dv.w));
+              x[c] = a.x;
+              x[c + 1] = a.y;
+              x[c + 2] = b.x;
+              x[c + 3] = b.y;
             }
           }
         }
@@ -547,26 +549,32 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
 #pragma unroll
           for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
         }
-        // two-level P (sage3.py:98-110, 186-190): per 16-key block, the factor
-        // l / r of its segment; P is rescaled onto [0, 448*6] before quantizing
-        float fr[CW / 16];
+        // two-level P (sage3.py:98-110, 186-190): per 16-key block its max
+        // bm, the factor r = 448*6 / (max of its segment) and l / r for the f16
+        // accumulation of dequant(P^F) * l / r
+        float bm[CW / 16], rr[CW / 16], fr[CW / 16];
         if constexpr (SAGE && TRAIN) {
-          float bm[CW / 16];
 #pragma unroll
           for (int b = 0; b < CW / 16; ++b) {
-            float v = x[16 * b];
+            float v0 = fmaxf(x[16 * b], x[16 * b + 1]), v1 = fmaxf(x[16 * b + 2], x[16 * b + 3]);
 #pragma unroll
-            for (int e = 1; e < 16; ++e) v = fmaxf(v, x[16 * b + e]);
-            bm[b] = v;
+            for (int e = 4; e < 16; e += 2) {
+              v0 = fmaxf(v0, x[16 * b + e]);
+              v1 = fmaxf(v1, x[16 * b + e + 1]);
+            }
+            bm[b] = fmaxf(v0, v1);
           }
+          float sm[CW / 16];
           const int seg = p.sage_seg;
+#pragma unroll
+          for (int b = 0; b < CW / 16; ++b) sm[b] = bm[b];
           if (seg == 0) {  // the whole row: max P = exp(max S - L)
             const float v = ex2(fmaf(mtrue, sl2, -L2));
 #pragma unroll
-            for (int b = 0; b < CW / 16; ++b) bm[b] = v;
+            for (int b = 0; b < CW / 16; ++b) sm[b] = v;
           } else if (seg == 32) {
-            bm[0] = bm[1] = fmaxf(bm[0], bm[1]);
-            bm[2] = bm[3] = fmaxf(bm[2], bm[3]);
+            sm[0] = sm[1] = fmaxf(bm[0], bm[1]);
+            sm[2] = sm[3] = fmaxf(bm[2], bm[3]);
           } else if (seg >= 64) {
             float v = fmaxf(fmaxf(bm[0], bm[1]), fmaxf(bm[2], bm[3]));
             if (seg == 128) {  // the other column split holds the other 64 keys
@@ -576,14 +584,13 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
               v = fmaxf(pm[row], pm[TILE + row]);
             }
 #pragma unroll
-            for (int b = 0; b < CW / 16; ++b) bm[b] = v;
+            for (int b = 0; b < CW / 16; ++b) sm[b] = v;
           }
 #pragma unroll
           for (int b = 0; b < CW / 16; ++b) {
-            const float r = bm[b] > 0.f ? __fdiv_rn(2688.0f, bm[b]) : 1.0f;
-            fr[b] = __fdiv_rn(l_scale, r);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[16 * b + e] = fminf(x[16 * b + e] * r, 2688.0f);
+            const bool pos = sm[b] > 0.f;
+            rr[b] = pos ? 2688.0f * rcp_approx(sm[b]) : 1.0f;
+            fr[b] = pos ? l_scale * sm[b] * (1.0f / 2688.0f) : l_scale;
           }
         }
         const int pb = pc % C::NP;
@@ -598,8 +605,9 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
         for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
 #pragma unroll
         for (int blk = 0; blk < CW / 16; blk += 2) {
-          const PBlock qa = quantize_p16(x + blk * 16);
-          const PBlock qb = quantize_p16(x + blk * 16 + 16);
+          const PBlock qa = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16, bm[blk], rr[blk]) : quantize_p16(x + blk * 16);
+          const PBlock qb =
+              (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16 + 16, bm[blk + 1], rr[blk + 1]) : quantize_p16(x + blk * 16 + 16);
           *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
               make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
           scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
@@ -608,7 +616,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
               const PBlock& q = t ? qb : qa;
-              const float f = q.sv * fr[blk + t];
+              const __half2 f2 = __float2half2_rn(q.sv * fr[blk + t]);
 #pragma unroll
               for (int h8 = 0; h8 < 2; ++h8) {
                 __half2 hh[4];
@@ -616,8 +624,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
                 uint32_t h[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float2 v = __half22float2(hh[e]);
-                  const __half2 o2 = __floats2half2_rn(v.x * f, v.y * f);
+                  const __half2 o2 = __hmul2(hh[e], f2);
                   h[e] = *reinterpret_cast<const uint32_t*>(&o2);
                 }
                 *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + blk * 16 + 16 * t + 8 * h8)) =

@@ -45,6 +45,29 @@ __device__ __forceinline__ PBlock quantize_p16(const float* p) {
   return b;
 }
 
+// Two-level P (sage3.py:98-110): the block of P * r quantized without
+// materializing P * r -- amax and 1/scale absorb the factor r (the clamp to
+// 448*6 is implicit: both conversions saturate). amax = max of the block of P.
+__device__ __forceinline__ PBlock quantize_p16_r(const float* p, float amax, float r) {
+  const float am = amax * r;
+  uint32_t sc = cvt_e4m3(am * (1.0f / 6.0f));
+  if (sc == 0 && am > 0.f) sc = 1;
+  PBlock b;
+  b.scale = sc;
+  b.sv = e4m3_to_f32_cvt(sc);
+  const float rs = b.sv > 0.f ? rcp_approx(b.sv) * r : 0.f;
+  float q[16];
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    const float2 v = __fmul2_rn(make_float2(p[e], p[e + 1]), make_float2(rs, rs));
+    q[e] = v.x;
+    q[e + 1] = v.y;
+  }
+  b.codes[0] = cvt_e2m1x8(q);
+  b.codes[1] = cvt_e2m1x8(q + 8);
+  return b;
+}
+
 // P = exp(S - L) for 2*NP consecutive in-tile key columns starting at column
 // c0 (c0 % 16 == 0): t = S_raw * log2(e)/sqrt(d) - L2 (one FFMA2 per pair),
 // exp2 split between MUFU and the FMA-pipe polynomial by in-tile pair index.
