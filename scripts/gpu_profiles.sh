@@ -16,4 +16,8 @@ ncu --set full --clock-control none --import-source on -k regex:quantize -s 2 -c
     python scripts/time_quant.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fp4mm_kernel -s 1 -c 1 -o gpurun_out/prof/fp4mm_8k \
     python scripts/time_fp4mm.py > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_sage3_c2.csv \
+    python scripts/prof_sage3.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel -s 4 -c 1 -o gpurun_out/prof/attn_fwd_sage3_c2 \
+    python scripts/prof_sage3.py > /dev/null 2>&1
 ls -la gpurun_out/prof

@@ -57,7 +57,15 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__issue_active.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.per_cycle_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum"]
-for rep in ("attn_fwd_c2", "attn_fwd_train_c4", "attn_bwd_c4", "quantize_c2", "fp4mm_8k"):
+if os.path.exists(os.path.join(SRC, "launches_sage3_c2.csv")):
+    with open(os.path.join(DST, f"{TAG}_launches_sage3_c2.txt"), "w") as fh:
+        fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none, scripts/prof_sage3.py (C2 shape: "
+                 "K4 training, K5, then sage3 with no toggles / smoothing / two-level P / all)\n")
+        for k, t in launches("sage3_c2"):
+            if "at::" not in k:
+                fh.write(f"{t:12.1f} us  {k[:110]}\n")
+
+for rep in ("attn_fwd_c2", "attn_fwd_train_c4", "attn_bwd_c4", "quantize_c2", "fp4mm_8k", "attn_fwd_sage3_c2"):
     path = os.path.join(SRC, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
