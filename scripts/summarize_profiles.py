@@ -38,8 +38,9 @@ for cfg in ("c2", "c4"):
         # the full-size timed step: the launches ending at the longest attention launch
         # (later, shorter launches are the host-pipelined e2e chunks)
         # (a full step starts with the quantizers; the roofline loop re-runs the attention kernel alone)
-        cand = [i for i in range(1, len(ours)) if "attn_" in ours[i][0]
-                and any(s in ours[i - per_step + 1][0] for s in ("quantize",))]
+        cand = [i for i in range(per_step - 1, len(ours)) if "attn_" in ours[i][0]
+                and "quantize" in ours[i - per_step + 1][0]
+                and sum("attn_" in ours[j][0] for j in range(i - per_step + 1, i + 1)) == {"c2": 1, "c4": 2}[cfg]]
         end = max(cand, key=lambda i: ours[i][1])
         step = ours[max(0, end + 1 - per_step):end + 1]
         tot = sum(t for _, t in step) or 1
