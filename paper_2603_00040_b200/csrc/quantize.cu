@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 // output-pointer branches, no reference-layout or fake-quant stores: one
 // thread = 32 columns (two blocks) of one row, one 16-byte code store and one
 // 2-byte scale store.
-template <int D, bool FQH>
-__global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+template <int D, bool FQH, bool F32 = false>
+__global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __restrict__ xv, int64_t rows,
                                                                   uint8_t* __restrict__ codes_t,
                                                                   uint8_t* __restrict__ sf_t,
                                                                   uint8_t* __restrict__ fqh_t, int fqh_dt) {
@@ -239,20 +239,38 @@ __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const __nv_bfl
     const int64_t row = t / NPAIR;
     const int64_t tile = row / TILE;
     const int rr = static_cast<int>(row % TILE);
-    const uint4* src = reinterpret_cast<const uint4*>(x + row * D + bp * 32);
-    const uint4 w[4] = {src[0], src[1], src[2], src[3]};
     Block16 q[2];
+    if constexpr (F32) {  // fp32 input (the sage3 centred operands)
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(xv) + row * D + bp * 32);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t ww[8] = {w[2 * h].x, w[2 * h].y, w[2 * h].z, w[2 * h].w,
-                              w[2 * h + 1].x, w[2 * h + 1].y, w[2 * h + 1].z, w[2 * h + 1].w};
-      float v[16];
+      for (int h = 0; h < 2; ++h) {
+        float v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        v[2 * j] = __uint_as_float(ww[j] << 16);
-        v[2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
+        for (int j = 0; j < 4; ++j) {
+          const float4 f = src[4 * h + j];
+          v[4 * j] = f.x;
+          v[4 * j + 1] = f.y;
+          v[4 * j + 2] = f.z;
+          v[4 * j + 3] = f.w;
+        }
+        quantize_block16<FQH, false>(v, q[h]);
       }
-      quantize_block16<FQH, false>(v, q[h]);
+    } else {
+      const uint4* src =
+          reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(xv) + row * D + bp * 32);
+      const uint4 w[4] = {src[0], src[1], src[2], src[3]};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t ww[8] = {w[2 * h].x, w[2 * h].y, w[2 * h].z, w[2 * h].w,
+                                w[2 * h + 1].x, w[2 * h + 1].y, w[2 * h + 1].z, w[2 * h + 1].w};
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[2 * j] = __uint_as_float(ww[j] << 16);
+          v[2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
+        }
+        quantize_block16<FQH, false>(v, q[h]);
+      }
     }
     if (FQH) {
       // the 16-bit fake-quantized operand tile the backward reuses (T8x8)
@@ -541,13 +559,20 @@ static int grid_for(int64_t work) {
 
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
-  const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
-                    !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+  const bool fast = (a.x_dt == kBF16 || a.x_dt == kF32) && a.codes_t && a.sf_t && !a.fq && !a.codes_ref &&
+                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
-  if (fast) {
+  if (fast && a.x_dt == kF32 && !a.fqh_t) {
     const int64_t rows = a.heads * a.n;
     const int g = grid_for(rows * (a.cols / 32));
-    const auto* x = static_cast<const __nv_bfloat16*>(a.x);
+    if (a.cols == 128) quantize_rows_tiled_kernel<128, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0);
+    else quantize_rows_tiled_kernel<64, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0);
+    return cudaGetLastError();
+  }
+  if (fast && a.x_dt == kBF16) {
+    const int64_t rows = a.heads * a.n;
+    const int g = grid_for(rows * (a.cols / 32));
+    const auto* x = a.x;
     uint8_t* fqh = static_cast<uint8_t*>(a.fqh_t);
     if (a.cols == 128) {
       if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt);

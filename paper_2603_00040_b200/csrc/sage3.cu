@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) center_kernel(const void* x, int dt, int6
 template <int D>
 __global__ void __launch_bounds__(128) delta_kernel(const double* q_bar, const float* gamma_k, int64_t t_q,
                                                     int64_t n_k, int64_t kpad, float* delta) {
-  __shared__ float qs[32][D];
+  __shared__ __align__(16) float qs[32][D];
   const int64_t h = blockIdx.x;
   const int64_t j = static_cast<int64_t>(blockIdx.y) * TILE + threadIdx.x;
   float g[D];
@@ -112,11 +112,22 @@ __global__ void __launch_bounds__(128) delta_kernel(const double* q_bar, const f
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
       const int t1 = t + 1 < nt ? t + 1 : t, t2 = t + 2 < nt ? t + 2 : t, t3 = t + 3 < nt ? t + 3 : t;
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        a0 = __fadd_rn(a0, __fmul_rn(qs[t][c], g[c]));
-        a1 = __fadd_rn(a1, __fmul_rn(qs[t1][c], g[c]));
-        a2 = __fadd_rn(a2, __fmul_rn(qs[t2][c], g[c]));
-        a3 = __fadd_rn(a3, __fmul_rn(qs[t3][c], g[c]));
+      for (int c = 0; c < D; c += 4) {
+        const float4 q0 = *reinterpret_cast<const float4*>(&qs[t][c]);
+        const float4 q1 = *reinterpret_cast<const float4*>(&qs[t1][c]);
+        const float4 q2 = *reinterpret_cast<const float4*>(&qs[t2][c]);
+        const float4 q3 = *reinterpret_cast<const float4*>(&qs[t3][c]);
+        const float* f0 = reinterpret_cast<const float*>(&q0);
+        const float* f1 = reinterpret_cast<const float*>(&q1);
+        const float* f2 = reinterpret_cast<const float*>(&q2);
+        const float* f3 = reinterpret_cast<const float*>(&q3);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          a0 = __fadd_rn(a0, __fmul_rn(f0[e], g[c + e]));
+          a1 = __fadd_rn(a1, __fmul_rn(f1[e], g[c + e]));
+          a2 = __fadd_rn(a2, __fmul_rn(f2[e], g[c + e]));
+          a3 = __fadd_rn(a3, __fmul_rn(f3[e], g[c + e]));
+        }
       }
       float* drow = delta + (h * t_q + t0 + t) * kpad + j;
       const bool ok = j < n_k;
