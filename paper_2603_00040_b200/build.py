@@ -39,6 +39,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+# sage3.cu reproduces the reference's separately rounded products and sums
+# (tensors.py:32-51): no multiply-add contraction there, packed or scalar
+FILE_FLAGS = {"sage3.cu": ("-fmad=false",)}
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), out=None, build_dir=None) -> str:
     """Compile csrc/*.cu into the shared library. ``defines`` / ``out`` /
     ``build_dir`` produce tuning variants (e.g. -DAQ_POLY_PAIRS_OF_8=4)."""
@@ -55,7 +60,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None, buil
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(os.path.basename(src), ()),
+                   *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) sums_kernel(const void* x, int dt, int64_
   const int c = threadIdx.x % d, ph = threadIdx.x / d;
   double acc = 0.0;
   const int64_t base = (h * n + s * chunk) * d + c;
+#pragma unroll 8
   for (int64_t r = ph; r < chunk; r += phases) acc += load_d(x, base + r * d, dt);
   part[threadIdx.x] = acc;
   __syncthreads();
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(128) delta_kernel(const double* q_bar, const f
       qs[i / D][i % D] = static_cast<float>(q_bar[(h * t_q + t0) * D + i]);
     __syncthreads();
     for (int t = 0; t < nt; t += 4) {
+      // scalar __fmul_rn / __fadd_rn: never contracted (ptxas fuses packed
+      // fp32x2 multiply + add into FFMA2 even with .rn and -fmad=false)
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
       const int t1 = t + 1 < nt ? t + 1 : t, t2 = t + 2 < nt ? t + 2 : t, t3 = t + 3 < nt ? t + 3 : t;
 #pragma unroll
