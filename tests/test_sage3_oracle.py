@@ -55,3 +55,14 @@ def test_smooth_properties():
     np.testing.assert_allclose(gq + np.repeat(q_bar, 16, axis=0), Q, rtol=0, atol=1e-15)
     with pytest.raises(ValueError):
         orc.smooth(np.zeros((10, 8)), np.zeros((10, 8)), 3)
+
+
+def test_sage3_api_validates_before_touching_the_gpu():
+    # TileConfig.validate / accum_width checks run on the host (flash.py:60-71)
+    import paper_2603_00040_b200 as aq
+    Q = np.zeros((256, 64))
+    with pytest.raises(aq.TileError):
+        aq.sage3_forward(Q, Q, Q, aq.TileConfig(b_q=96, b_k=128))
+    with pytest.raises(aq.InvalidValue):
+        aq.sage3_forward(Q, Q, Q, aq.TileConfig(b_q=128, b_k=128, accum_width=64))
+    assert aq.P_RESCALE_MAX == orc.P_RESCALE_MAX == 2688.0
