@@ -1,4 +1,4 @@
-"""Small ragged cases of every GPU entry point, for compute-sanitizer (memcheck / racecheck)."""
+"""Small ragged cases of every GPU entry point (incl. sage3), for compute-sanitizer (memcheck / racecheck)."""
 import os
 import sys
 
@@ -16,6 +16,11 @@ for n, d, causal in ((200, 64, True), (77, 128, False)):
     aq.attn_forward(q.detach(), k.detach(), v.detach(), causal=causal, train=False)
     cache = aq.kv4_quantize(k.detach(), v.detach())
     aq.attn_forward_kv4(q.detach(), cache, causal=causal)
+for n, d, causal, b_q, b_k, tl in ((200, 64, True, 40, 200, True), (77, 128, False, 77, 77, True),
+                                   (77, 128, True, 77, 77, False), (256, 64, True, 16, 128, True),
+                                   (256, 128, False, 8, 32, True)):
+    q, k, v = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() + 1 for _ in range(3))
+    aq.attn_forward_sage3(q, k, v, causal=causal, b_q=b_q, b_k=b_k, two_level_p=tl)
 x = torch.randn(37, 48, generator=g, device="cuda")
 aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))
 aq.fake_quantize(torch.randn(5, 64, generator=g, device="cuda"), aq.MXFP4)
