@@ -16,6 +16,7 @@ from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, Sha
 from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward, attn_forward_host,
                     attn_qat_host, flash_backward, flash_forward_inference, flash_forward_training)
 from .kvcache import KV4Cache, attn_forward_kv4, attn_forward_kv4_host, kv4_quantize, load_kv4, save_kv4
+from .materialized import OracleTrace, QuantPoints, oracle_backward, oracle_forward
 from .sage3 import P_RESCALE_MAX, attn_forward_sage3, sage3_forward
 from .tensors import Rng, fp4mm, load_quant_tensor, load_tensor, matmul, randn, save_quant_tensor, save_tensor
 

@@ -66,3 +66,11 @@ def test_sage3_api_validates_before_touching_the_gpu():
     with pytest.raises(aq.InvalidValue):
         aq.sage3_forward(Q, Q, Q, aq.TileConfig(b_q=128, b_k=128, accum_width=64))
     assert aq.P_RESCALE_MAX == orc.P_RESCALE_MAX == 2688.0
+
+
+def test_quant_points_semantics():
+    # oracle.py:27-46
+    import paper_2603_00040_b200 as aq
+    assert aq.QuantPoints() == aq.QuantPoints.all_on()
+    assert aq.QuantPoints.all_on().any and not aq.QuantPoints.all_off().any
+    assert aq.QuantPoints(p=False).any and aq.QuantPoints(False, False, False, True).p
