@@ -59,3 +59,19 @@ def test_oracle_errors():
     aq.oracle_forward(Q + 1, Q, Q, points=aq.QuantPoints.all_off())  # fine without
     with pytest.raises(aq.ShapeError):
         aq.oracle_forward(np.zeros((32, 16)), np.zeros((16, 16)), np.zeros((16, 16)), causal=True)
+
+
+def test_fused_forward_memory_is_linear_in_n():
+    # the use the reference's tracker exists for: fused attention keeps O(N)
+    # device memory (the materialized oracle is O(N^2))
+    from paper_2603_00040_b200 import tracking
+    peaks = []
+    for n in (2048, 4096):
+        q = torch.randn(1, 4, n, 128, device="cuda").bfloat16()
+        with tracking.AllocationTracker() as t:
+            aq.attn_forward(q, q, q, causal=True, train=True)
+        peaks.append(t.peak)
+    assert 1.5 <= peaks[1] / peaks[0] <= 2.5
+    with tracking.AllocationTracker() as t:
+        aq.oracle_forward(*(torch.randn(1024, 64, device="cuda") for _ in range(3)))
+    assert t.peak >= 1024 * 1024 * 8      # S / P materialized

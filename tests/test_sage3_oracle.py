@@ -74,3 +74,15 @@ def test_quant_points_semantics():
     assert aq.QuantPoints() == aq.QuantPoints.all_on()
     assert aq.QuantPoints.all_on().any and not aq.QuantPoints.all_off().any
     assert aq.QuantPoints(p=False).any and aq.QuantPoints(False, False, False, True).p
+
+
+def test_tracking_api():
+    # tracking.py:16-69: live / peak bookkeeping, scopes release their registrations
+    from paper_2603_00040_b200 import tracking
+    assert tracking.track(np.zeros(4)) is not None          # no tracker: a no-op
+    with tracking.AllocationTracker() as t:
+        tracking.track(np.zeros(100))                       # 800 bytes
+        with tracking.scope():
+            tracking.track(np.zeros(50))                    # 400 bytes, released on exit
+        assert t.live == 800
+    assert t.peak >= 1200
