@@ -133,9 +133,9 @@ int aq_attn_fwd_kv4(const AqFwdArgs* args, const uint8_t* k_codes, const uint8_t
  * decomposition S = fp4(gamma_q) fp4(gamma_k)^T + q_bar gamma_k^T + bias
  * (sage3.py:74-88) and two-level P (each row of each b_k key segment rescaled
  * onto [0, 448*6] before NVFP4, the product divided back, sage3.py:98-110,
- * 186-190). Every toggle is independent. Two-level P needs b_k in
- * {16, 32, 64, 128} or b_k == n_k (AQ_E_TILE otherwise); b_q must divide n_q,
- * b_k must divide n_k. Outputs O [heads][n_q][d] (o_dtype) and L. */
+ * 186-190). Every toggle is independent. b_q must divide n_q, b_k must
+ * divide n_k (and be a multiple of 16 when n_k > b_k); AQ_E_TILE otherwise.
+ * Outputs O [heads][n_q][d] (o_dtype) and L. */
 typedef struct {
   const void* q; const void* k; const void* v; /* [heads][n][d], in_dtype */
   int in_dtype;
@@ -149,7 +149,8 @@ typedef struct {
   void* workspace;   /* aq_attn_fwd_sage3_workspace_bytes() */
 } AqSage3Args;
 
-int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q);
+int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q,
+                                          int64_t b_k);
 /* Replaces sage3_forward (sage3.py:113-194) for quantized=True. */
 int aq_attn_fwd_sage3(const AqSage3Args* args, void* stream);
 

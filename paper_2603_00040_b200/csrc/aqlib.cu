@@ -271,10 +271,14 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
 namespace {
 struct SageWs {
   FwdWs f;
-  int64_t fwd, gamma_q, gamma_k, q_bar, k_bar, delta, bias, sums, total, kpad;
+  int64_t fwd, gamma_q, gamma_k, q_bar, k_bar, delta, bias, sums, segmax, total, kpad;
 };
 
-SageWs sage_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q) {
+bool sage_local_seg(int64_t n_k, int64_t b_k) {
+  return b_k >= n_k || b_k == 16 || b_k == 32 || b_k == 64 || b_k == 128;
+}
+
+SageWs sage_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q, int64_t b_k) {
   SageWs w{};
   w.f = fwd_ws(heads, n_q, n_k, d, 1, 0);
   w.kpad = ceil_div(n_k, TILE) * TILE;
@@ -293,14 +297,17 @@ SageWs sage_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q) 
   w.bias = take(heads * n_q * 4);
   const int64_t cq = n_q / sage_chunk_rows(b_q), ck = n_k / sage_chunk_rows(n_k);
   w.sums = take(heads * (cq > ck ? cq : ck) * d * 8);  // chunk sums of the means
+  // two-level P segment maxima when segments do not sit inside one kernel tile
+  w.segmax = (b_k > 0 && n_k % b_k == 0 && !sage_local_seg(n_k, b_k)) ? take(heads * n_q * (n_k / b_k) * 4) : -1;
   w.total = off;
   return w;
 }
 }  // namespace
 
-int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q) {
+int64_t aq_attn_fwd_sage3_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int64_t b_q,
+                                          int64_t b_k) {
   if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128) || b_q <= 0 || n_q % b_q) return 0;
-  return sage_ws(heads, n_q, n_k, d, b_q).total;
+  return sage_ws(heads, n_q, n_k, d, b_q, b_k).total;
 }
 
 int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
@@ -313,15 +320,15 @@ int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
   // TileConfig.validate (flash.py:60-71) and smooth's b_q check (sage3.py:50-53)
   if (a->b_q <= 0 || a->b_k <= 0 || a->n_q % a->b_q || a->n_k % a->b_k) return AQ_E_TILE;
   if (a->n_k > a->b_k && a->b_k % 16) return AQ_E_TILE;
-  int seg = -1;
+  int seg = -2;  // no two-level P
   if (a->two_level_p) {
     if (a->b_k >= a->n_k) seg = 0;
-    else if (a->b_k == 16 || a->b_k == 32 || a->b_k == 64 || a->b_k == 128) seg = static_cast<int>(a->b_k);
-    else return AQ_E_TILE;  // segments must sit inside one 128-key kernel tile
+    else if (sage_local_seg(a->n_k, a->b_k)) seg = static_cast<int>(a->b_k);
+    else seg = -1;  // segment maxima from pass 1
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int d = static_cast<int>(a->d);
-  const SageWs w = sage_ws(a->heads, a->n_q, a->n_k, a->d, a->b_q);
+  const SageWs w = sage_ws(a->heads, a->n_q, a->n_k, a->d, a->b_q, a->b_k);
   uint8_t* base = static_cast<uint8_t*>(a->workspace);
   uint8_t* ws = base + w.fwd;
   float* gq = reinterpret_cast<float*>(base + w.gamma_q);
@@ -393,6 +400,12 @@ int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
   p.sage_bq = a->b_q;
   p.sage_kpad = w.kpad;
   p.sage_seg = seg;
+  p.sage_bk = a->b_k;
+  if (seg == -1) {
+    p.sage_segmax = reinterpret_cast<unsigned*>(base + w.segmax);
+    if (cudaMemsetAsync(p.sage_segmax, 0, a->heads * a->n_q * (a->n_k / a->b_k) * 4, st) != cudaSuccess)
+      return AQ_E_CUDA;
+  }
   return cuda_status(launch_attn_fwd_sage(p, st));
 }
 

@@ -45,7 +45,10 @@ struct FwdParams {
   const float* sage_delta;  // [heads][n_q / sage_bq][sage_kpad]: q_bar gamma_k^T per query tile, or null
   const float* sage_bias;   // [heads][n_q]: q_bar k_bar + gamma_q k_bar per row, or null
   int64_t sage_bq, sage_kpad;
-  int sage_seg;             // two-level P segment (keys): 16 / 32 / 64 / 128, 0 = the whole row
+  int sage_seg;             // two-level P segment (keys): 16 / 32 / 64 / 128, 0 = the whole row,
+                            // -1 = any other b_k: segment maxima of S from pass 1 in sage_segmax
+  unsigned* sage_segmax;    // [heads][n_q][n_k / sage_bk], order-preserving float codes, zeroed
+  int64_t sage_bk;
 };
 
 struct BwdParams {

@@ -37,6 +37,16 @@ namespace aq {
 
 namespace fwd {
 
+// float <-> unsigned with the same order (atomicMax on floats); 0 is below
+// every encoded value, so a zeroed buffer is the identity
+__device__ __forceinline__ unsigned f2ord(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
 // Tuning aid, compiled in with -DAQ_FWD_PROFILE and enabled at run time by
 // AQ_FWD_DEBUG bit 32: cycle sums per softmax segment, accumulated from lane
 // 0 of every softmax warp.
@@ -470,6 +480,29 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
           if (p.sage_seg == 0) {
 #pragma unroll
             for (int c = 0; c < CW; ++c) mtrue = fmaxf(mtrue, x[c]);
+          } else if (p.sage_seg < 0 && grow < p.n_q) {
+            // segments of b_k keys that need not align with the 128-key tiles:
+            // per 16-key block max, merged per segment, atomically into HBM
+            const int64_t nseg = p.n_k / p.sage_bk;
+            unsigned* sm_row = p.sage_segmax + (head * p.n_q + grow) * nseg;
+            const int64_t k0 = static_cast<int64_t>(jj) * TILE + cbase;
+            float run = -INFINITY;
+            int64_t run_s = -1;
+#pragma unroll
+            for (int b = 0; b < CW / 16; ++b) {
+              float v = x[16 * b];
+#pragma unroll
+              for (int e = 1; e < 16; ++e) v = fmaxf(v, x[16 * b + e]);
+              const int64_t s = (k0 + 16 * b) / p.sage_bk;
+              if (s != run_s) {
+                if (run_s >= 0 && run_s < nseg && run > -INFINITY) atomicMax(sm_row + run_s, f2ord(run));
+                run_s = s;
+                run = v;
+              } else {
+                run = fmaxf(run, v);
+              }
+            }
+            if (run_s >= 0 && run_s < nseg && run > -INFINITY) atomicMax(sm_row + run_s, f2ord(run));
           }
         }
         auto expsum = [&](float base) {
@@ -572,6 +605,17 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
             const float v = ex2(fmaf(mtrue, sl2, -L2));
 #pragma unroll
             for (int b = 0; b < CW / 16; ++b) sm[b] = v;
+          } else if (seg < 0) {  // segment maxima of S from pass 1 (ordered after the merge barrier)
+            const int64_t nseg = p.n_k / p.sage_bk;
+            const int64_t gr = grow < p.n_q ? grow : p.n_q - 1;
+            const unsigned* sm_row = p.sage_segmax + (head * p.n_q + gr) * nseg;
+            const int64_t k0 = static_cast<int64_t>(jj) * TILE + cbase;
+#pragma unroll
+            for (int b = 0; b < CW / 16; ++b) {
+              const int64_t s = (k0 + 16 * b) / p.sage_bk;
+              const unsigned u = s < nseg ? __ldcg(sm_row + s) : 0u;
+              sm[b] = u ? ex2(fmaf(ord2f(u), sl2, -L2)) : 0.f;
+            }
           } else if (seg == 32) {
             sm[0] = sm[1] = fmaxf(bm[0], bm[1]);
             sm[2] = sm[3] = fmaxf(bm[2], bm[3]);

@@ -17,9 +17,10 @@ terms) runs in csrc/sage3.cu and the attention in the K4 kernel's SAGE
 instances (csrc/attn_fwd.cu): the delta / bias terms are added to the S tile
 after the FP4 MMA in both passes; two-level P quantizes P * r in registers and
 accumulates dequant(P^F) * l / r through the f16 MMA (the per-segment 1/r is
-applied before the accumulation). Two-level P needs b_k in {16, 32, 64, 128}
-(segments inside one 128-key kernel tile) or b_k == n_k (one segment per
-row). ``quantized=False`` is plain attention (the heuristics are exact no-ops
+applied before the accumulation). Segment maxima: in registers for b_k in
+{16, 32, 64} and via a shared-memory exchange for 128; from the exact pass-1
+row max when b_k == n_k; otherwise pass 1 reduces them per (row, segment)
+into an HBM scratch with atomicMax. ``quantized=False`` is plain attention (the heuristics are exact no-ops
 in exact arithmetic, sage3.py:117-120) and runs on the plain path.
 """
 
@@ -54,7 +55,7 @@ def attn_forward_sage3(q, k, v, causal=False, b_q=128, b_k=128, smooth_q=True, s
     heads = q3.shape[0]
     out_dtype = out_dtype or dt
     lib = _lib.load()
-    ws_bytes = lib.aq_attn_fwd_sage3_workspace_bytes(heads, n_q, n_k, d, b_q) if b_q > 0 and n_q % b_q == 0 else 0
+    ws_bytes = lib.aq_attn_fwd_sage3_workspace_bytes(heads, n_q, n_k, d, b_q, b_k) if b_q > 0 and n_q % b_q == 0 else 0
     if ws_bytes <= 0 and d in (64, 128) and n_q > 0 and n_k > 0:
         ws_bytes = 256  # the entry point reports the tile error
     if ws_bytes <= 0:

@@ -10,7 +10,7 @@ import paper_2603_00040_b200 as aq  # noqa: E402
 from oracle import nvfp4_attn_oracle as orc  # noqa: E402
 
 sg = np.load("tests/golden/sage3.npz")
-for name in ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none"]:
+for name in ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none", "s48", "s256c", "s80c"]:
     n_q, n_k, d, causal, b_q, b_k, sq, sk, tl, qz = (int(x) for x in sg[f"{name}_meta"])
     Q, K, V = sg[f"{name}_Q"], sg[f"{name}_K"], sg[f"{name}_V"]
     o = aq.sage3_forward(Q, K, V, aq.TileConfig(b_q=b_q, b_k=b_k, causal=bool(causal)), smooth_q=bool(sq),

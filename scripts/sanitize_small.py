@@ -18,7 +18,8 @@ for n, d, causal in ((200, 64, True), (77, 128, False)):
     aq.attn_forward_kv4(q.detach(), cache, causal=causal)
 for n, d, causal, b_q, b_k, tl in ((200, 64, True, 40, 200, True), (77, 128, False, 77, 77, True),
                                    (77, 128, True, 77, 77, False), (256, 64, True, 16, 128, True),
-                                   (256, 128, False, 8, 32, True)):
+                                   (256, 128, False, 8, 32, True), (384, 64, True, 64, 48, True),
+                                   (512, 128, False, 128, 256, True)):
     q, k, v = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() + 1 for _ in range(3))
     aq.attn_forward_sage3(q, k, v, causal=causal, b_q=b_q, b_k=b_k, two_level_p=tl)
 x = torch.randn(37, 48, generator=g, device="cuda")

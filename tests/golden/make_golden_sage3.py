@@ -33,6 +33,9 @@ CASES = {
     "kOnly": (128, 256, 128, True, 128, 128, False, True, True, True),
     "qOnly": (256, 256, 64, False, 16, 64, True, False, True, True),
     "none": (256, 256, 64, True, 128, 128, False, False, False, True),
+    "s48": (256, 384, 64, False, 64, 48, True, True, True, True),
+    "s256c": (512, 512, 128, True, 128, 256, True, True, True, True),
+    "s80c": (160, 320, 64, True, 32, 80, True, False, True, True),
 }
 
 

@@ -12,7 +12,7 @@ from oracle import nvfp4_attn_oracle as orc
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-NAMES = ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none"]
+NAMES = ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none", "s48", "s256c", "s80c"]
 # O rel-L2 <= 2e-3 vs the goldens (measured <= 1e-4: fp32 tensor-core
 # accumulation vs fixed-order fp32, plus the f16 rounding of dequant(P^F) * l / r
 # under two-level P; a single P^F code flip costs ~1e-3), L <= 5e-5 absolute
@@ -102,9 +102,9 @@ def test_sage3_batched_torch_api_matches_per_head():
 def test_sage3_errors():
     q = torch.randn(512, 64, device="cuda")
     with pytest.raises(aq.TileError):
-        aq.attn_forward_sage3(q, q, q, b_q=128, b_k=256)  # two-level segment must sit in one 128-key tile
-    with pytest.raises(aq.TileError):
         aq.attn_forward_sage3(q, q, q, b_q=96, b_k=128)   # b_q must divide n_q
     with pytest.raises(aq.TileError):
         aq.attn_forward_sage3(q, q, q, b_q=128, b_k=48)   # b_k must divide n_k
-    aq.attn_forward_sage3(q, q, q, b_q=128, b_k=256, two_level_p=False)  # fine without two-level P
+    with pytest.raises(aq.TileError):
+        aq.attn_forward_sage3(q, q, q, b_q=128, b_k=40)    # b_k must be a multiple of 16
+    aq.attn_forward_sage3(q, q, q, b_q=128, b_k=256)       # segments spanning two kernel tiles

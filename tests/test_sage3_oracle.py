@@ -22,7 +22,7 @@ def case(sg, name):
                  two_level_p=bool(tl), quantized=bool(qz)))
 
 
-NAMES = ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none"]
+NAMES = ["s16", "s64c", "s128", "s32", "srow", "srowc", "noTL", "kOnly", "qOnly", "none", "s48", "s256c", "s80c"]
 
 
 @pytest.mark.parametrize("name", NAMES)
