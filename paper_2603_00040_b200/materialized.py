@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .codec import NVFP4, fake_quantize, fake_quantize_cols, fake_quantize_padded, to_device
+from .codec import NVFP4, fake_quantize, fake_quantize_cols, fake_quantize_padded
 from .errors import ShapeError
 from .flash import AttnGrads
 
@@ -67,6 +67,20 @@ def _dt(accum_width):
     return torch.float32 if accum_width == 32 else torch.float64
 
 
+def _dev(x):
+    """(cuda tensor, came_from_numpy), keeping float64 (the unquantized points
+    run in the accumulation width, like the reference)."""
+    from . import _lib
+    _lib.require_cuda()
+    if isinstance(x, torch.Tensor):
+        t, was_np = x, False
+    else:
+        t, was_np = torch.from_numpy(np.ascontiguousarray(np.asarray(x))), True
+    if not t.is_floating_point():
+        t = t.to(torch.float32)
+    return t.to("cuda"), was_np
+
+
 def _np(t, as_np):
     return t.cpu().numpy() if as_np else t
 
@@ -74,9 +88,9 @@ def _np(t, as_np):
 def oracle_forward(Q, K, V, spec=NVFP4, points=QuantPoints(), causal=False, accum_width=32):
     """Reference attention forward with fake quantization at the chosen points
     (oracle.py:106-131)."""
-    q, as_np = to_device(Q)
-    k, _ = to_device(K)
-    v, _ = to_device(V)
+    q, as_np = _dev(Q)
+    k, _ = _dev(K)
+    v, _ = _dev(V)
     if q.dim() != 2 or k.dim() != 2 or v.dim() != 2:
         raise ShapeError("attention operands must be 2-D (one head at a time)")
     n_q, d = q.shape
@@ -112,15 +126,15 @@ def oracle_forward(Q, K, V, spec=NVFP4, points=QuantPoints(), causal=False, accu
 def oracle_backward(trace, Qf, Kf, Vf, dO, accum_width=32):
     """Gradients through the explicit softmax Jacobian (oracle.py:141-161):
     dS = P * (dP - delta) / sqrt(d), delta_i = P_i . dP_i."""
-    qf, as_np = to_device(Qf)
-    kf, _ = to_device(Kf)
-    vf, _ = to_device(Vf)
-    do, _ = to_device(dO)
+    qf, as_np = _dev(Qf)
+    kf, _ = _dev(Kf)
+    vf, _ = _dev(Vf)
+    do, _ = _dev(dO)
     n_q, d = qf.shape
     if tuple(do.shape) != (n_q, d):
         raise ShapeError(f"dO shape {tuple(do.shape)} does not match Q {tuple(qf.shape)}")
-    P = to_device(trace.P)[0].double() if not isinstance(trace.P, torch.Tensor) else trace.P.double()
-    P_fq = to_device(trace.P_fq)[0].double() if not isinstance(trace.P_fq, torch.Tensor) else trace.P_fq.double()
+    P = _dev(trace.P)[0].double()
+    P_fq = _dev(trace.P_fq)[0].double()
     if tuple(P.shape) != (n_q, kf.shape[0]):
         raise ShapeError("trace does not match the provided operands")
     dt = _dt(accum_width)
@@ -131,3 +145,34 @@ def oracle_backward(trace, Qf, Kf, Vf, dO, accum_width=32):
     dQ = dS @ kf.to(dt)
     dK = dS.t() @ qf.to(dt)
     return AttnGrads(dQ=_np(dQ, as_np), dK=_np(dK, as_np), dV=_np(dV, as_np))
+
+
+def fd_attention_grads(Q, K, V, dO, causal=False, step=1e-3):
+    """Central finite differences of <dO, O> on the unquantized path
+    (oracle.py:164-194): an independent fp64 gradient check, O(params)
+    materialized forwards -- tiny shapes only."""
+    q, as_np = _dev(Q)
+    k, _ = _dev(K)
+    v, _ = _dev(V)
+    do = _dev(dO)[0].double()
+    base = [t.double() for t in (q, k, v)]
+    off = QuantPoints.all_off()
+
+    def loss(args):
+        tr = oracle_forward(*args, points=off, causal=causal, accum_width=64)
+        return float((do * tr.O).sum())
+
+    grads = []
+    for which in range(3):
+        g = torch.zeros_like(base[which])
+        flat = base[which].view(-1)
+        for i in range(flat.numel()):
+            keep = float(flat[i])
+            flat[i] = keep + step
+            up = loss(base)
+            flat[i] = keep - step
+            down = loss(base)
+            flat[i] = keep
+            g.view(-1)[i] = (up - down) / (2 * step)
+        grads.append(g)
+    return AttnGrads(dQ=_np(grads[0], as_np), dK=_np(grads[1], as_np), dV=_np(grads[2], as_np))

@@ -75,3 +75,15 @@ def test_fused_forward_memory_is_linear_in_n():
     with tracking.AllocationTracker() as t:
         aq.oracle_forward(*(torch.randn(1024, 64, device="cuda") for _ in range(3)))
     assert t.peak >= 1024 * 1024 * 8      # S / P materialized
+
+
+def test_fd_grads_match_oracle_backward():
+    # oracle.py:164-194 vs the explicit Jacobian on the unquantized path
+    from paper_2603_00040_b200.materialized import fd_attention_grads
+    Q, K, V = orc.make_qkv(80, 6, 8, 16)
+    dO = orc.randn((6, 16), 81)
+    fd = fd_attention_grads(Q, K, V, dO, causal=True)
+    tr = aq.oracle_forward(Q, K, V, points=aq.QuantPoints.all_off(), causal=True, accum_width=64)
+    g = aq.oracle_backward(tr, Q, K, V, dO, accum_width=64)
+    for a, b in ((fd.dQ, g.dQ), (fd.dK, g.dK), (fd.dV, g.dV)):
+        assert np.max(np.abs(a - b)) <= 1e-5 * max(1.0, np.max(np.abs(b)))
