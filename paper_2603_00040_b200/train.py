@@ -146,6 +146,67 @@ class AttnLayer(torch.nn.Module):
         return o @ self.w_o.to(dtype).t()
 
 
+def random_prediction_baseline(targets):
+    """Mean loss of predicting zero: the target second moment (harness.py:185-187)."""
+    t = targets.float() if isinstance(targets, torch.Tensor) else torch.from_numpy(np.asarray(targets)).float()
+    return float((t ** 2).mean())
+
+
+@torch.no_grad()
+def evaluate(layer, X, targets, eval_mode="bf16", causal=False, dtype=torch.bfloat16):
+    """Deterministic last-token MSE under the chosen attention precision
+    (harness.py:326-344): "bf16" the unquantized forward, "fp4" the real-quant
+    inference kernel (K5), "fp4-fake" the training forward (K4) -- the two FP4
+    paths give the same O bit for bit, so "fp4" and "fp4-fake" agree exactly."""
+    from .flash import attn_forward
+    dev = layer.w_q.device
+    x = (X if isinstance(X, torch.Tensor) else torch.from_numpy(np.asarray(X))).to(dev)
+    t = (targets if isinstance(targets, torch.Tensor) else torch.from_numpy(np.asarray(targets))).to(dev)
+    if eval_mode == "bf16":
+        y = layer(x, causal, dtype=dtype, quantized=False)
+    elif eval_mode in ("fp4", "fp4-fake"):
+        train = eval_mode == "fp4-fake"
+
+        def fwd(q, k, v, causal_, variant, quantized=True):
+            return attn_forward(q, k, v, causal=causal_, train=train)[0]
+        saved = layer.attn_fn
+        layer.attn_fn = fwd
+        try:
+            y = layer(x, causal, dtype=dtype)
+        finally:
+            layer.attn_fn = saved
+    else:
+        raise InvalidValue(f"unknown eval_mode {eval_mode!r}")
+    return float(((y[:, -1].float() - t.float()) ** 2).mean())
+
+
+def qat_matmul(A, B, spec=None, accum_width=64):
+    """C = fq(A) fq(B) (harness.py:356-358): both operands fake-quantized along
+    their last axis on the GPU quantizers, the product in the accumulation width."""
+    from .codec import NVFP4, fake_quantize
+    spec = spec or NVFP4
+    dt = torch.float64 if accum_width == 64 else torch.float32
+    a = torch.as_tensor(fake_quantize(A, spec))
+    b = torch.as_tensor(fake_quantize(B, spec))
+    out = a.to("cuda", dt) @ b.to("cuda", dt)
+    return out.cpu().numpy() if not isinstance(A, torch.Tensor) else out
+
+
+def qat_matmul_backward(A, B, dC, spec=None, accum_width=64):
+    """Straight-through gradients (harness.py:361-369): dA = dC fq(B)^T,
+    dB = fq(A)^T dC -- exactly, an identity of the estimator."""
+    from .codec import NVFP4, fake_quantize
+    spec = spec or NVFP4
+    dt = torch.float64 if accum_width == 64 else torch.float32
+    a = torch.as_tensor(fake_quantize(A, spec)).to("cuda", dt)
+    b = torch.as_tensor(fake_quantize(B, spec)).to("cuda", dt)
+    dc = torch.as_tensor(dC if isinstance(dC, torch.Tensor) else np.asarray(dC)).to("cuda", dt)
+    dA, dB = dc @ b.t(), a.t() @ dc
+    if not isinstance(A, torch.Tensor):
+        return dA.cpu().numpy(), dB.cpu().numpy()
+    return dA, dB
+
+
 class GradAllReduce:
     """NCCL all-reduce of parameter gradients, each launched asynchronously the
     moment its gradient is final, averaged over ranks."""
