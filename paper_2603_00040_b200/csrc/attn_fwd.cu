@@ -24,6 +24,8 @@
 // K/V stream through an NS-stage ring, S through NB1 (pass 1) / NB2 (pass 2)
 // TMEM buffers, P^F through NP SMEM buffers; every ring counts phases across
 // items.
+// The SAGE instances (sage3.py) add the smoothing score terms and, with TRAIN,
+// two-level P; see the comment above attn_fwd_kernel.
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>

@@ -30,7 +30,8 @@ def test_library_exports_every_header_symbol():
 def test_struct_fields_match_header():
     from paper_2603_00040_b200 import _lib
     src = open(os.path.join(ROOT, "include", "attnqat_b200.h")).read()
-    for struct, cls in (("AqFwdArgs", _lib.AqFwdArgs), ("AqBwdArgs", _lib.AqBwdArgs)):
+    for struct, cls in (("AqFwdArgs", _lib.AqFwdArgs), ("AqBwdArgs", _lib.AqBwdArgs),
+                        ("AqSage3Args", _lib.AqSage3Args)):
         body = re.search(r"typedef struct \{([^}]*)\}\s*" + struct, src, re.S).group(1)
         body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
         fields = []
@@ -56,6 +57,11 @@ def test_workspace_queries_reject_bad_dims():
     assert lib.aq_attn_fwd_workspace_bytes(1, 256, 256, 96, 1, 0) == 0
     assert lib.aq_attn_fwd_workspace_bytes(2, 256, 256, 64, 1, 1) > 0
     assert lib.aq_attn_bwd_workspace_bytes(2, 256, 256, 128) > 0
+    assert lib.aq_attn_fwd_sage3_workspace_bytes(2, 256, 256, 64, 96, 128) == 0   # b_q must divide n_q
+    assert lib.aq_attn_fwd_sage3_workspace_bytes(2, 256, 256, 128, 64, 128) > 0
+    # the pass-1 segment-maxima scratch only when segments leave the 128-key tiles
+    assert (lib.aq_attn_fwd_sage3_workspace_bytes(2, 256, 384, 64, 64, 48)
+            > lib.aq_attn_fwd_sage3_workspace_bytes(2, 256, 384, 64, 64, 128))
 
 
 def test_tile_config_validation_matches_reference():
