@@ -117,6 +117,13 @@ int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int
 /* Replaces flash_forward_training / flash_forward_inference (flash.py:176-314). */
 int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 
+/* quantized=False (flash.py:195-200): plain softmax attention on the same
+ * kernel skeleton with 16-bit operands (fmt 0 = fp16, 1 = bf16; inputs are
+ * converted), S and P^ V on kind::f16 MMAs with fp32 accumulation. Writes O
+ * (args->o) and L; args->train / o_hp / keep_for_bwd / operands_staged are
+ * ignored. Workspace: aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 1, 1). */
+int aq_attn_fwd_plain(const AqFwdArgs* args, int fmt, void* stream);
+
 /* FP4 KV cache: inference forward (flash_forward_inference, flash.py:249-314)
  * over K and V already quantized in the reference QuantTensor layout -- the
  * payload of ATQ4 files (tensors.py:173-188):

@@ -409,6 +409,39 @@ int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
   return cuda_status(launch_attn_fwd_sage(p, st));
 }
 
+int aq_attn_fwd_plain(const AqFwdArgs* a, int fmt, void* stream) {
+  if (!a || !a->q || !a->k || !a->v || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->o_dtype) || (fmt != 0 && fmt != 1)) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 1, 1);
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  const int d = static_cast<int>(a->d);
+  if (launch_tile16(a->q, a->in_dtype, a->heads, a->n_q, d, fmt, ws + w.q_hb, st) != cudaSuccess ||
+      launch_tile16(a->k, a->in_dtype, a->heads, a->n_k, d, fmt, ws + w.k_hb, st) != cudaSuccess ||
+      launch_tile16(a->v, a->in_dtype, a->heads, a->n_k, d, fmt, ws + w.v_hb, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  FwdParams p{};
+  p.q_codes = ws + w.q_hb;
+  p.k_codes = ws + w.k_hb;
+  p.v_h = ws + w.v_hb;
+  p.o = nullptr;
+  p.o_hp = a->o;  // the P^ V accumulator with 1/l is O here
+  p.o_hp_dt = a->o_dtype;
+  p.lse = a->lse;
+  p.heads = a->heads;
+  p.n_q = a->n_q;
+  p.n_k = a->n_k;
+  p.d = d;
+  p.causal = a->causal;
+  p.train = 1;
+  p.plain_fmt = fmt;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  return cuda_status(launch_attn_fwd_plain(p, st));
+}
+
 int aq_attn_fwd_kv4(const AqFwdArgs* a, const uint8_t* k_codes, const uint8_t* k_scales, const uint8_t* vt_codes,
                     const uint8_t* vt_scales, void* stream) {
   if (!a || !a->q || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;

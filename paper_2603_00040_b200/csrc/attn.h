@@ -49,6 +49,7 @@ struct FwdParams {
                             // -1 = any other b_k: segment maxima of S from pass 1 in sage_segmax
   unsigned* sage_segmax;    // [heads][n_q][n_k / sage_bk], order-preserving float codes, zeroed
   int64_t sage_bk;
+  int plain_fmt;            // PLAIN instances: 16-bit operand format, 0 = fp16, 1 = bf16
 };
 
 struct BwdParams {
@@ -83,6 +84,12 @@ cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 // K4 with the sage3 score terms; p.train selects two-level P (O written from
 // the f16 accumulator into p.o_hp) vs plain NVFP4 P (O into p.o)
 cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st);
+// quantized=False on K4: 16-bit Q / K / V tiles (q_codes / k_codes / v_h hold T8x8
+// images), O written to p.o_hp
+cudaError_t launch_attn_fwd_plain(const FwdParams& p, cudaStream_t st);
+// [heads][n][d] (x_dt) -> 16-bit T8x8 tiles (fmt 0 fp16 / 1 bf16), rows zero-padded to 128
+cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int d, int fmt, uint8_t* out,
+                          cudaStream_t st);
 // rows per partial-sum chunk of a mean over `seg` rows: the largest divisor of seg <= 128
 inline int64_t sage_chunk_rows(int64_t seg) {
   int64_t c = seg < 128 ? seg : 128;

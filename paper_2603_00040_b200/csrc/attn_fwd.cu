@@ -59,14 +59,15 @@ __device__ unsigned long long g_prof[16];
 #define AQ_PROF(...)
 #endif
 
-template <int D, bool TRAIN, int CS, bool SAGE = false>
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
 struct Cfg {
+  static_assert(!PLAIN || (TRAIN && !SAGE), "plain attention runs on the training layout");
   static constexpr int NSW = 4 * CS;                 // softmax warps
   static constexpr int NUM_THREADS = 32 * (NSW + 3);
   static constexpr int PRODUCER = NSW, PRODUCER1 = NSW + 1, MMA = NSW + 2;
-  static constexpr int NK1 = 4;                      // K ring (K codes + SF only), both passes
+  static constexpr int NK1 = PLAIN ? 2 : 4;          // K ring (K codes + SF; 16-bit K for PLAIN), both passes
   static constexpr int CW = TILE / CS;               // key columns per softmax thread
-  static constexpr int NS = TRAIN ? 2 : 5;           // K/V stages
+  static constexpr int NS = TRAIN ? 2 : 5;           // V stages
   static constexpr int NB1 = 3;                      // S buffers in pass 1 (1 and 2 alias O / O')
   static constexpr int NB2 = TRAIN ? 1 : 2;          // S buffers in pass 2
   static constexpr int NP = TRAIN ? 2 : 3;           // P^F (and P^) buffers
@@ -74,22 +75,22 @@ struct Cfg {
   static constexpr uint32_t T_O = TRAIN ? 128 : 256, T_OP = 256;
   static constexpr uint32_t T_QSF = 384, T_PSF = T_QSF + 8, T_VSF = T_PSF + 8 * NP, T_KSF1 = T_VSF + 8 * NS;
   // shared memory
-  static constexpr int Q_CODES = 0;
-  static constexpr int Q_SF = Q_CODES + TILE * D / 2;
-  static constexpr int STAGE0 = Q_SF + (D / 64) * 512;
+  static constexpr int Q_CODES = 0;                   // FP4 Q (16-bit Q tile for PLAIN)
+  static constexpr int Q_SF = Q_CODES + (PLAIN ? TILE * D * 2 : TILE * D / 2);
+  static constexpr int STAGE0 = Q_SF + (PLAIN ? 0 : (D / 64) * 512);
   // pass-2 stage: V^T codes + scale factors (+ V^F fp16); K tiles of both
   // passes come through the small K ring of producer 1
   static constexpr int ST_V = 0;
-  static constexpr int ST_VSF = ST_V + TILE * D / 2;
-  static constexpr int ST_VH = ST_VSF + 1024;
+  static constexpr int ST_VSF = ST_V + (PLAIN ? 0 : TILE * D / 2);
+  static constexpr int ST_VH = ST_VSF + (PLAIN ? 0 : 1024);
   static constexpr int STAGE_BYTES = ST_VH + (TRAIN ? TILE * D * 2 : 0);
   static constexpr int P0 = STAGE0 + NS * STAGE_BYTES;
-  static constexpr int PB_CODES = 0, PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024;
+  static constexpr int PB_CODES = 0, PB_SF = PLAIN ? 0 : TILE * TILE / 2, PB_H = PB_SF + (PLAIN ? 0 : 1024);
   static constexpr int P_BYTES = PB_H + (TRAIN ? TILE * TILE * 2 : 0);
   static constexpr int ML = P0 + NP * P_BYTES;       // pass-1 (m, l) partials
   // (m, l) partials (+ the exact row max and the two-level P exchange with SAGE)
   static constexpr int K1_0 = ML + (SAGE ? 3 : 2) * CS * TILE * 4;  // pass-1 K ring
-  static constexpr int K1_BYTES = TILE * D / 2 + (D / 64) * 512;
+  static constexpr int K1_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + (D / 64) * 512;
   // SAGE: per softmax warp, two 512-byte delta buffers (up to two q_bar rows x 64 keys)
   static constexpr int DL = K1_0 + NK1 * K1_BYTES;
   static constexpr int BARS = DL + (SAGE ? NSW * 1024 : 0);
@@ -98,9 +99,9 @@ struct Cfg {
   static constexpr int USED = TMEM_SLOT + 16;
   // one CTA per SM (the kernel owns all 512 TMEM columns)
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
-  static constexpr int Q_BYTES = TILE * D / 2 + (D / 64) * 512;
-  static constexpr int K_BYTES = TILE * D / 2 + (D / 64) * 512;
-  static constexpr int V_BYTES = TILE * D / 2 + 1024 + (TRAIN ? TILE * D * 2 : 0);
+  static constexpr int Q_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + (D / 64) * 512;
+  static constexpr int K_BYTES = K1_BYTES;
+  static constexpr int V_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + 1024 + (TRAIN ? TILE * D * 2 : 0);
   // barrier slots
   static constexpr int B_Q_FULL = 0, B_Q_EMPTY = 1, B_O_FULL = 2, B_O_EMPTY = 3, B_KV_FULL = 4,
                        B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS, B_S_EMPTY = B_S_FULL + NB1,
@@ -153,9 +154,12 @@ struct SUses {
 // accumulates dequant(P^F) * l / r, so the 1/r of every segment is applied
 // before the accumulation (the FP4 PV MMA is skipped; O comes out of the O'
 // epilogue).
-template <int D, bool TRAIN, int CS, bool SAGE = false>
-__global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
-  using C = Cfg<D, TRAIN, CS, SAGE>;
+// PLAIN (quantized=False, flash.py:195-200): S = Q K^T on 16-bit operands
+// (kind::f16, fp16 or bf16 per p.plain_fmt), no P quantization, O = P^ V
+// through the O' path with 1/l in the epilogue (written to p.o_hp).
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
+__global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
+  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN>;
   static_assert(!SAGE || CS == 2, "the sage3 instances use 64 key columns per thread");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
@@ -205,8 +209,12 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
       if (k > 0) mbar_wait(&bars[C::B_Q_EMPTY], (k - 1) & 1);
       if (elect_one()) {
         mbar_expect_tx(&bars[C::B_Q_FULL], C::Q_BYTES);
-        bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q_FULL]);
-        bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q_FULL]);
+        if (PLAIN) {
+          bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * h_tile_bytes(D), TILE * D * 2, &bars[C::B_Q_FULL]);
+        } else {
+          bulk_g2s(smem + C::Q_CODES, p.q_codes + qtile_idx * fp4_tile_bytes(D), TILE * D / 2, &bars[C::B_Q_FULL]);
+          bulk_g2s(smem + C::Q_SF, p.q_sf + qtile_idx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[C::B_Q_FULL]);
+        }
       }
       __syncwarp();
       // pass-2 stages (V [+ V^F]); the K tiles of both passes come from producer 1's ring
@@ -218,8 +226,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
         uint64_t* fb = &bars[C::B_KV_FULL + st];
         if (elect_one()) {
           mbar_expect_tx(fb, C::V_BYTES);
-          bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-          bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
+          if (!PLAIN) {
+            bulk_g2s(sb + C::ST_V, p.v_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+            bulk_g2s(sb + C::ST_VSF, p.v_sf + kt_idx * kSfTileBytesV, 1024, fb);
+          }
           if (TRAIN) bulk_g2s(sb + C::ST_VH, p.v_h + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
         }
         __syncwarp();
@@ -241,8 +251,12 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
         uint64_t* fb = &bars[C::B_K1_FULL + st];
         if (elect_one()) {
           mbar_expect_tx(fb, C::K_BYTES);
-          bulk_g2s(sb, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
-          bulk_g2s(sb + TILE * D / 2, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
+          if (PLAIN) {
+            bulk_g2s(sb, p.k_codes + kt_idx * h_tile_bytes(D), TILE * D * 2, fb);
+          } else {
+            bulk_g2s(sb, p.k_codes + kt_idx * fp4_tile_bytes(D), TILE * D / 2, fb);
+            bulk_g2s(sb + TILE * D / 2, p.k_sf + kt_idx * sf_tile_bytes_qk(D), (D / 64) * 512, fb);
+          }
         }
         __syncwarp();
       }
@@ -251,7 +265,8 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
     constexpr uint32_t id_pv = idesc_nvf4(128, D);
-    constexpr uint32_t id_op = idesc_f16(128, D, /*f16*/ 0, /*a_mn*/ 0, /*b_mn*/ 1);
+    const uint32_t id_op = idesc_f16(128, D, PLAIN ? static_cast<uint32_t>(p.plain_fmt) : 0u, /*a_mn*/ 0, /*b_mn*/ 1);
+    const uint32_t id_s16 = idesc_f16(128, 128, static_cast<uint32_t>(p.plain_fmt), 0, 0);  // PLAIN S
     constexpr uint64_t t_k = desc_template(2048, 128);       // Q / K / P^F codes (K-major T8x32, 128 rows)
     constexpr uint64_t t_v = desc_template(D * 16, 128);     // V^T codes (K-major T8x32, D rows)
     constexpr uint64_t t_sf = desc_template(0, 128);         // SF512 images for tcgen05.cp
@@ -271,13 +286,20 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
       tc_fence_after();
       const uint32_t kb = s0 + C::K1_0 + st * C::K1_BYTES;
       if (elect_one()) {
+        if constexpr (PLAIN) {
 #pragma unroll
-        for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + C::T_KSF1 + 8 * st + 4 * ks, desc_at(t_sf, kb + TILE * D / 2 + ks * 512));
+          for (int ks = 0; ks < D / 16; ++ks)
+            mma_f16_ss(tmem + 128 * b, desc_at(t_ph, q_base + ks * 4096), desc_at(t_ph, kb + ks * 4096), id_s16,
+                       ks > 0);
+        } else {
 #pragma unroll
-        for (int ks = 0; ks < D / 64; ++ks)
-          mma_nvf4_ss(tmem + 128 * b, desc_at(t_k, q_base + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
-                      tmem + C::T_QSF + 4 * ks, tmem + C::T_KSF1 + 8 * st + 4 * ks, ks > 0);
+          for (int ks = 0; ks < D / 64; ++ks)
+            tmem_cp_32x128_x4(tmem + C::T_KSF1 + 8 * st + 4 * ks, desc_at(t_sf, kb + TILE * D / 2 + ks * 512));
+#pragma unroll
+          for (int ks = 0; ks < D / 64; ++ks)
+            mma_nvf4_ss(tmem + 128 * b, desc_at(t_k, q_base + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
+                        tmem + C::T_QSF + 4 * ks, tmem + C::T_KSF1 + 8 * st + 4 * ks, ks > 0);
+        }
         tc_commit(&bars[C::B_S_FULL + b]);
         tc_commit(&bars[C::B_K1_EMPTY + st]);
       }
@@ -288,7 +310,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
       mbar_wait(&bars[C::B_Q_FULL], k & 1);
       tc_fence_after();
-      if (elect_one()) {
+      if (!PLAIN && elect_one()) {
         for (int ks = 0; ks < D / 64; ++ks)
           tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, desc_at(t_sf, s0 + C::Q_SF + ks * 512));
       }
@@ -321,7 +343,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
         const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
         const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
         if (elect_one()) {
-          if (!(SAGE && TRAIN)) {
+          if (!(SAGE && TRAIN) && !PLAIN) {
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
               tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
@@ -650,7 +672,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
 #pragma unroll
         for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
 #pragma unroll
-        for (int blk = 0; blk < CW / 16; blk += 2) {
+        for (int blk = 0; blk < (PLAIN ? 0 : CW / 16); blk += 2) {
           const PBlock qa = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16, bm[blk], rr[blk]) : quantize_p16(x + blk * 16);
           const PBlock qb =
               (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16 + 16, bm[blk + 1], rr[blk + 1]) : quantize_p16(x + blk * 16 + 16);
@@ -679,7 +701,8 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
             }
           }
         }
-        if (CW >= 64) {
+        if (PLAIN) {
+        } else if (CW >= 64) {
 #pragma unroll
           for (int s = 0; s < CW / 64; ++s)
             *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
@@ -687,6 +710,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
           *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
         }
         if (TRAIN && !SAGE) {
+          const bool bf = PLAIN && p.plain_fmt == 1;  // PLAIN with bf16 operands: P^ in bf16
           uint8_t* ph = smem + C::P0 + pb * C::P_BYTES + C::PB_H;
 #pragma unroll
           for (int c8 = 0; c8 < CW / 8; ++c8) {
@@ -695,8 +719,13 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
             for (int e = 0; e < 4; ++e) {
               const float2 ph2 = __fmul2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]),
                                             make_float2(l_scale, l_scale));
-              const __half2 v = __floats2half2_rn(ph2.x, ph2.y);
-              h[e] = *reinterpret_cast<const uint32_t*>(&v);
+              if (bf) {
+                const __nv_bfloat162 v = __floats2bfloat162_rn(ph2.x, ph2.y);
+                h[e] = *reinterpret_cast<const uint32_t*>(&v);
+              } else {
+                const __half2 v = __floats2half2_rn(ph2.x, ph2.y);
+                h[e] = *reinterpret_cast<const uint32_t*>(&v);
+              }
             }
             *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
           }
@@ -798,10 +827,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE>::NUM_THREADS, 1) attn_
   }
 }
 
-template <int D, bool TRAIN, int CS, bool SAGE = false>
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
-  using C = Cfg<D, TRAIN, CS, SAGE>;
-  auto kern = attn_fwd_kernel<D, TRAIN, CS, SAGE>;
+  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN>;
+  auto kern = attn_fwd_kernel<D, TRAIN, CS, SAGE, PLAIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -841,6 +870,12 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
     if (cudaMemcpyToSymbol(fwd::g_prof, z, sizeof(z)) != cudaSuccess) return 5;
   }
   return 0;
+}
+
+cudaError_t launch_attn_fwd_plain(const FwdParams& p, cudaStream_t st) {
+  if (p.d == 64) return fwd::launch<64, true, 2, false, true>(p, st);
+  if (p.d == 128) return fwd::launch<128, true, 2, false, true>(p, st);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st) {

@@ -557,6 +557,46 @@ static int grid_for(int64_t work) {
   return static_cast<int>(g);
 }
 
+// Plain (unquantized) attention operands: [heads][n][d] -> 16-bit T8x8 tiles,
+// padding rows zero. One thread = 8 consecutive columns of one row.
+template <int D>
+__global__ void __launch_bounds__(256) tile16_kernel(const void* __restrict__ x, int x_dt, int64_t heads, int64_t n,
+                                                     int fmt, uint8_t* __restrict__ out) {
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t total = heads * n_pad * (D / 8);
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(t % (D / 8));
+    const int64_t rp = t / (D / 8);  // padded row over all heads
+    const int64_t h = rp / n_pad, r = rp % n_pad;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = r < n ? load_elem(x, (h * n + r) * D + c8 * 8 + e, x_dt) : 0.f;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (fmt == 1) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+        w[e] = *reinterpret_cast<const uint32_t*>(&b);
+      } else {
+        const __half2 b = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
+        w[e] = *reinterpret_cast<const uint32_t*>(&b);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + (h * (n_pad / TILE) + r / TILE) * h_tile_bytes(D) +
+                              t8x8_off(static_cast<int>(r % TILE), c8 * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int d, int fmt, uint8_t* out,
+                          cudaStream_t st) {
+  const int g = grid_for(heads * ceil_div(n, TILE) * TILE * (d / 8));
+  if (d == 64) tile16_kernel<64><<<g, 256, 0, st>>>(x, x_dt, heads, n, fmt, out);
+  else if (d == 128) tile16_kernel<128><<<g, 256, 0, st>>>(x, x_dt, heads, n, fmt, out);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
   const bool fast = (a.x_dt == kBF16 || a.x_dt == kF32) && a.codes_t && a.sf_t && !a.fq && !a.codes_ref &&

@@ -3,21 +3,19 @@
 flash_forward_training / flash_backward with quantized=False skip every fake
 quantization (flash.py:195-200, 344-349): O = O' = softmax(QK^T/sqrt(d)) V and
 the textbook backward. The reference harness uses it for its "bf16" training
-and evaluation mode (harness.py:40, 333-335). It is not the NVFP4 hot path, so
-it runs on a library kernel -- FlashAttention-2 (flash_attn 2.8, like calling
-cuBLAS) -- rather than on the hand-written tcgen05 kernels:
+and evaluation mode (harness.py:40, 333-335).
 
-  * layout: our [heads, n, d] operands are viewed as FA2's [batch=heads, n,
-    1 head, d] without a copy;
-  * masking: FA2's causal mask is bottom-right aligned for n_q != n_k, which
-    is the reference's right-aligned mask (oracle.py:62-75);
-  * L: FA2's softmax LSE is the natural-log L of flash.py:217;
-  * dtypes: FA2 computes in fp16 / bf16 with fp32 accumulation; fp32 inputs run
-    in fp16 when they fit its range (else bf16) and results come back in the
-    caller's dtype;
-  * backward: D = rowsum(dO . O_ref) is computed by FA2 from the ``out`` it is
-    given, so O_ref (O or O', identical here) is passed there
-    (flash.py:333-351); deterministic mode, no atomics in dQ.
+* forward, d in {64, 128}: the hand-written K4 skeleton with 16-bit operands
+  (``aq_attn_fwd_plain``): Q / K / V staged as fp16 (or bf16 when a value
+  exceeds the fp16 range) T8x8 tiles, S and P^ V on ``kind::f16`` MMAs with
+  fp32 accumulation, the two-pass softmax of the FP4 path (L final before the
+  P V pass, 1/l in the epilogue);
+* other head dims, and the backward: FlashAttention-2 (flash_attn 2.8, library
+  kernels like cuBLAS). FA2's causal mask is bottom-right aligned for
+  n_q != n_k, the reference's right-aligned mask (oracle.py:62-75); its LSE is
+  the natural-log L of flash.py:217, so the backward consumes the forward's O
+  and L directly; D = rowsum(dO . O_ref) from the ``out`` it is given
+  (flash.py:333-351); deterministic mode, no atomics in dQ.
 """
 
 from __future__ import annotations
@@ -57,12 +55,40 @@ def _fa_view(t, dt):
     return t.to(dt).unsqueeze(2).contiguous()
 
 
+def _plain_forward_b200(q3, k3, v3, causal, dt):
+    """The hand-written path (aq_attn_fwd_plain): K4's skeleton with 16-bit
+    operands, S and P^V on kind::f16 MMAs, fp32 softmax statistics."""
+    from . import _lib
+    lib = _lib.load()
+    heads, n_q, d = q3.shape
+    n_k = k3.shape[1]
+    in_dt = q3.dtype
+    if in_dt not in _lib.DT_CODE or k3.dtype != in_dt or v3.dtype != in_dt:
+        q3, k3, v3 = q3.float(), k3.float(), v3.float()
+        in_dt = torch.float32
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    ws = torch.empty(lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 1, 1), dtype=torch.uint8, device=q3.device)
+    o = torch.empty((heads, n_q, d), dtype=q3.dtype, device=q3.device)
+    lse = torch.empty((heads, n_q), dtype=torch.float32, device=q3.device)
+    args = _lib.AqFwdArgs(q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[in_dt],
+                          heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=1,
+                          o=o.data_ptr(), o_dtype=_lib.DT_CODE[o.dtype], o_hp=None, o_hp_dtype=0,
+                          lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=1, operands_staged=0)
+    _lib.check(lib.aq_attn_fwd_plain(args, 0 if dt == torch.float16 else 1, _lib.stream_ptr()))
+    return o, lse
+
+
 def plain_forward(q3, k3, v3, causal):
-    """q3 [heads, n_q, d], k3 / v3 [heads, n_k, d] CUDA -> (O [heads, n_q, d] in q's dtype, L fp32)."""
-    if q3.shape[-1] % 8 or q3.shape[-1] > 256:
-        raise InvalidValue("plain attention supports head dims that are multiples of 8, up to 256")
+    """q3 [heads, n_q, d], k3 / v3 [heads, n_k, d] CUDA -> (O [heads, n_q, d] in q's dtype, L fp32).
+
+    Head dims 64 / 128 run on the hand-written sm_100a kernel; other head dims
+    (multiples of 8 up to 256) on FlashAttention-2."""
     if causal and q3.shape[1] > k3.shape[1]:
         raise ShapeError("causal attention requires N_q <= N_k")
+    if q3.shape[-1] in (64, 128):
+        return _plain_forward_b200(q3, k3, v3, causal, _compute_dtype(q3, k3, v3))
+    if q3.shape[-1] % 8 or q3.shape[-1] > 256:
+        raise InvalidValue("plain attention supports head dims that are multiples of 8, up to 256")
     fa = _flash()
     dt = _compute_dtype(q3, k3, v3)
     scale = 1.0 / math.sqrt(q3.shape[-1])

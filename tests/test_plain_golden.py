@@ -68,3 +68,22 @@ def test_gpu_plain_autograd_and_training_mode():
     cfg = T.TrainConfig(steps=3, attn_mode="bf16", seq_len=128, batch=4)
     _, log = T.train(cfg)
     assert len(log.losses) == 3 and all(np.isfinite(log.losses))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,causal", [(1024, 128, True), (640, 64, False), (300, 128, True)])
+def test_gpu_plain_forward_is_native_and_matches_oracle(n, d, causal):
+    # quantized=False at d = 64 / 128 runs the hand-written kernel (aq_attn_fwd_plain);
+    # bf16 operands, fp32 accumulation: O within 1e-2 of the fp64 oracle, L within 1e-4
+    import torch
+    import paper_2603_00040_b200 as aq
+    from paper_2603_00040_b200 import plain
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    q, k, v = (torch.randn(2, n, d, generator=g, device="cuda").bfloat16() for _ in range(3))
+    o, lse, o_hp, _ = aq.attn_forward(q, k, v, causal=causal, train=True, quantized=False)
+    o_n, l_n = plain._plain_forward_b200(q, k, v, causal, torch.bfloat16)
+    assert torch.equal(o, o_n) and torch.equal(lse, l_n) and torch.equal(o_hp, o)
+    Q, K, V = (t[1].double().cpu().numpy() for t in (q, k, v))
+    O, L, _ = orc.forward_training(Q, K, V, causal, width=64, quantized=False, ordered=False)
+    assert orc.rel_l2(o[1].float().cpu().numpy(), O) <= 1e-2
+    assert np.max(np.abs(lse[1].cpu().numpy() - L)) <= 1e-4
