@@ -28,6 +28,15 @@
 #ifndef AQ_FWDI_QSLOTS
 #define AQ_FWDI_QSLOTS 2
 #endif
+#ifndef AQ_FWDI_NSA
+#define AQ_FWDI_NSA 4
+#endif
+#ifndef AQ_FWDI_NSB
+#define AQ_FWDI_NSB 3
+#endif
+#ifndef AQ_FWDI_NP
+#define AQ_FWDI_NP 2
+#endif
 
 namespace aq {
 namespace fwdi {
@@ -40,7 +49,7 @@ struct Cfg {
   static constexpr int WA = 0, WB = NSW, PROD_A = 2 * NSW, PROD_B = PROD_A + 1, MMA_A = PROD_B + 1,
                        MMA_B = MMA_A + 1;
   static constexpr int NUM_THREADS = 32 * (MMA_B + 1);
-  static constexpr int NSA = 4, NSB = 3, NP = 2;     // ring depths
+  static constexpr int NSA = AQ_FWDI_NSA, NSB = AQ_FWDI_NSB, NP = AQ_FWDI_NP;  // ring depths
   static constexpr int NQ = AQ_FWDI_QSLOTS;           // Q slots: how far pass 1 may run ahead of pass 2
   // TMEM
   static constexpr uint32_t T_SA = 0, T_SB = 128, T_O = 256;
