@@ -108,3 +108,15 @@ def test_sage3_errors():
     with pytest.raises(aq.TileError):
         aq.attn_forward_sage3(q, q, q, b_q=128, b_k=40)    # b_k must be a multiple of 16
     aq.attn_forward_sage3(q, q, q, b_q=128, b_k=256)       # segments spanning two kernel tiles
+
+
+def test_sage3_input_dtypes_agree():
+    # bf16-representable values given as bf16, fp16 (exact here) and fp32: same
+    # centred operands, so the same bits out
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = (torch.randn(2, 256, 64, generator=g, device="cuda").bfloat16() for _ in range(3))
+    ref = aq.attn_forward_sage3(q, k, v, causal=True, b_q=64, b_k=64, out_dtype=torch.float32)
+    for dt in (torch.float32, torch.float16):
+        o, l = aq.attn_forward_sage3(q.to(dt), k.to(dt), v.to(dt), causal=True, b_q=64, b_k=64,
+                                     out_dtype=torch.float32)
+        assert torch.equal(o, ref[0]) and torch.equal(l, ref[1]), dt
