@@ -3,6 +3,7 @@
 // caller-owned workspace, and launches the quantizers + attention kernels on
 // the caller's stream. No host synchronisation, no device allocation.
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -401,6 +402,10 @@ int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
   p.sage_kpad = w.kpad;
   p.sage_seg = seg;
   p.sage_bk = a->b_k;
+  {
+    const char* e = std::getenv("AQ_SAGE_HEAD_GROUP");
+    p.head_group = e ? std::atoi(e) : 0;
+  }
   if (seg == -1) {
     p.sage_segmax = reinterpret_cast<unsigned*>(base + w.segmax);
     if (cudaMemsetAsync(p.sage_segmax, 0, a->heads * a->n_q * (a->n_k / a->b_k) * 4, st) != cudaSuccess)
@@ -438,6 +443,12 @@ int aq_attn_fwd_plain(const AqFwdArgs* a, int fmt, void* stream) {
   p.causal = a->causal;
   p.train = 1;
   p.plain_fmt = fmt;
+  {
+    // d = 128: the 16-bit K / V stream is HBM-bound in the global longest-first
+    // order (22 GB read at C2); groups of 4 heads keep it in L2 (4.77 -> 4.15 ms)
+    const char* e = std::getenv("AQ_PLAIN_HEAD_GROUP");
+    p.head_group = e ? std::atoi(e) : (d == 128 ? 4 : 0);
+  }
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
   return cuda_status(launch_attn_fwd_plain(p, st));
 }

@@ -50,6 +50,7 @@ struct FwdParams {
   unsigned* sage_segmax;    // [heads][n_q][n_k / sage_bk], order-preserving float codes, zeroed
   int64_t sage_bk;
   int plain_fmt;            // PLAIN instances: 16-bit operand format, 0 = fp16, 1 = bf16
+  int head_group;           // causal item order: 0 = longest-first over all heads, G > 0 = within groups of G heads
 };
 
 struct BwdParams {

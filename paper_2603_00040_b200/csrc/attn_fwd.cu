@@ -123,7 +123,19 @@ struct Item {
 
 __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_tiles, int k_tiles) {
   Item it;
-  if (p.causal) {
+  if (p.causal && p.head_group > 0) {
+    // longest-first within groups of G heads, so the CTAs in flight share the
+    // K / V tiles of a few heads in L2 (the 16-bit PLAIN operands are 4x the
+    // FP4 bytes and would otherwise stream from HBM for every query tile)
+    const int64_t gsz = static_cast<int64_t>(p.head_group) * q_tiles;
+    const int64_t g = w / gsz, r = w % gsz;
+    const int64_t G = min(static_cast<int64_t>(p.head_group), p.heads - g * p.head_group);
+    it.qt = q_tiles - 1 - static_cast<int>(r / G);
+    it.head = g * p.head_group + r % G;
+    const int64_t last =
+        static_cast<int64_t>(min(it.qt * TILE + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
+    it.nt = min(k_tiles, static_cast<int>(last / TILE) + 1);
+  } else if (p.causal) {
     it.qt = q_tiles - 1 - static_cast<int>(w / p.heads);
     it.head = w % p.heads;
     const int64_t last =

@@ -20,4 +20,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python scripts/prof_sage3.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel -s 4 -c 1 -o gpurun_out/prof/attn_fwd_sage3_c2 \
     python scripts/prof_sage3.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel -s 1 -c 1 -o gpurun_out/prof/attn_fwd_plain_c2 \
+    python scripts/prof_plain.py > /dev/null 2>&1
 ls -la gpurun_out/prof
