@@ -91,6 +91,11 @@ int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int
  * C [M][N] fp32 with row stride ldc. Block-scaled tcgen05 MMAs (exact block
  * products, fp32 accumulation). workspace: aq_fp4mm_workspace_bytes(M, N, K). */
 int64_t aq_fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+/* The same for MXFP4 QuantTensors (codec.py:123-166): UE8M0 scales, one per
+ * 32 codes (a_scales [M][K/32], b_scales [N][K/32]), K % 32 == 0, on
+ * tcgen05.mma.kind::mxf4.block_scale.block32. Workspace as for aq_fp4mm. */
+int aq_fp4mm_mx(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
+                const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, void* workspace, void* stream);
 int aq_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
              const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, void* workspace, void* stream);
 

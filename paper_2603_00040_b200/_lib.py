@@ -67,6 +67,7 @@ PROTOTYPES = {
     "aq_dequantize": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_vp]),
     "aq_fp4mm_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
     "aq_fp4mm": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "aq_fp4mm_mx": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "aq_quantize_mx": (c_int, [c_vp, c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
     "aq_dequantize_mx": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_vp]),
     "aq_e8m0_codes": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_vp]),

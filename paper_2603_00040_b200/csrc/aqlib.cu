@@ -227,6 +227,15 @@ int aq_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const u
                                   static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream)));
 }
 
+int aq_fp4mm_mx(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
+                const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, void* workspace, void* stream) {
+  if (!a_codes || !a_scales || !b_codes || !b_scales || !c || !workspace) return AQ_E_INVALID;
+  if (M < 0 || N < 0 || K <= 0 || K % 32 || ldc < N) return AQ_E_SHAPE;
+  if (M == 0 || N == 0) return AQ_OK;
+  return cuda_status(launch_fp4mm(a_codes, a_scales, M, b_codes, b_scales, N, K, c, ldc,
+                                  static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream), true));
+}
+
 int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int keep) {
   if (heads <= 0 || n_q <= 0 || n_k <= 0 || (d != 64 && d != 128)) return 0;
   return fwd_ws(heads, n_q, n_k, d, train, keep).total;

@@ -109,7 +109,7 @@ cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st);
 int64_t fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
                          const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, uint8_t* ws,
-                         cudaStream_t st);
+                         cudaStream_t st, bool mx = false);
 cudaError_t launch_quantize_mx(const void* x, int x_dt, int64_t rows, int64_t cols, uint8_t* codes, uint8_t* scales,
                                void* fq, int fq_dt, int* nonfinite, cudaStream_t st);
 cudaError_t launch_dequantize_mx(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,

@@ -48,6 +48,9 @@ constexpr uint32_t T_ACC = 0, T_SF = 256;      // acc buffers [0,128), [128,256)
 static_assert(SMEM <= 227 * 1024, "shared memory");
 static_assert(T_SF + 16 * NST <= 512, "TMEM columns");
 
+// MX = MXFP4 operands (UE8M0 scale per 32 codes, codec.py:123-166): the same
+// code tiles; the SF512 images then hold 4 scales per 128 K (one image per slab).
+template <bool MX>
 __global__ void __launch_bounds__(256) pack_operand(const uint8_t* __restrict__ codes,
                                                      const uint8_t* __restrict__ scales, int64_t rows, int64_t K,
                                                      int64_t kp, uint8_t* __restrict__ codes_t,
@@ -65,13 +68,14 @@ __global__ void __launch_bounds__(256) pack_operand(const uint8_t* __restrict__ 
     uint8_t s = 0;
     if (r < rows && b * 16 < K) {
       c = *reinterpret_cast<const uint2*>(codes + r * (K / 2) + b * 8);
-      s = scales[r * (K / 16) + b];
+      s = MX ? scales[r * (K / 32) + b / 2] : scales[r * (K / 16) + b];
     }
     // T8x32 with 128 rows and kp columns: 32-wide K chunks of 2 KB, K-chunk-major
     const int64_t kk = b * 16;
     *reinterpret_cast<uint2*>(codes_t + tile * (TILE * kp / 2) + (kk >> 5) * (TILE * 16) + (rr >> 3) * 128 +
                               (rr & 7) * 16 + ((kk & 31) >> 1)) = c;
-    sf_t[tile * (kp / 64) * 512 + sf512_off(rr, static_cast<int>(b))] = s;
+    if (!MX) sf_t[tile * (kp / 64) * 512 + sf512_off(rr, static_cast<int>(b))] = s;
+    else if ((b & 1) == 0) sf_t[tile * (kp / 64) * 512 + sf512_off(rr, static_cast<int>(b / 2))] = s;
   }
 }
 
@@ -85,6 +89,7 @@ struct GemmParams {
   int64_t kp;               // padded K (multiple of BK)
 };
 
+template <bool MX>
 __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BAR0);
@@ -126,13 +131,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams 
         if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
         if (elect_one()) {
           uint8_t* dst = smem + st * STAGE;
-          mbar_expect_tx(&full[st], STAGE);
+          constexpr int SFB = MX ? 512 : SF_SLAB;  // scale bytes per operand per slab
+          mbar_expect_tx(&full[st], 2 * (CODE_SLAB + SFB));
           bulk_g2s(dst, p.a_codes + tm * (TILE * p.kp / 2) + s * CODE_SLAB, CODE_SLAB, &full[st]);
-          bulk_g2s(dst + CODE_SLAB, p.a_sf + tm * (p.kp / 64) * 512 + s * SF_SLAB, SF_SLAB, &full[st]);
+          bulk_g2s(dst + CODE_SLAB, p.a_sf + tm * (p.kp / 64) * 512 + s * SFB, SFB, &full[st]);
           bulk_g2s(dst + CODE_SLAB + SF_SLAB, p.b_codes + tn * (TILE * p.kp / 2) + s * CODE_SLAB, CODE_SLAB,
                    &full[st]);
-          bulk_g2s(dst + 2 * CODE_SLAB + SF_SLAB, p.b_sf + tn * (p.kp / 64) * 512 + s * SF_SLAB, SF_SLAB,
-                   &full[st]);
+          bulk_g2s(dst + 2 * CODE_SLAB + SF_SLAB, p.b_sf + tn * (p.kp / 64) * 512 + s * SFB, SFB, &full[st]);
         }
         __syncwarp();
       }
@@ -158,15 +163,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams 
                        b_s = base + 2 * CODE_SLAB + SF_SLAB;
         const uint32_t sfa = tmem + T_SF + 16 * st, sfb = sfa + 8;
         if (elect_one()) {
+          if constexpr (MX) {
+            // one image per slab: scales of K blocks 0-3 (32 wide); K step ks
+            // starts at byte 2 ks of each row's 32-bit scale cell
+            tmem_cp_32x128_x4(sfa, desc_at(t_sf, a_s));
+            tmem_cp_32x128_x4(sfb, desc_at(t_sf, b_s));
 #pragma unroll
-          for (int ks = 0; ks < BK / 64; ++ks) {
-            tmem_cp_32x128_x4(sfa + 4 * ks, desc_at(t_sf, a_s + ks * 512));
-            tmem_cp_32x128_x4(sfb + 4 * ks, desc_at(t_sf, b_s + ks * 512));
+            for (int ks = 0; ks < BK / 64; ++ks) {
+              const uint32_t sid = 2u * ks;
+              mma_mxf4_ss(acc, desc_at(t_code, a_c + ks * 4096), desc_at(t_code, b_c + ks * 4096),
+                          idesc_mxf4(BM, BN, sid), sfa | (sid << 30), sfb | (sid << 30), (s > 0 || ks > 0));
+            }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < BK / 64; ++ks) {
+              tmem_cp_32x128_x4(sfa + 4 * ks, desc_at(t_sf, a_s + ks * 512));
+              tmem_cp_32x128_x4(sfb + 4 * ks, desc_at(t_sf, b_s + ks * 512));
+            }
+#pragma unroll
+            for (int ks = 0; ks < BK / 64; ++ks)
+              mma_nvf4_ss(acc, desc_at(t_code, a_c + ks * 4096), desc_at(t_code, b_c + ks * 4096), id, sfa + 4 * ks,
+                          sfb + 4 * ks, (s > 0 || ks > 0));
           }
-#pragma unroll
-          for (int ks = 0; ks < BK / 64; ++ks)
-            mma_nvf4_ss(acc, desc_at(t_code, a_c + ks * 4096), desc_at(t_code, b_c + ks * 4096), id, sfa + 4 * ks,
-                        sfb + 4 * ks, (s > 0 || ks > 0));
           tc_commit(&empty[st]);
           if (s == slabs - 1) tc_commit(&acc_full[ab]);
         }
@@ -234,7 +252,7 @@ int64_t fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 
 cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_t M, const uint8_t* b_codes,
                          const uint8_t* b_scales, int64_t N, int64_t K, float* c, int64_t ldc, uint8_t* ws,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool mx) {
   using namespace gemm;
   const int64_t kp = ceil_div(K, BK) * BK;
   const int64_t a_codes_b = ceil_div(M, TILE) * (TILE * kp / 2), a_sf_b = ceil_div(M, TILE) * (kp / 64) * 512;
@@ -243,11 +261,18 @@ cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_
   uint8_t* as = ac + a_codes_b;
   uint8_t* bc = as + a_sf_b;
   uint8_t* bs = bc + b_codes_b;
-  pack_operand<<<grid_for(ceil_div(M, TILE) * TILE * (kp / 16)), 256, 0, st>>>(a_codes, a_scales, M, K, kp, ac, as);
-  pack_operand<<<grid_for(ceil_div(N, TILE) * TILE * (kp / 16)), 256, 0, st>>>(b_codes, b_scales, N, K, kp, bc, bs);
+  const int ga = grid_for(ceil_div(M, TILE) * TILE * (kp / 16)), gb = grid_for(ceil_div(N, TILE) * TILE * (kp / 16));
+  if (mx) {
+    pack_operand<true><<<ga, 256, 0, st>>>(a_codes, a_scales, M, K, kp, ac, as);
+    pack_operand<true><<<gb, 256, 0, st>>>(b_codes, b_scales, N, K, kp, bc, bs);
+  } else {
+    pack_operand<false><<<ga, 256, 0, st>>>(a_codes, a_scales, M, K, kp, ac, as);
+    pack_operand<false><<<gb, 256, 0, st>>>(b_codes, b_scales, N, K, kp, bc, bs);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fp4mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  auto kern = mx ? fp4mm_kernel<true> : fp4mm_kernel<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -255,7 +280,7 @@ cudaError_t launch_fp4mm(const uint8_t* a_codes, const uint8_t* a_scales, int64_
   const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   GemmParams p{ac, as, bc, bs, c, M, N, ldc, kp};
-  fp4mm_kernel<<<grid, NUM_THREADS, SMEM, st>>>(p);
+  kern<<<grid, NUM_THREADS, SMEM, st>>>(p);
   return cudaGetLastError();
 }
 

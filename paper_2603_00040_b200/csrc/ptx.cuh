@@ -169,6 +169,18 @@ __device__ __forceinline__ void mma_nvf4_ss(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
       : "memory");
 }
+// MXFP4 block-scaled MMA: E2M1 operands, UE8M0 scale per 32 elements (two
+// per row per K=64 instruction; the scale-factor ID -- byte offset inside the
+// 32-bit TMEM cell -- travels in the address bits [30,32) and the descriptor).
+__device__ __forceinline__ void mma_mxf4_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
 // smem -> TMEM copy of a 32-lane x 128-bit block, replicated to all 4 lane quarters.
 __device__ __forceinline__ void tmem_cp_32x128_x4(uint32_t dst_tmem, uint64_t src_desc) {
   asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(dst_tmem), "l"(src_desc) : "memory");
@@ -253,6 +265,18 @@ __host__ __device__ constexpr uint32_t idesc_nvf4(uint32_t M, uint32_t N) {
          | ((N >> 3) << 17)     // n_dim
          | (0u << 23)           // scale_format = UE4M3
          | ((M >> 4) << 24);    // m_dim
+}
+
+// Instruction descriptor, kind::mxf4 with UE8M0 scales (block32), K-major,
+// K=64; sf_id = byte of the 32-bit scale cell the instruction starts at.
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N, uint32_t sf_id) {
+  return (sf_id << 4)           // b_sf_id
+         | (1u << 7)            // a_format = E2M1
+         | (1u << 10)           // b_format = E2M1
+         | ((N >> 3) << 17)     // n_dim
+         | (1u << 23)           // scale_format = UE8M0
+         | ((M >> 4) << 24)     // m_dim
+         | (sf_id << 29);       // a_sf_id
 }
 
 // ---------------------------------------------------------------- converts

@@ -174,9 +174,9 @@ def _dev_u8(a):
 
 
 def fp4mm(aq, bq_t, accum_width=32):
-    """C = A @ B from NVFP4 QuantTensors, B supplied transposed (both blocked
-    along the contraction axis; tensors.py:54-86), on block-scaled tcgen05
-    MMAs. Exact block products, fp32 accumulation (accum_width=64 raises
+    """C = A @ B from NVFP4 or MXFP4 QuantTensors, B supplied transposed (both
+    blocked along the contraction axis; tensors.py:54-86), on block-scaled
+    tcgen05 MMAs (kind::mxf4nvf4 block16 / kind::mxf4 block32). Exact block products, fp32 accumulation (accum_width=64 raises
     InvalidValue: the tensor cores accumulate in fp32). NumPy operands give a
     NumPy result, torch operands a CUDA tensor."""
     from . import _lib
@@ -191,8 +191,9 @@ def fp4mm(aq, bq_t, accum_width=32):
         raise ShapeError(f"accum_width must be 32 or 64, got {accum_width}")
     if accum_width != 32:
         raise InvalidValue("the B200 path accumulates in fp32 (tensor cores); accum_width=64 is CPU-only")
-    if aq.spec != NVFP4:
-        raise InvalidValue("the B200 path implements NVFP4 only")
+    from .codec import MXFP4
+    if aq.spec not in (NVFP4, MXFP4):
+        raise InvalidValue("the B200 path implements NVFP4 and MXFP4")
     _lib.require_cuda()
     as_np = not isinstance(aq.codes, torch.Tensor)
     ac, asf, bc, bsf = (_dev_u8(x) for x in (aq.codes, aq.scales, bq_t.codes, bq_t.scales))
@@ -200,8 +201,9 @@ def fp4mm(aq, bq_t, accum_width=32):
     lib = _lib.load()
     ws = torch.empty(lib.aq_fp4mm_workspace_bytes(M, N, K), dtype=torch.uint8, device="cuda")
     c = torch.empty((M, N), dtype=torch.float32, device="cuda")
-    _lib.check(lib.aq_fp4mm(_lib.ptr(ac), _lib.ptr(asf), M, _lib.ptr(bc), _lib.ptr(bsf), N, K, _lib.ptr(c), N,
-                            _lib.ptr(ws), _lib.stream_ptr()))
+    fn = lib.aq_fp4mm_mx if aq.spec == MXFP4 else lib.aq_fp4mm
+    _lib.check(fn(_lib.ptr(ac), _lib.ptr(asf), M, _lib.ptr(bc), _lib.ptr(bsf), N, K, _lib.ptr(c), N,
+                  _lib.ptr(ws), _lib.stream_ptr()))
     return c.cpu().numpy() if as_np else c
 
 

@@ -57,3 +57,18 @@ def test_matmul():
     np.testing.assert_allclose(aq.matmul(a, b, 64), a @ b, rtol=1e-12, atol=1e-12)
     with pytest.raises(aq.ShapeError):
         aq.matmul(a, b[:3])
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (37, 200, 96), (256, 384, 1024), (300, 129, 288), (1, 1, 32)])
+def test_fp4mm_mxfp4_matches_dequantized_product(M, N, K):
+    # MXFP4 QuantTensors (UE8M0 per 32, codec.py:123-166) on kind::mxf4 block32:
+    # exact block products, fp32 accumulation
+    rng = np.random.default_rng(M + 3 * N + K)
+    a = torch.from_numpy(rng.standard_normal((M, K)) * 10.0 ** rng.uniform(-3, 3, (M, 1))).float().cuda()
+    b = torch.from_numpy(rng.standard_normal((N, K))).float().cuda()
+    qa, qb = aq.quantize(a, aq.MXFP4), aq.quantize(b, aq.MXFP4)
+    c = aq.fp4mm(qa, qb)
+    ref = aq.dequantize(qa, torch.float32).double() @ aq.dequantize(qb, torch.float32).double().T
+    assert c.shape == (M, N)
+    np.testing.assert_allclose(c.double().cpu().numpy(), ref.cpu().numpy(), rtol=2e-6,
+                               atol=1e-6 * float(ref.abs().max()))
