@@ -122,6 +122,13 @@ int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int
 /* Replaces flash_forward_training / flash_forward_inference (flash.py:176-314). */
 int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 
+/* flash_forward_inference with cfg.spec = MXFP4 (flash.py:249-314,
+ * codec.py:123-203): Q / K / V^T quantized in 32-element blocks with UE8M0
+ * scales, P in 32-key blocks, S and PV on tcgen05.mma.kind::mxf4 block32.
+ * args->train must be 0; d % 32 == 0 (d in {64, 128}). Workspace:
+ * aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 0, 0). */
+int aq_attn_fwd_mx(const AqFwdArgs* args, void* stream);
+
 /* quantized=False (flash.py:195-200): plain softmax attention on the same
  * kernel skeleton with 16-bit operands (fmt 0 = fp16, 1 = bf16; inputs are
  * converted), S and P^ V on kind::f16 MMAs with fp32 accumulation. Writes O

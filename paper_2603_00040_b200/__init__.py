@@ -14,6 +14,7 @@ from .codec import (MXFP4, NVFP4, BlockSpec, Fp4Block, QuantTensor, ScaleFormat,
 from .errors import (AttnQatError, FormatError, InvalidValue, MissingOPrime, ShapeError, StabilityError,
                      TileError)
 from .flash import (AttnGrads, AttnOutputs, BwdVariant, TileConfig, attn_backward, attn_forward, attn_forward_host,
+                    attn_forward_mx,
                     attn_qat_host, flash_backward, flash_forward_inference, flash_forward_training)
 from .kvcache import KV4Cache, attn_forward_kv4, attn_forward_kv4_host, kv4_quantize, load_kv4, save_kv4
 from .materialized import OracleTrace, QuantPoints, oracle_backward, oracle_forward

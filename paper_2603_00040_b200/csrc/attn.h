@@ -88,6 +88,13 @@ cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st);
 // quantized=False on K4: 16-bit Q / K / V tiles (q_codes / k_codes / v_h hold T8x8
 // images), O written to p.o_hp
 cudaError_t launch_attn_fwd_plain(const FwdParams& p, cudaStream_t st);
+// MXFP4 inference forward on K4 (kind::mxf4 block32; the attention tiles from
+// launch_mx_attn_operands, P quantized in 32-key UE8M0 blocks)
+cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
+                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf,
+                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf,
+                                    cudaStream_t st);
 // [heads][n][d] (x_dt) -> 16-bit T8x8 tiles (fmt 0 fp16 / 1 bf16), rows zero-padded to 128
 cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int d, int fmt, uint8_t* out,
                           cudaStream_t st);

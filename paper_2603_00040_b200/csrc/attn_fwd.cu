@@ -59,8 +59,9 @@ __device__ unsigned long long g_prof[16];
 #define AQ_PROF(...)
 #endif
 
-template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false, bool MX = false>
 struct Cfg {
+  static_assert(!MX || (!TRAIN && !SAGE && !PLAIN), "MXFP4 runs the inference layout");
   static_assert(!PLAIN || (TRAIN && !SAGE), "plain attention runs on the training layout");
   static constexpr int NSW = 4 * CS;                 // softmax warps
   static constexpr int NUM_THREADS = 32 * (NSW + 3);
@@ -169,9 +170,13 @@ struct SUses {
 // PLAIN (quantized=False, flash.py:195-200): S = Q K^T on 16-bit operands
 // (kind::f16, fp16 or bf16 per p.plain_fmt), no P quantization, O = P^ V
 // through the O' path with 1/l in the epilogue (written to p.o_hp).
-template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
-__global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
-  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN>;
+// MX (MXFP4, codec.py:123-203 with flash.py:249-314): the same tiles and
+// scale-factor images (one image per 128 K holds four UE8M0 scales), S and PV
+// on kind::mxf4 block32 with scale-factor IDs 0 / 2 per K = 64 step, P
+// quantized in 32-key blocks.
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false, bool MX = false>
+__global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREADS, 1) attn_fwd_kernel(const FwdParams p) {
+  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>;
   static_assert(!SAGE || CS == 2, "the sage3 instances use 64 key columns per thread");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
@@ -303,6 +308,15 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
           for (int ks = 0; ks < D / 16; ++ks)
             mma_f16_ss(tmem + 128 * b, desc_at(t_ph, q_base + ks * 4096), desc_at(t_ph, kb + ks * 4096), id_s16,
                        ks > 0);
+        } else if constexpr (MX) {
+          tmem_cp_32x128_x4(tmem + C::T_KSF1 + 8 * st, desc_at(t_sf, kb + TILE * D / 2));
+#pragma unroll
+          for (int ks = 0; ks < D / 64; ++ks) {
+            const uint32_t sid = 2u * ks;
+            mma_mxf4_ss(tmem + 128 * b, desc_at(t_k, q_base + ks * 4096), desc_at(t_k, kb + ks * 4096),
+                        idesc_mxf4(128, 128, sid), (tmem + C::T_QSF) | (sid << 30),
+                        (tmem + C::T_KSF1 + 8 * st) | (sid << 30), ks > 0);
+          }
         } else {
 #pragma unroll
           for (int ks = 0; ks < D / 64; ++ks)
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
       mbar_wait(&bars[C::B_Q_FULL], k & 1);
       tc_fence_after();
       if (!PLAIN && elect_one()) {
-        for (int ks = 0; ks < D / 64; ++ks)
+        for (int ks = 0; ks < (MX ? 1 : D / 64); ++ks)
           tmem_cp_32x128_x4(tmem + C::T_QSF + 4 * ks, desc_at(t_sf, s0 + C::Q_SF + ks * 512));
       }
       __syncwarp();
@@ -355,7 +369,18 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
         const uint32_t sb = s0 + C::STAGE0 + st * C::STAGE_BYTES;
         const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
         if (elect_one()) {
-          if (!(SAGE && TRAIN) && !PLAIN) {
+          if constexpr (MX) {
+            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb, desc_at(t_sf, pbase + C::PB_SF));
+            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st, desc_at(t_sf, sb + C::ST_VSF));
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t sid = 2u * ks;
+              mma_mxf4_ss(tmem + C::T_O, desc_at(t_k, pbase + C::PB_CODES + ks * 4096),
+                          desc_at(t_v, sb + C::ST_V + ks * 2 * (D * 16)), idesc_mxf4(128, D, sid),
+                          (tmem + C::T_PSF + 8 * pb) | (sid << 30), (tmem + C::T_VSF + 8 * st) | (sid << 30),
+                          (pj > 0 || ks > 0));
+            }
+          } else if (!(SAGE && TRAIN) && !PLAIN) {
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
               tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
@@ -683,8 +708,19 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
         uint32_t scw[(CW + 63) / 64];
 #pragma unroll
         for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
+        if constexpr (MX) {  // 32-key UE8M0 blocks: codes + one scale byte each
+          uint32_t scs = 0;
 #pragma unroll
-        for (int blk = 0; blk < (PLAIN ? 0 : CW / 16); blk += 2) {
+          for (int b = 0; b < CW / 32; ++b) {
+            uint32_t cd[4], sc;
+            quantize_p32_mx(x + 32 * b, cd, sc);
+            *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + 32 * b, TILE)) = make_uint4(cd[0], cd[1], cd[2], cd[3]);
+            scs |= sc << (8 * b);
+          }
+          *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 32)) = static_cast<uint16_t>(scs);
+        }
+#pragma unroll
+        for (int blk = 0; blk < ((PLAIN || MX) ? 0 : CW / 16); blk += 2) {
           const PBlock qa = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16, bm[blk], rr[blk]) : quantize_p16(x + blk * 16);
           const PBlock qb =
               (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16 + 16, bm[blk + 1], rr[blk + 1]) : quantize_p16(x + blk * 16 + 16);
@@ -713,7 +749,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
             }
           }
         }
-        if (PLAIN) {
+        if (PLAIN || MX) {
         } else if (CW >= 64) {
 #pragma unroll
           for (int s = 0; s < CW / 64; ++s)
@@ -839,10 +875,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN>::NUM_THREADS, 1
   }
 }
 
-template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false>
+template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false, bool MX = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
-  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN>;
-  auto kern = attn_fwd_kernel<D, TRAIN, CS, SAGE, PLAIN>;
+  using C = Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>;
+  auto kern = attn_fwd_kernel<D, TRAIN, CS, SAGE, PLAIN, MX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -882,6 +918,12 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
     if (cudaMemcpyToSymbol(fwd::g_prof, z, sizeof(z)) != cudaSuccess) return 5;
   }
   return 0;
+}
+
+cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st) {
+  if (p.d == 64) return fwd::launch<64, false, 2, false, false, true>(p, st);
+  if (p.d == 128) return fwd::launch<128, false, 2, false, false, true>(p, st);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_attn_fwd_plain(const FwdParams& p, cudaStream_t st) {

@@ -68,6 +68,37 @@ __device__ __forceinline__ PBlock quantize_p16_r(const float* p, float amax, flo
   return b;
 }
 
+// MXFP4 P block (32 keys, codec.py:123-203): UE8M0 scale = nearest power of
+// two of amax / 6 with ties up (0 for a zero block), codes = E2M1_RNE(p / scale)
+// with the exact power-of-two reciprocal. P >= 0.
+__device__ __forceinline__ void quantize_p32_mx(const float* p, uint32_t (&codes)[4], uint32_t& sc) {
+  float m0 = p[0], m1 = p[1];
+#pragma unroll
+  for (int e = 2; e < 32; e += 2) {
+    m0 = fmaxf(m0, p[e]);
+    m1 = fmaxf(m1, p[e + 1]);
+  }
+  const float amax = fmaxf(m0, m1);
+  const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);
+  sc = 0u;
+  if (raw > 0.f) {
+    int e;
+    const float m = frexpf(raw, &e);
+    const int c = ((2.0f * m < 1.5f) ? e - 1 : e) + 127;
+    sc = static_cast<uint32_t>(c < 0 ? 0 : (c > 254 ? 254 : c));
+  }
+  const float rs = __int_as_float(static_cast<int>((254u - sc) << 23));
+  float q[32];
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const float2 v = __fmul2_rn(make_float2(p[e], p[e + 1]), make_float2(rs, rs));
+    q[e] = v.x;
+    q[e + 1] = v.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) codes[k] = cvt_e2m1x8(q + 8 * k);
+}
+
 // P = exp(S - L) for 2*NP consecutive in-tile key columns starting at column
 // c0 (c0 % 16 == 0): t = S_raw * log2(e)/sqrt(d) - L2 (one FFMA2 per pair),
 // exp2 split between MUFU and the FMA-pipe polynomial by in-tile pair index.

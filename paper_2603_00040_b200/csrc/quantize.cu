@@ -844,6 +844,91 @@ __global__ void __launch_bounds__(256) e8m0_codes_kernel(const T* __restrict__ x
 
 }  // namespace
 
+// MXFP4 attention operands straight into the MMA tiles (codec.py:123-203 per
+// block, layouts.cuh images): Q / K rows blocked along d (one SF512 image per
+// tile holds the 4 blocks of 32 of a 128-wide row), V^T blocked along tokens
+// (per column, 4 blocks of 32 tokens per tile). Padding rows / tokens are zero.
+__device__ __forceinline__ void mx_block(const float* v, uint32_t (&packed)[4], uint32_t& sc) {
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) amax = fmaxf(amax, fabsf(v[j]));
+  const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);
+  sc = raw > 0.f ? e8m0_code(raw) : 0u;
+  const float rs = __int_as_float(static_cast<int>((254u - sc) << 23));
+  float q[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) q[j] = v[j] * rs + 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) packed[k] = cvt_e2m1x8(q + 8 * k);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x_dt, int64_t heads, int64_t n,
+                                                            uint8_t* codes_t, uint8_t* sf_t) {
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t total = heads * n_pad * (D / 32);
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(t % (D / 32));
+    const int64_t rp = t / (D / 32);
+    const int64_t h = rp / n_pad, r = rp % n_pad;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = r < n ? load_elem(x, (h * n + r) * D + b * 32 + j, x_dt) : 0.f;
+    uint32_t packed[4], sc;
+    mx_block(v, packed, sc);
+    const int64_t tile = h * (n_pad / TILE) + r / TILE;
+    const int rr = static_cast<int>(r % TILE);
+    *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, 32 * b, TILE)) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    sf_t[tile * sf_tile_bytes_qk(D) + sf512_off(rr, b)] = static_cast<uint8_t>(sc);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x_dt, int64_t heads, int64_t n,
+                                                            uint8_t* codes_t, uint8_t* sf_t) {
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t total = heads * (n_pad / 32) * D;  // (head, 32-token block, column)
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % D);
+    const int64_t bb = t / D;                 // 32-token block over all heads
+    const int64_t h = bb / (n_pad / 32), tok0 = (bb % (n_pad / 32)) * 32;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = tok0 + j < n ? load_elem(x, (h * n + tok0 + j) * D + c, x_dt) : 0.f;
+    uint32_t packed[4], sc;
+    mx_block(v, packed, sc);
+    const int64_t tile = h * (n_pad / TILE) + tok0 / TILE;
+    const int kt = static_cast<int>(tok0 % TILE);
+    *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
+  }
+}
+
+cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
+                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf,
+                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf,
+                                    cudaStream_t st) {
+  const int gq = grid_for(heads * ceil_div(n_q, TILE) * TILE * (d / 32));
+  const int gk = grid_for(heads * ceil_div(n_k, TILE) * TILE * (d / 32));
+  const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * d);
+  if (d == 128) {
+    mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
+    mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
+    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf);
+  } else if (d == 64) {
+    mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
+    mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
+    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize_mx(const void* x, int x_dt, int64_t rows, int64_t cols, uint8_t* codes, uint8_t* scales,
                                void* fq, int fq_dt, int* nonfinite, cudaStream_t st) {
   quantize_mx_kernel<<<grid_for(rows * (cols / 32)), 256, 0, st>>>(x, x_dt, rows, cols, codes, scales, fq, fq_dt,

@@ -343,14 +343,15 @@ def _check_attention_shapes(Q, K, V):
     return n_q, n_k, d
 
 
-def _check_cfg(cfg, n_q, n_k, d, quantized):
+def _check_cfg(cfg, n_q, n_k, d, quantized, allow_mx=False):
     cfg.validate(n_q, n_k, quantized)
     if cfg.accum_width not in (32, 64):
         raise ShapeError(f"accum_width must be 32 or 64, got {cfg.accum_width}")
     if cfg.accum_width != 32:
         raise InvalidValue("the B200 path accumulates in fp32 (tensor cores); accum_width=64 is CPU-only")
-    if cfg.spec != NVFP4:
-        raise InvalidValue("the B200 path implements NVFP4 only")
+    from .codec import MXFP4
+    if cfg.spec != NVFP4 and not (allow_mx and cfg.spec == MXFP4):
+        raise InvalidValue("the B200 attention path implements NVFP4 (and MXFP4 for the inference forward)")
     if quantized and d % cfg.spec.block_size:
         raise ShapeError("d must be a multiple of the block size when quantizing")
     if cfg.causal and n_q > n_k:
@@ -392,10 +393,48 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     return AttnOutputs(O=o, L=lse, O_prime=o_hp)
 
 
+def attn_forward_mx(q, k, v, causal=False, out_dtype=None):
+    """MXFP4 inference forward on CUDA tensors [..., N, d] -> (O, L)
+    (flash.py:249-314 with cfg.spec = MXFP4; aq_attn_fwd_mx)."""
+    _lib.require_cuda()
+    q3, n_q, d = _heads_view(q)
+    k3, n_k, _ = _heads_view(k)
+    v3, _, _ = _heads_view(v)
+    dt = q.dtype
+    if k.dtype != dt or v.dtype != dt or dt not in _lib.DT_CODE:
+        raise InvalidValue("q, k, v must share a float32 / bfloat16 / float16 dtype")
+    q3, k3, v3 = q3.contiguous(), k3.contiguous(), v3.contiguous()
+    heads = q3.shape[0]
+    out_dtype = out_dtype or dt
+    lib = _lib.load()
+    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 0, 0)
+    if ws_bytes <= 0:
+        raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    o = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
+    lse = torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
+    args = _lib.AqFwdArgs(
+        q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
+        heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=0,
+        o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype], o_hp=None, o_hp_dtype=0,
+        lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=0, operands_staged=0)
+    _lib.check(lib.aq_attn_fwd_mx(args, _lib.stream_ptr()))
+    lead = q.shape[:-2]
+    return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)
+
+
 def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
-    """Inference forward on real FP4 codes: O, L (flash.py:249-314)."""
+    """Inference forward on real FP4 codes: O, L (flash.py:249-314); NVFP4 or
+    MXFP4 per cfg.spec."""
+    from .codec import MXFP4
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
-    _check_cfg(cfg, n_q, n_k, d, True)
+    _check_cfg(cfg, n_q, n_k, d, True, allow_mx=True)
+    if cfg.spec == MXFP4:
+        q, as_np = to_device(Q)
+        k, _ = to_device(K)
+        v, _ = to_device(V)
+        o, lse = attn_forward_mx(q, k, v, causal=cfg.causal, out_dtype=torch.float32 if as_np else None)
+        return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=None)
     if _is_host(Q):
         o, lse, _ = attn_forward_host(*(_host_f32(x) for x in (Q, K, V)), causal=cfg.causal, train=False,
                                       out_dtype=torch.float32)

@@ -22,6 +22,10 @@ for n, d, causal, b_q, b_k, tl in ((200, 64, True, 40, 200, True), (77, 128, Fal
                                    (512, 128, False, 128, 256, True)):
     q, k, v = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() + 1 for _ in range(3))
     aq.attn_forward_sage3(q, k, v, causal=causal, b_q=b_q, b_k=b_k, two_level_p=tl)
+for n, d, causal in ((200, 64, True), (77, 128, False)):
+    q, k, v = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() for _ in range(3))
+    aq.attn_forward_mx(q, k, v, causal=causal)
+    aq.fp4mm(aq.quantize(q[0, 0].float(), aq.MXFP4), aq.quantize(k[0, 0].float(), aq.MXFP4))
 x = torch.randn(37, 48, generator=g, device="cuda")
 aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))
 aq.fake_quantize(torch.randn(5, 64, generator=g, device="cuda"), aq.MXFP4)

@@ -1,0 +1,37 @@
+"""MXFP4 inference forward (flash_forward_inference with cfg.spec = MXFP4) on
+tcgen05.mma.kind::mxf4 vs the reference's own outputs (tests/golden/make_golden_mxattn.py)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_00040_b200 as aq
+from oracle import nvfp4_attn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def mx():
+    return np.load(os.path.join(GOLD, "mxattn.npz"))
+
+
+@pytest.mark.parametrize("name", ["m64", "m128c", "mrag"])
+def test_mx_inference_matches_reference(mx, name):
+    # as for NVFP4 (test_gpu_forward.py): O rel-L2 <= 1e-2 (fp32 tensor-core vs
+    # fixed-order accumulation can flip a P code at a midpoint), L <= 2e-5
+    n_q, n_k, d, causal, b_q, b_k = (int(x) for x in mx[f"{name}_meta"])
+    cfg = aq.TileConfig(b_q=b_q, b_k=b_k, causal=bool(causal), spec=aq.MXFP4)
+    outs = aq.flash_forward_inference(mx[f"{name}_Q"], mx[f"{name}_K"], mx[f"{name}_V"], cfg)
+    assert outs.O_prime is None
+    assert orc.rel_l2(outs.O, mx[f"{name}_O"]) <= 1e-2, orc.rel_l2(outs.O, mx[f"{name}_O"])
+    assert np.max(np.abs(outs.L - mx[f"{name}_L"])) <= 2e-5
+
+
+def test_mx_training_raises():
+    Q = np.zeros((128, 64))
+    with pytest.raises(aq.InvalidValue):
+        aq.flash_forward_training(Q, Q, Q, aq.TileConfig(b_q=128, b_k=128, spec=aq.MXFP4))
