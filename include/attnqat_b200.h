@@ -125,8 +125,9 @@ int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 /* flash_forward_inference with cfg.spec = MXFP4 (flash.py:249-314,
  * codec.py:123-203): Q / K / V^T quantized in 32-element blocks with UE8M0
  * scales, P in 32-key blocks, S and PV on tcgen05.mma.kind::mxf4 block32.
- * args->train must be 0; d % 32 == 0 (d in {64, 128}). Workspace:
- * aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 0, 0). */
+ * args->train = 1 also writes O' (args->o_hp; flash.py:176-246). d % 32 == 0
+ * (d in {64, 128}). Workspace: aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d,
+ * train, 0). */
 int aq_attn_fwd_mx(const AqFwdArgs* args, void* stream);
 
 /* quantized=False (flash.py:195-200): plain softmax attention on the same

@@ -425,19 +425,23 @@ int aq_attn_fwd_sage3(const AqSage3Args* a, void* stream) {
 
 int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
   if (!a || !a->q || !a->k || !a->v || !a->o || !a->lse || !a->workspace) return AQ_E_INVALID;
-  if (a->train) return AQ_E_INVALID;  // MXFP4: inference forward only
+  if (a->train && !a->o_hp) return AQ_E_INVALID;
   if (!dtype_ok(a->in_dtype) || !dtype_ok(a->o_dtype)) return AQ_E_INVALID;
   if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
   if (a->d % 32) return AQ_E_SHAPE;  // flash.py:260 with block_size 32
   if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
   if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 0);
+  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, 0);
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
   const int d = static_cast<int>(a->d);
+  if (a->train) {  // padded token rows of the V^F tiles must read as zero
+    if (cudaMemsetAsync(ws + w.v_h16, 0, a->heads * ceil_div(a->n_k, TILE) * h_tile_bytes(d), st) != cudaSuccess)
+      return AQ_E_CUDA;
+  }
   if (launch_mx_attn_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
                               ws + w.q_sf, ws + w.k_codes, ws + w.k_sf, ws + w.v_codes, ws + w.v_sf,
-                              st) != cudaSuccess)
+                              a->train ? ws + w.v_h16 : nullptr, st) != cudaSuccess)
     return AQ_E_CUDA;
   FwdParams p{};
   p.q_codes = ws + w.q_codes;
@@ -446,15 +450,18 @@ int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
   p.k_sf = ws + w.k_sf;
   p.v_codes = ws + w.v_codes;
   p.v_sf = ws + w.v_sf;
+  p.v_h = a->train ? ws + w.v_h16 : nullptr;
   p.o = a->o;
   p.o_dt = a->o_dtype;
+  p.o_hp = a->train ? a->o_hp : nullptr;
+  p.o_hp_dt = a->o_hp_dtype;
   p.lse = a->lse;
   p.heads = a->heads;
   p.n_q = a->n_q;
   p.n_k = a->n_k;
   p.d = d;
   p.causal = a->causal;
-  p.train = 0;
+  p.train = a->train;
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
   return cuda_status(launch_attn_fwd_mx(p, st));
 }

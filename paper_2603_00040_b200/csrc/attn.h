@@ -94,7 +94,7 @@ cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                     int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf,
                                     uint8_t* k_codes, uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf,
-                                    cudaStream_t st);
+                                    uint8_t* v_h16, cudaStream_t st);
 // [heads][n][d] (x_dt) -> 16-bit T8x8 tiles (fmt 0 fp16 / 1 bf16), rows zero-padded to 128
 cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int d, int fmt, uint8_t* out,
                           cudaStream_t st);

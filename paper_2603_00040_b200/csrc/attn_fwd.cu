@@ -61,7 +61,7 @@ __device__ unsigned long long g_prof[16];
 
 template <int D, bool TRAIN, int CS, bool SAGE = false, bool PLAIN = false, bool MX = false>
 struct Cfg {
-  static_assert(!MX || (!TRAIN && !SAGE && !PLAIN), "MXFP4 runs the inference layout");
+  static_assert(!MX || (!SAGE && !PLAIN), "MXFP4 runs the plain NVFP4 layouts");
   static_assert(!PLAIN || (TRAIN && !SAGE), "plain attention runs on the training layout");
   static constexpr int NSW = 4 * CS;                 // softmax warps
   static constexpr int NUM_THREADS = 32 * (NSW + 3);
@@ -921,8 +921,10 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
 }
 
 cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st) {
-  if (p.d == 64) return fwd::launch<64, false, 2, false, false, true>(p, st);
-  if (p.d == 128) return fwd::launch<128, false, 2, false, false, true>(p, st);
+  if (p.d == 64) return p.train ? fwd::launch<64, true, 2, false, false, true>(p, st)
+                                : fwd::launch<64, false, 2, false, false, true>(p, st);
+  if (p.d == 128) return p.train ? fwd::launch<128, true, 2, false, false, true>(p, st)
+                                 : fwd::launch<128, false, 2, false, false, true>(p, st);
   return cudaErrorInvalidValue;
 }
 

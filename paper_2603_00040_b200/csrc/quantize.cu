@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
 
 template <int D>
 __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x_dt, int64_t heads, int64_t n,
-                                                            uint8_t* codes_t, uint8_t* sf_t) {
+                                                            uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t) {
   const int64_t n_pad = ceil_div(n, TILE) * TILE;
   const int64_t total = heads * (n_pad / 32) * D;  // (head, 32-token block, column)
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -905,24 +905,32 @@ __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
+    if (fqh_t) {  // training: V^F as fp16 T8x8 tiles for the O' MMA (exact: E2M1 x power of two)
+      const float s = __int_as_float(static_cast<int>(sc << 23));
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
+        *reinterpret_cast<__half*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2half_rn(fv);
+      }
+    }
   }
 }
 
 cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                     int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf,
                                     uint8_t* k_codes, uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf,
-                                    cudaStream_t st) {
+                                    uint8_t* v_h16, cudaStream_t st) {
   const int gq = grid_for(heads * ceil_div(n_q, TILE) * TILE * (d / 32));
   const int gk = grid_for(heads * ceil_div(n_k, TILE) * TILE * (d / 32));
   const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * d);
   if (d == 128) {
     mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
     mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
-    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf);
+    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16);
   } else if (d == 64) {
     mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
     mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
-    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf);
+    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16);
   } else {
     return cudaErrorInvalidValue;
   }

@@ -372,9 +372,18 @@ def _np_out(t, as_np, dtype=np.float32):
 
 
 def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, threads=1):
-    """Training forward: O, L and the auxiliary O' (flash.py:176-246)."""
+    """Training forward: O, L and the auxiliary O' (flash.py:176-246); NVFP4, or
+    MXFP4 per cfg.spec."""
+    from .codec import MXFP4
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
-    _check_cfg(cfg, n_q, n_k, d, quantized)
+    _check_cfg(cfg, n_q, n_k, d, quantized, allow_mx=True)
+    if quantized and cfg.spec == MXFP4:
+        q, as_np = to_device(Q)
+        k, _ = to_device(K)
+        v, _ = to_device(V)
+        o, lse, o_hp = attn_forward_mx(q, k, v, causal=cfg.causal, out_dtype=torch.float32 if as_np else None,
+                                       train=True)
+        return AttnOutputs(O=_np_out(o, as_np), L=_np_out(lse, as_np, np.float64), O_prime=_np_out(o_hp, as_np))
     if not quantized:
         q, as_np = to_device(Q)
         k, _ = to_device(K)
@@ -393,9 +402,9 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     return AttnOutputs(O=o, L=lse, O_prime=o_hp)
 
 
-def attn_forward_mx(q, k, v, causal=False, out_dtype=None):
-    """MXFP4 inference forward on CUDA tensors [..., N, d] -> (O, L)
-    (flash.py:249-314 with cfg.spec = MXFP4; aq_attn_fwd_mx)."""
+def attn_forward_mx(q, k, v, causal=False, out_dtype=None, train=False):
+    """MXFP4 forward on CUDA tensors [..., N, d] -> (O, L), or (O, L, O') with
+    train=True (flash.py:176-314 with cfg.spec = MXFP4; aq_attn_fwd_mx)."""
     _lib.require_cuda()
     q3, n_q, d = _heads_view(q)
     k3, n_k, _ = _heads_view(k)
@@ -407,19 +416,23 @@ def attn_forward_mx(q, k, v, causal=False, out_dtype=None):
     heads = q3.shape[0]
     out_dtype = out_dtype or dt
     lib = _lib.load()
-    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 0, 0)
+    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, int(train), 0)
     if ws_bytes <= 0:
         raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
     o = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device)
+    o_hp = torch.empty((heads, n_q, d), dtype=out_dtype, device=q.device) if train else None
     lse = torch.empty((heads, n_q), dtype=torch.float32, device=q.device)
     args = _lib.AqFwdArgs(
         q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
-        heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=0,
-        o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype], o_hp=None, o_hp_dtype=0,
-        lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=0, operands_staged=0)
+        heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=int(train),
+        o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype], o_hp=o_hp.data_ptr() if train else None,
+        o_hp_dtype=_lib.DT_CODE[out_dtype], lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=0,
+        operands_staged=0)
     _lib.check(lib.aq_attn_fwd_mx(args, _lib.stream_ptr()))
     lead = q.shape[:-2]
+    if train:
+        return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q), o_hp.reshape(*lead, n_q, d)
     return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)
 
 

@@ -1,11 +1,11 @@
-"""Golden outputs of the REFERENCE's MXFP4 inference forward.
+"""Golden outputs of the REFERENCE's MXFP4 inference and training forwards.
 
 Run in the build container (where /root/reference exists):
 
     python tests/golden/make_golden_mxattn.py
 
-flash_forward_inference(Q, K, V, TileConfig(..., spec=MXFP4)) (flash.py:249-314
-with the MXFP4 codec, codec.py:123-203) on bf16-representable inputs, fp32
+flash_forward_inference / flash_forward_training(Q, K, V, TileConfig(...,
+spec=MXFP4)) (flash.py:176-314 with the MXFP4 codec, codec.py:123-203) on bf16-representable inputs, fp32
 accumulation. Writes mxattn.npz next to this script.
 """
 
@@ -31,14 +31,16 @@ def bf16(x):
 def main():
     sys.path.insert(0, REF)
     from attnqat.codec import MXFP4
-    from attnqat.flash import TileConfig, flash_forward_inference
+    from attnqat.flash import TileConfig, flash_forward_inference, flash_forward_training
 
     out = {}
     for i, (name, (n_q, n_k, d, causal, b_q, b_k)) in enumerate(CASES.items()):
         g = np.random.default_rng(500 + i)
         Q, K, V = (bf16(g.standard_normal((n, d))) for n in (n_q, n_k, n_k))
-        o = flash_forward_inference(Q, K, V, TileConfig(b_q=b_q, b_k=b_k, causal=causal, accum_width=32, spec=MXFP4))
-        for k_, v_ in dict(Q=Q, K=K, V=V, O=o.O, L=o.L).items():
+        cfg = TileConfig(b_q=b_q, b_k=b_k, causal=causal, accum_width=32, spec=MXFP4)
+        o = flash_forward_inference(Q, K, V, cfg)
+        t = flash_forward_training(Q, K, V, cfg)
+        for k_, v_ in dict(Q=Q, K=K, V=V, O=o.O, L=o.L, Otr=t.O, Ltr=t.L, Op=t.O_prime).items():
             out[f"{name}_{k_}"] = v_
         out[f"{name}_meta"] = np.array([n_q, n_k, d, int(causal), b_q, b_k])
         print(name, "done", flush=True)

@@ -31,7 +31,14 @@ def test_mx_inference_matches_reference(mx, name):
     assert np.max(np.abs(outs.L - mx[f"{name}_L"])) <= 2e-5
 
 
-def test_mx_training_raises():
-    Q = np.zeros((128, 64))
-    with pytest.raises(aq.InvalidValue):
-        aq.flash_forward_training(Q, Q, Q, aq.TileConfig(b_q=128, b_k=128, spec=aq.MXFP4))
+@pytest.mark.parametrize("name", ["m64", "m128c", "mrag"])
+def test_mx_training_forward_matches_reference(mx, name):
+    # O, L as the inference forward; O' = P V^F (fp16 P^ in the f16 MMA): <= 2e-3
+    n_q, n_k, d, causal, b_q, b_k = (int(x) for x in mx[f"{name}_meta"])
+    cfg = aq.TileConfig(b_q=b_q, b_k=b_k, causal=bool(causal), spec=aq.MXFP4)
+    outs = aq.flash_forward_training(mx[f"{name}_Q"], mx[f"{name}_K"], mx[f"{name}_V"], cfg)
+    assert orc.rel_l2(outs.O, mx[f"{name}_Otr"]) <= 1e-2
+    assert orc.rel_l2(outs.O_prime, mx[f"{name}_Op"]) <= 2e-3
+    assert np.max(np.abs(outs.L - mx[f"{name}_Ltr"])) <= 2e-5
+    inf = aq.flash_forward_inference(mx[f"{name}_Q"], mx[f"{name}_K"], mx[f"{name}_V"], cfg)
+    np.testing.assert_array_equal(outs.O, inf.O)   # same MMAs, same P codes
