@@ -195,6 +195,10 @@ typedef struct {
 int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d);
 /* Replaces flash_backward (flash.py:317-390). */
 int aq_attn_bwd(const AqBwdArgs* args, void* stream);
+/* The same for MXFP4 operands (cfg.spec = MXFP4): S recomputed on
+ * tcgen05.mma.kind::mxf4 block32, P^F in 32-key UE8M0 blocks, Q^F / K^F / V^F
+ * re-quantized from args->q / k / v (args->fwd_workspace is ignored); d % 32 == 0. */
+int aq_attn_bwd_mx(const AqBwdArgs* args, void* stream);
 
 /* ---- measurement utilities (bench.py roofline denominators) ---------------
  * One CTA per SM issuing back-to-back tcgen05 MMAs from shared memory:

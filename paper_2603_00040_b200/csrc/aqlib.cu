@@ -545,7 +545,15 @@ int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int
   return bwd_ws(heads, n_q, n_k, d).total;
 }
 
-int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
+static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx);
+
+int aq_attn_bwd(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stream, false); }
+
+int aq_attn_bwd_mx(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stream, true); }
+
+}  // extern "C"
+
+static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx) {
   if (!a || !a->q || !a->k || !a->v || !a->d_o || !a->lse || !a->dq || !a->dk || !a->dv || !a->workspace)
     return AQ_E_INVALID;
   if (!dtype_ok(a->in_dtype) || !dtype_ok(a->do_dtype) || !dtype_ok(a->o_dtype) || !dtype_ok(a->g_dtype))
@@ -565,7 +573,18 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
   const FwdWs fw = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 1);
   const uint8_t* ops;
   FwdWs w;
-  if (a->fwd_workspace) {
+  if (mx) {
+    // MXFP4 (codec.py:123-203): Q / K codes + UE8M0 images for the S recompute,
+    // bf16 Q^F / K^F / V^F tiles for the 16-bit MMAs
+    if (a->d % 32) return AQ_E_SHAPE;
+    uint8_t* b = ws + bw.fwd;
+    if (launch_mx_bwd_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, static_cast<int>(a->d),
+                               b + fw.q_codes, b + fw.q_sf, b + fw.q_hb, b + fw.k_codes, b + fw.k_sf, b + fw.k_hb,
+                               b + fw.v_codes, b + fw.v_sf, b + fw.v_hb, st) != cudaSuccess)
+      return AQ_E_CUDA;
+    ops = b;
+    w = fw;
+  } else if (a->fwd_workspace) {
     ops = static_cast<const uint8_t*>(a->fwd_workspace);
     w = fw;
   } else {
@@ -600,9 +619,8 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) {
   p.d = static_cast<int>(a->d);
   p.causal = a->causal;
   p.fq_p = (a->variant == AQ_BWD_CORRECT || a->variant == AQ_BWD_LOW_PREC_O) ? 1 : 0;  // flash.py:93-95
+  p.mx = mx ? 1 : 0;
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
   p.inv_sqrt_d = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a->d)));
   return cuda_status(launch_attn_bwd(p, st));
 }
-
-}  // extern "C"

@@ -159,7 +159,7 @@ enum KvBar {
 //   dP_i half 0 | S_{i+1} | dP_i half 1 | dV_i (once P^F_i is in SMEM) | dK_i (once dS_i is)
 // so S_{i+1} runs while the compute warps are still on tile i, and the Q
 // codes / dO / Q^F rings are released by the MMA that last reads them.
-template <int D>
+template <int D, bool MX>
 __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head) {
   using L = KvSmem<D>;
   constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
@@ -288,11 +288,21 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       tc_fence_after();
       if (elect_one()) {
         // S = Q K^T (FP4, same instruction sequence as the forward)
-        for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + KV_T_QSF + 4 * ks, desc_at(t_sf, qc + TILE * D / 2 + ks * 512));
-        for (int ks = 0; ks < D / 64; ++ks)
-          mma_nvf4_ss(tmem + KV_T_S, desc_at(t_fp4, qc + ks * 4096), desc_at(t_fp4, k_codes + ks * 4096), id_s,
-                      tmem + KV_T_QSF + 4 * ks, tmem + KV_T_KSF + 4 * ks, ks > 0);
+        if constexpr (MX) {
+          tmem_cp_32x128_x4(tmem + KV_T_QSF, desc_at(t_sf, qc + TILE * D / 2));
+          for (int ks = 0; ks < D / 64; ++ks) {
+            const uint32_t sid = 2u * ks;
+            mma_mxf4_ss(tmem + KV_T_S, desc_at(t_fp4, qc + ks * 4096), desc_at(t_fp4, k_codes + ks * 4096),
+                        idesc_mxf4(128, 128, sid), (tmem + KV_T_QSF) | (sid << 30), (tmem + KV_T_KSF) | (sid << 30),
+                        ks > 0);
+          }
+        } else {
+          for (int ks = 0; ks < D / 64; ++ks)
+            tmem_cp_32x128_x4(tmem + KV_T_QSF + 4 * ks, desc_at(t_sf, qc + TILE * D / 2 + ks * 512));
+          for (int ks = 0; ks < D / 64; ++ks)
+            mma_nvf4_ss(tmem + KV_T_S, desc_at(t_fp4, qc + ks * 4096), desc_at(t_fp4, k_codes + ks * 4096), id_s,
+                        tmem + KV_T_QSF + 4 * ks, tmem + KV_T_KSF + 4 * ks, ks > 0);
+        }
         tc_commit(&bars[KV_B_S_FULL]);
         tc_commit(&bars[KV_B_QC_EMPTY + s]);
       }
@@ -402,6 +412,25 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       if (ii > 0) mbar_wait(&bars[KV_B_PF_FREE], (ii - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       // P^F (or P) -> bf16 [query][key] T8x8
+      if (MX && p.fq_p) {  // MXFP4 P^F: 32-key UE8M0 blocks, dequantized exactly to bf16
+#pragma unroll
+        for (int b32 = 0; b32 < KPT / 32; ++b32) {
+          uint32_t cd[4], sc;
+          quantize_p32_mx(pr + 32 * b32, cd, sc);
+          const float sv = __int_as_float(static_cast<int>(sc << 23));
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t c0 = (cd[g] >> (8 * e)) & 0xF, c1 = (cd[g] >> (8 * e + 4)) & 0xF;
+              o[e] = pack_bf16(e2m1_to_f32(c0) * sv, e2m1_to_f32(c1) * sv);
+            }
+            *reinterpret_cast<uint4*>(p_h + t8x8_off(row, kb + 32 * b32 + 8 * g)) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      }
+if (!(MX && p.fq_p)) {
 #pragma unroll
       for (int blk = 0; blk < KPT / 16; ++blk) {
         uint4 w[2];
@@ -438,6 +467,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
         }
         *reinterpret_cast<uint4*>(p_h + t8x8_off(row, kb + blk * 16)) = w[0];
         *reinterpret_cast<uint4*>(p_h + t8x8_off(row, kb + blk * 16 + 8)) = w[1];
+      }
       }
       fence_async_smem();
       mbar_arrive(&bars[KV_B_PF_FULL]);
@@ -518,7 +548,7 @@ enum QBar {
 
 // MMA issue order: S_0 dP_0 | S_1 dP_1 dQ_0 | S_2 dP_2 dQ_1 | ... so S_{j+1} and
 // dP_{j+1} run while the compute warps turn S_j / dP_j into dS_j.
-template <int D>
+template <int D, bool MX>
 __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, int qt, int64_t head) {
   using L = QSmem<D>;
   constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
@@ -633,11 +663,21 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       if (j > 0) mbar_wait(&bars[Q_B_S_EMPTY], (j - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        for (int ks = 0; ks < D / 64; ++ks)
-          tmem_cp_32x128_x4(tmem + Q_T_KSF + 8 * st + 4 * ks, desc_at(t_sf, kc + TILE * D / 2 + ks * 512));
-        for (int ks = 0; ks < D / 64; ++ks)
-          mma_nvf4_ss(tmem + Q_T_S, desc_at(t_fp4, q_codes + ks * 4096), desc_at(t_fp4, kc + ks * 4096), id_s,
-                      tmem + Q_T_QSF + 4 * ks, tmem + Q_T_KSF + 8 * st + 4 * ks, ks > 0);
+        if constexpr (MX) {
+          tmem_cp_32x128_x4(tmem + Q_T_KSF + 8 * st, desc_at(t_sf, kc + TILE * D / 2));
+          for (int ks = 0; ks < D / 64; ++ks) {
+            const uint32_t sid = 2u * ks;
+            mma_mxf4_ss(tmem + Q_T_S, desc_at(t_fp4, q_codes + ks * 4096), desc_at(t_fp4, kc + ks * 4096),
+                        idesc_mxf4(128, 128, sid), (tmem + Q_T_QSF) | (sid << 30),
+                        (tmem + Q_T_KSF + 8 * st) | (sid << 30), ks > 0);
+          }
+        } else {
+          for (int ks = 0; ks < D / 64; ++ks)
+            tmem_cp_32x128_x4(tmem + Q_T_KSF + 8 * st + 4 * ks, desc_at(t_sf, kc + TILE * D / 2 + ks * 512));
+          for (int ks = 0; ks < D / 64; ++ks)
+            mma_nvf4_ss(tmem + Q_T_S, desc_at(t_fp4, q_codes + ks * 4096), desc_at(t_fp4, kc + ks * 4096), id_s,
+                        tmem + Q_T_QSF + 4 * ks, tmem + Q_T_KSF + 8 * st + 4 * ks, ks > 0);
+        }
         tc_commit(&bars[Q_B_S_FULL]);
         tc_commit(&bars[Q_B_KC_EMPTY + st]);
       }
@@ -751,7 +791,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 // ranks alternate KV tile 0, Q tile T-1, KV tile 1, Q tile T-2, ... Items of
 // one head run together and share its operands in L2 (head-fastest order
 // is 18% slower at C4); KV and Q items share no barriers.
-template <int D>
+template <int D, bool MX>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t head = blockIdx.y;
@@ -766,8 +806,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
   } else {
     qt = q_tiles - 1 - (r - m);
   }
-  if (kv >= 0) bwd_kv_tile<D>(p, smem, kv, head);
-  else bwd_q_tile<D>(p, smem, qt, head);
+  if (kv >= 0) bwd_kv_tile<D, MX>(p, smem, kv, head);
+  else bwd_q_tile<D, MX>(p, smem, qt, head);
 }
 
 // K6: D = rowsum(dO . O_ref) (fp32) and dO -> bf16 T8x8 tiles (pad rows zero).
@@ -843,7 +883,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt
 
 template <int D>
 cudaError_t launch(const BwdParams& p, cudaStream_t st) {
-  auto kern = attn_bwd_kernel<D>;
+  auto kern = p.mx ? attn_bwd_kernel<D, true> : attn_bwd_kernel<D, false>;
   constexpr int smem = KvSmem<D>::TOTAL > QSmem<D>::TOTAL ? KvSmem<D>::TOTAL : QSmem<D>::TOTAL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

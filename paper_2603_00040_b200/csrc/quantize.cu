@@ -864,7 +864,7 @@ __device__ __forceinline__ void mx_block(const float* v, uint32_t (&packed)[4], 
 
 template <int D>
 __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x_dt, int64_t heads, int64_t n,
-                                                            uint8_t* codes_t, uint8_t* sf_t) {
+                                                            uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t = nullptr) {
   const int64_t n_pad = ceil_div(n, TILE) * TILE;
   const int64_t total = heads * n_pad * (D / 32);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -882,12 +882,30 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, 32 * b, TILE)) =
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * sf_tile_bytes_qk(D) + sf512_off(rr, b)] = static_cast<uint8_t>(sc);
+    if (fqh_t) {  // the bf16 fake-quantized operand tile of the backward (T8x8)
+      const float s = __int_as_float(static_cast<int>(sc << 23));
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j0 = 8 * g + 2 * e;
+          const float a = e2m1_to_f32((packed[j0 >> 3] >> (4 * (j0 & 7))) & 0xF) * s;
+          const float c2 = e2m1_to_f32((packed[(j0 + 1) >> 3] >> (4 * ((j0 + 1) & 7))) & 0xF) * s;
+          const __nv_bfloat162 bv = __floats2bfloat162_rn(a, c2);
+          w[e] = *reinterpret_cast<const uint32_t*>(&bv);
+        }
+        *reinterpret_cast<uint4*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(rr, 32 * b + 8 * g)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
   }
 }
 
 template <int D>
 __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x_dt, int64_t heads, int64_t n,
-                                                            uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t) {
+                                                            uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t,
+                                                            int fqh_bf16 = 0) {
   const int64_t n_pad = ceil_div(n, TILE) * TILE;
   const int64_t total = heads * (n_pad / 32) * D;  // (head, 32-token block, column)
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -910,10 +928,36 @@ __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
-        *reinterpret_cast<__half*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2half_rn(fv);
+        if (fqh_bf16)
+          *reinterpret_cast<__nv_bfloat16*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) =
+              __float2bfloat16_rn(fv);
+        else
+          *reinterpret_cast<__half*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2half_rn(fv);
       }
     }
   }
+}
+
+cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
+                                   int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf, uint8_t* q_h,
+                                   uint8_t* k_codes, uint8_t* k_sf, uint8_t* k_h, uint8_t* v_codes, uint8_t* v_sf,
+                                   uint8_t* v_h, cudaStream_t st) {
+  const int gq = grid_for(heads * ceil_div(n_q, TILE) * TILE * (d / 32));
+  const int gk = grid_for(heads * ceil_div(n_k, TILE) * TILE * (d / 32));
+  const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * d);
+  // (the V^T codes / scales are a by-product here: the backward reads V^F only)
+  if (d == 128) {
+    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1);
+    mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
+    mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
+  } else if (d == 64) {
+    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1);
+    mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
+    mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,

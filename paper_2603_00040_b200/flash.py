@@ -159,13 +159,13 @@ def attn_forward(q, k, v, causal=False, train=True, out_dtype=None, keep_for_bwd
 
 
 def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.CORRECT, grad_dtype=None,
-                  fwd_workspace=None, workspace=None, grads_out=None, quantized=True):
+                  fwd_workspace=None, workspace=None, grads_out=None, quantized=True, mx=False):
     """Fused QAT backward on CUDA tensors -> (dQ, dK, dV) (flash.py:317-390)."""
     _lib.require_cuda()
     if q.device.type == "cuda" and q.device.index is not None and q.device.index != torch.cuda.current_device():
         with torch.cuda.device(q.device):
             return attn_backward(q, k, v, d_o, o, o_hp, lse, causal, variant, grad_dtype, fwd_workspace,
-                                 workspace, grads_out, quantized)
+                                 workspace, grads_out, quantized, mx)
     q3, n_q, d = _heads_view(q)
     k3, n_k, _ = _heads_view(k)
     v3, _, _ = _heads_view(v)
@@ -218,7 +218,7 @@ def attn_backward(q, k, v, d_o, o, o_hp, lse, causal=False, variant=BwdVariant.C
         variant=variant.code, dq=dq.data_ptr(), dk=dk.data_ptr(), dv=dv.data_ptr(),
         g_dtype=_lib.DT_CODE[grad_dtype], workspace=ws.data_ptr(),
         fwd_workspace=fwd_workspace.data_ptr() if fwd_workspace is not None else None)
-    _lib.check(lib.aq_attn_bwd(args, _lib.stream_ptr()))
+    _lib.check((lib.aq_attn_bwd_mx if mx else lib.aq_attn_bwd)(args, _lib.stream_ptr()))
     return (dq.reshape(q.shape[:-2] + (n_q, d)), dk.reshape(k.shape[:-2] + (n_k, d)),
             dv.reshape(v.shape[:-2] + (n_k, d)))
 
@@ -461,8 +461,9 @@ def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
 
 def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized=True, instrument=None):
     """Recompute-and-requantize QAT backward (flash.py:317-390)."""
+    from .codec import MXFP4
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
-    _check_cfg(cfg, n_q, n_k, d, quantized)
+    _check_cfg(cfg, n_q, n_k, d, quantized, allow_mx=True)
     if tuple(dO.shape) != tuple(Q.shape):
         raise ShapeError(f"dO shape {tuple(dO.shape)} does not match Q {tuple(Q.shape)}")
     if tuple(outs.L.shape) != tuple(Q.shape[:-1]):
@@ -479,5 +480,5 @@ def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized
     g_dt = torch.float32 if as_np else None
     dq, dk, dv = attn_backward(q, k, v, d_o.to(q.dtype) if d_o.dtype != q.dtype and not as_np else d_o,
                                o, o_hp, lse, causal=cfg.causal, variant=variant, grad_dtype=g_dt,
-                               quantized=quantized)
+                               quantized=quantized, mx=quantized and cfg.spec == MXFP4)
     return AttnGrads(dQ=_np_out(dq, as_np), dK=_np_out(dk, as_np), dV=_np_out(dv, as_np))

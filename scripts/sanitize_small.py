@@ -25,6 +25,8 @@ for n, d, causal, b_q, b_k, tl in ((200, 64, True, 40, 200, True), (77, 128, Fal
 for n, d, causal in ((200, 64, True), (77, 128, False)):
     q, k, v = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() for _ in range(3))
     aq.attn_forward_mx(q, k, v, causal=causal)
+    o, lse, o_hp = aq.attn_forward_mx(q, k, v, causal=causal, train=True)
+    aq.attn_backward(q, k, v, torch.randn_like(q), o, o_hp, lse, causal=causal, mx=True)
     aq.fp4mm(aq.quantize(q[0, 0].float(), aq.MXFP4), aq.quantize(k[0, 0].float(), aq.MXFP4))
 x = torch.randn(37, 48, generator=g, device="cuda")
 aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))

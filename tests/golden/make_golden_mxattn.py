@@ -1,4 +1,4 @@
-"""Golden outputs of the REFERENCE's MXFP4 inference and training forwards.
+"""Golden outputs of the REFERENCE's MXFP4 inference / training forwards and backward.
 
 Run in the build container (where /root/reference exists):
 
@@ -31,7 +31,7 @@ def bf16(x):
 def main():
     sys.path.insert(0, REF)
     from attnqat.codec import MXFP4
-    from attnqat.flash import TileConfig, flash_forward_inference, flash_forward_training
+    from attnqat.flash import TileConfig, flash_backward, flash_forward_inference, flash_forward_training
 
     out = {}
     for i, (name, (n_q, n_k, d, causal, b_q, b_k)) in enumerate(CASES.items()):
@@ -40,7 +40,10 @@ def main():
         cfg = TileConfig(b_q=b_q, b_k=b_k, causal=causal, accum_width=32, spec=MXFP4)
         o = flash_forward_inference(Q, K, V, cfg)
         t = flash_forward_training(Q, K, V, cfg)
-        for k_, v_ in dict(Q=Q, K=K, V=V, O=o.O, L=o.L, Otr=t.O, Ltr=t.L, Op=t.O_prime).items():
+        dO = bf16(g.standard_normal((n_q, d)))
+        gr = flash_backward(Q, K, V, dO, t, cfg)
+        for k_, v_ in dict(Q=Q, K=K, V=V, O=o.O, L=o.L, Otr=t.O, Ltr=t.L, Op=t.O_prime, dO=dO, dQ=gr.dQ, dK=gr.dK,
+                           dV=gr.dV).items():
             out[f"{name}_{k_}"] = v_
         out[f"{name}_meta"] = np.array([n_q, n_k, d, int(causal), b_q, b_k])
         print(name, "done", flush=True)

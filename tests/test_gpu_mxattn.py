@@ -42,3 +42,15 @@ def test_mx_training_forward_matches_reference(mx, name):
     assert np.max(np.abs(outs.L - mx[f"{name}_Ltr"])) <= 2e-5
     inf = aq.flash_forward_inference(mx[f"{name}_Q"], mx[f"{name}_K"], mx[f"{name}_V"], cfg)
     np.testing.assert_array_equal(outs.O, inf.O)   # same MMAs, same P codes
+
+
+@pytest.mark.parametrize("name", ["m64", "m128c", "mrag"])
+def test_mx_backward_matches_reference(mx, name):
+    # as for NVFP4 (test_gpu_backward.py): bf16 operands in the 16-bit MMAs -> 1e-2
+    n_q, n_k, d, causal, b_q, b_k = (int(x) for x in mx[f"{name}_meta"])
+    cfg = aq.TileConfig(b_q=b_q, b_k=b_k, causal=bool(causal), spec=aq.MXFP4)
+    Q, K, V, dO = (mx[f"{name}_{t}"] for t in ("Q", "K", "V", "dO"))
+    outs = aq.flash_forward_training(Q, K, V, cfg)
+    g = aq.flash_backward(Q, K, V, dO, outs, cfg)
+    for t in ("dQ", "dK", "dV"):
+        assert orc.rel_l2(getattr(g, t), mx[f"{name}_{t}"]) <= 1e-2, (t, orc.rel_l2(getattr(g, t), mx[f"{name}_{t}"]))
