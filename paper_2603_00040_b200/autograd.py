@@ -12,29 +12,37 @@ from __future__ import annotations
 
 import torch
 
-from .flash import BwdVariant, attn_backward, attn_forward
+from .flash import BwdVariant, attn_backward, attn_forward, attn_forward_mx
 
 
 class AttnQATFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True):
-        o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True, quantized=quantized)
+    def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True, mx=False):
+        if quantized and mx:   # MXFP4 (the backward re-quantizes from q / k / v)
+            o, lse, o_hp = attn_forward_mx(q, k, v, causal=causal, train=True)
+            ws = torch.empty(0, dtype=torch.uint8, device=q.device)
+        else:
+            o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True,
+                                            quantized=quantized)
         ctx.save_for_backward(q, k, v, o, o_hp, lse, ws)
         ctx.causal = causal
         ctx.variant = variant
         ctx.quantized = quantized
+        ctx.mx = quantized and mx
         return o
 
     @staticmethod
     def backward(ctx, d_o):
         q, k, v, o, o_hp, lse, ws = ctx.saved_tensors
         dq, dk, dv = attn_backward(q, k, v, d_o.contiguous(), o, o_hp, lse, causal=ctx.causal,
-                                   variant=ctx.variant, grad_dtype=q.dtype, fwd_workspace=ws,
-                                   quantized=ctx.quantized)
-        return dq, dk, dv, None, None, None
+                                   variant=ctx.variant, grad_dtype=q.dtype,
+                                   fwd_workspace=None if ctx.mx else ws, quantized=ctx.quantized, mx=ctx.mx)
+        return dq, dk, dv, None, None, None, None
 
 
-def attn_qat(q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True):
+def attn_qat(q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True, spec=None):
     """NVFP4 QAT attention: O = softmax_fq(Q^F K^F^T / sqrt(d)) V^F with the Attn-QAT backward.
+    ``spec=MXFP4`` runs the MXFP4 format (UE8M0 scales per 32 elements);
     ``quantized=False`` is the reference's bf16 mode (plain attention, plain.py)."""
-    return AttnQATFunction.apply(q, k, v, causal, variant, quantized)
+    from .codec import MXFP4
+    return AttnQATFunction.apply(q, k, v, causal, variant, quantized, spec == MXFP4)

@@ -38,6 +38,8 @@ ATTN_MODES = {
     "fp4-qat/lowpreco": (True, BwdVariant.LOW_PREC_O),
     "fp4-qat/nofqp": (True, BwdVariant.NO_FAKE_QUANT_P),
     "fp4-qat/naive-bf16-bwd": (True, BwdVariant.NAIVE_BF16_BWD),
+    # the MXFP4 format (UE8M0 scales per 32 elements) with the correct backward
+    "mxfp4-qat": (True, BwdVariant.CORRECT),
 }
 TASK_COMMON_GAIN = 12.0  # harness.py:37
 DIVERGENCE_LOSS = 1e6
@@ -245,6 +247,11 @@ def train(cfg: TrainConfig, device=None, attn_fn=None, log_every=0):
     if problems:
         raise InvalidValue("; ".join(problems))
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
+    if attn_fn is None and cfg.attn_mode == "mxfp4-qat":
+        from .codec import MXFP4
+
+        def attn_fn(q, k, v, causal, variant, quantized=True):
+            return attn_qat(q, k, v, causal, variant, quantized, spec=MXFP4)
     layer = AttnLayer(cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.seed, device, attn_fn)
     opt = torch.optim.AdamW(layer.parameters(), lr=cfg.lr, betas=(cfg.beta1, cfg.beta2),
                             weight_decay=cfg.weight_decay)

@@ -54,3 +54,15 @@ def test_mx_backward_matches_reference(mx, name):
     g = aq.flash_backward(Q, K, V, dO, outs, cfg)
     for t in ("dQ", "dK", "dV"):
         assert orc.rel_l2(getattr(g, t), mx[f"{name}_{t}"]) <= 1e-2, (t, orc.rel_l2(getattr(g, t), mx[f"{name}_{t}"]))
+
+
+def test_mx_autograd_matches_functional():
+    g = torch.Generator(device="cuda").manual_seed(21)
+    q, k, v = (torch.randn(2, 2, 256, 64, generator=g, device="cuda").bfloat16().requires_grad_() for _ in range(3))
+    o = aq.attn_qat(q, k, v, causal=True, spec=aq.MXFP4)
+    d_o = torch.randn_like(o)
+    o.backward(d_o)
+    o2, lse, o_hp = aq.attn_forward_mx(q.detach(), k.detach(), v.detach(), causal=True, train=True)
+    dq, dk, dv = aq.attn_backward(q.detach(), k.detach(), v.detach(), d_o, o2, o_hp, lse, causal=True, mx=True)
+    assert torch.equal(o, o2)
+    assert torch.equal(q.grad, dq) and torch.equal(k.grad, dk) and torch.equal(v.grad, dv)

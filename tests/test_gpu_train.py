@@ -18,7 +18,7 @@ def test_qat_training_reduces_loss():
     assert last < 0.8 * first
 
 
-@pytest.mark.parametrize("mode", ["fp4-qat/lowpreco", "fp4-qat/nofqp", "fp4-qat/naive-bf16-bwd"])
+@pytest.mark.parametrize("mode", ["fp4-qat/lowpreco", "fp4-qat/nofqp", "fp4-qat/naive-bf16-bwd", "mxfp4-qat"])
 def test_ablation_variants_run(mode):
     cfg = T.TrainConfig(steps=3, seq_len=128, batch=4, d_model=128, n_heads=2, head_dim=64, attn_mode=mode)
     _, log = T.train(cfg)
