@@ -921,6 +921,8 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
 }
 
 cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st) {
+  // inference: the split-pass kernel; AQ_FWD_INFER=0 keeps it on K4 (comparisons)
+  if (!p.train && env_int("AQ_FWD_INFER", 1)) return launch_attn_fwd_infer_mx(p, st);
   if (p.d == 64) return p.train ? fwd::launch<64, true, 2, false, false, true>(p, st)
                                 : fwd::launch<64, false, 2, false, false, true>(p, st);
   if (p.d == 128) return p.train ? fwd::launch<128, true, 2, false, false, true>(p, st)

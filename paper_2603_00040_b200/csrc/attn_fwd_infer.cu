@@ -105,7 +105,10 @@ __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_t
   return it;
 }
 
-template <int D>
+// MX: the MXFP4 variant (codec.py:123-203) -- S and PV on kind::mxf4 block32
+// with one scale-factor image per 128 K (IDs 0 / 2 per K = 64 step), P in
+// 32-key UE8M0 blocks; same pipeline.
+template <int D, bool MX = false>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       mbar_wait(&bars[C::B_Q_FULL + qs], (k / C::NQ) & 1);
       tc_fence_after();
       if (elect_one()) {
-        for (int ks = 0; ks < D / 64; ++ks)
+        for (int ks = 0; ks < (MX ? 1 : D / 64); ++ks)
           tmem_cp_32x128_x4(tmem + C::T_QSF + 8 * qs + 4 * ks, desc_at(t_sf, qb + C::QC_BYTES + ks * 512));
         tc_commit(&bars[C::B_QSF + qs]);  // Q scale factors in TMEM, for MMA B too
       }
@@ -231,13 +234,24 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         tc_fence_after();
         const uint32_t kb = s0 + C::KA0 + st * C::KA_BYTES;
         if (elect_one()) {
+          if constexpr (MX) {
+            tmem_cp_32x128_x4(tmem + C::T_KSFA + 8 * st, desc_at(t_sf, kb + C::QC_BYTES));
 #pragma unroll
-          for (int ks = 0; ks < D / 64; ++ks)
-            tmem_cp_32x128_x4(tmem + C::T_KSFA + 8 * st + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
+            for (int ks = 0; ks < D / 64; ++ks) {
+              const uint32_t sid = 2u * ks;
+              mma_mxf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096),
+                          idesc_mxf4(128, 128, sid), (tmem + C::T_QSF + 8 * qs) | (sid << 30),
+                          (tmem + C::T_KSFA + 8 * st) | (sid << 30), ks > 0);
+            }
+          } else {
 #pragma unroll
-          for (int ks = 0; ks < D / 64; ++ks)
-            mma_nvf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
-                        tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFA + 8 * st + 4 * ks, ks > 0);
+            for (int ks = 0; ks < D / 64; ++ks)
+              tmem_cp_32x128_x4(tmem + C::T_KSFA + 8 * st + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
+#pragma unroll
+            for (int ks = 0; ks < D / 64; ++ks)
+              mma_nvf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
+                          tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFA + 8 * st + 4 * ks, ks > 0);
+          }
           tc_commit(&bars[C::B_SA_FULL]);
           tc_commit(&bars[C::B_KA_EMPTY + st]);
         }
@@ -263,13 +277,24 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           tc_fence_after();
           const uint32_t kb = s0 + C::KB0 + st * C::KB_BYTES;
           if (elect_one()) {
+            if constexpr (MX) {
+              tmem_cp_32x128_x4(tmem + C::T_KSFB + 8 * st, desc_at(t_sf, kb + C::QC_BYTES));
 #pragma unroll
-            for (int ks = 0; ks < D / 64; ++ks)
-              tmem_cp_32x128_x4(tmem + C::T_KSFB + 8 * st + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
+              for (int ks = 0; ks < D / 64; ++ks) {
+                const uint32_t sid = 2u * ks;
+                mma_mxf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096),
+                            idesc_mxf4(128, 128, sid), (tmem + C::T_QSF + 8 * qs) | (sid << 30),
+                            (tmem + C::T_KSFB + 8 * st) | (sid << 30), ks > 0);
+              }
+            } else {
 #pragma unroll
-            for (int ks = 0; ks < D / 64; ++ks)
-              mma_nvf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
-                          tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFB + 8 * st + 4 * ks, ks > 0);
+              for (int ks = 0; ks < D / 64; ++ks)
+                tmem_cp_32x128_x4(tmem + C::T_KSFB + 8 * st + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
+#pragma unroll
+              for (int ks = 0; ks < D / 64; ++ks)
+                mma_nvf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
+                            tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFB + 8 * st + 4 * ks, ks > 0);
+            }
             tc_commit(&bars[C::B_SB_FULL]);
             if (ns == nt - 1) tc_commit(&bars[C::B_Q_EMPTY + qs]);  // last read of this Q slot
           }
@@ -287,16 +312,29 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         const uint32_t sb = s0 + C::KB0 + st * C::KB_BYTES;
         const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
         if (elect_one()) {
+          if constexpr (MX) {
+            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb, desc_at(t_sf, pbase + C::PB_SF));
+            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st, desc_at(t_sf, sb + C::KB_VSF));
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
-            tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::KB_VSF + ks * 512));
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t sid = 2u * ks;
+              mma_mxf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096),
+                          desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)), idesc_mxf4(128, D, sid),
+                          (tmem + C::T_PSF + 8 * pb) | (sid << 30), (tmem + C::T_VSF + 8 * st) | (sid << 30),
+                          (pj > 0 || ks > 0));
+            }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
+              tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::KB_VSF + ks * 512));
+            }
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096),
+                          desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
+                          tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
           }
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096), desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)),
-                        id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks, tmem + C::T_VSF + 8 * st + 4 * ks,
-                        (pj > 0 || ks > 0));
           tc_commit(&bars[C::B_P_EMPTY + pb]);
           tc_commit(&bars[C::B_KB_EMPTY + st]);
         }
@@ -443,6 +481,14 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             qa.scale = __float_as_uint(x[blk * 16]) & 0xff; qa.codes[0] = __float_as_uint(x[blk * 16 + 1]); qa.codes[1] = __float_as_uint(x[blk * 16 + 2]);
             qb = qa;
 #else
+            if constexpr (MX) {
+              uint32_t cd[4], sc;
+              quantize_p32_mx(x + blk * 16, cd, sc);
+              *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
+                  make_uint4(cd[0], cd[1], cd[2], cd[3]);
+              scw[0] |= sc << (8 * (blk / 2));
+              return;
+            }
             const PBlock qa = quantize_p16(x + blk * 16);
             const PBlock qb = quantize_p16(x + blk * 16 + 16);
 #endif
@@ -457,9 +503,13 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
 #pragma unroll
             for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, true);
           }
+          if constexpr (MX) {
+            *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 32)) = static_cast<uint16_t>(scw[0]);
+          } else {
 #pragma unroll
-          for (int s = 0; s < CW / 64; ++s)
-            *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
+            for (int s = 0; s < CW / 64; ++s)
+              *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
+          }
           fence_async_smem();
           mbar_arrive(&bars[C::B_P_FULL + pb]);
         }
@@ -510,10 +560,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   }
 }
 
-template <int D>
+template <int D, bool MX = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   using C = Cfg<D>;
-  auto kern = attn_fwd_infer_kernel<D>;
+  auto kern = attn_fwd_infer_kernel<D, MX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -530,6 +580,12 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st) {
   if (p.d == 64) return fwdi::launch<64>(p, st);
   if (p.d == 128) return fwdi::launch<128>(p, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_attn_fwd_infer_mx(const FwdParams& p, cudaStream_t st) {
+  if (p.d == 64) return fwdi::launch<64, true>(p, st);
+  if (p.d == 128) return fwdi::launch<128, true>(p, st);
   return cudaErrorInvalidValue;
 }
 

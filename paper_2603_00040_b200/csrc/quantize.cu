@@ -873,8 +873,22 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
     const int64_t rp = t / (D / 32);
     const int64_t h = rp / n_pad, r = rp % n_pad;
     float v[32];
+    if (x_dt == kBF16 && r < n) {  // 4 x 16-byte loads
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + (h * n + r) * D + b * 32);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = r < n ? load_elem(x, (h * n + r) * D + b * 32 + j, x_dt) : 0.f;
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 w = src[q4];
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[8 * q4 + 2 * e] = __uint_as_float(ww[e] << 16);
+          v[8 * q4 + 2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = r < n ? load_elem(x, (h * n + r) * D + b * 32 + j, x_dt) : 0.f;
+    }
     uint32_t packed[4], sc;
     mx_block(v, packed, sc);
     const int64_t tile = h * (n_pad / TILE) + r / TILE;
