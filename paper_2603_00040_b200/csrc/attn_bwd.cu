@@ -791,6 +791,8 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 // ranks alternate KV tile 0, Q tile T-1, KV tile 1, Q tile T-2, ... Items of
 // one head run together and share its operands in L2 (head-fastest order
 // is 18% slower at C4); KV and Q items share no barriers.
+// MX: the MXFP4 instance (S recomputed on kind::mxf4 block32, P^F in 32-key
+// UE8M0 blocks dequantized exactly to bf16; everything else is shared).
 template <int D, bool MX>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];

@@ -24,8 +24,10 @@
 // K/V stream through an NS-stage ring, S through NB1 (pass 1) / NB2 (pass 2)
 // TMEM buffers, P^F through NP SMEM buffers; every ring counts phases across
 // items.
-// The SAGE instances (sage3.py) add the smoothing score terms and, with TRAIN,
-// two-level P; see the comment above attn_fwd_kernel.
+// Further instances (template flags, see the comments above attn_fwd_kernel):
+// SAGE (sage3.py smoothing terms, two-level P with TRAIN), PLAIN
+// (quantized=False: 16-bit S and P^V on kind::f16) and MX (MXFP4 operands on
+// kind::mxf4 block32, 32-key UE8M0 P blocks).
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
