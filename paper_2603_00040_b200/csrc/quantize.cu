@@ -952,6 +952,67 @@ __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x
   }
 }
 
+// bf16 fast path of mx_cols_tiled_kernel: one CTA (D threads) per 32-token slab,
+// staged through shared memory with 16-byte coalesced loads; thread c
+// quantizes column c.
+template <int D>
+__global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads, int64_t n,
+                                                         uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t, int fqh_bf16) {
+  constexpr int PITCH = D + 8;
+  __shared__ __align__(16) __nv_bfloat16 slab[32][PITCH];
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t nslabs = heads * (n_pad / 32);
+  const int c = threadIdx.x;
+  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
+    const int64_t h = sidx / (n_pad / 32), tok0 = (sidx % (n_pad / 32)) * 32;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32 * D / 8 / D; ++k) {
+      const int i = threadIdx.x + k * D;
+      const int tt = i / (D / 8), cc = (i % (D / 8)) * 8;
+      uint4 w = make_uint4(0u, 0u, 0u, 0u);
+      if (tok0 + tt < n) w = *reinterpret_cast<const uint4*>(x + (h * n + tok0 + tt) * D + cc);
+      *reinterpret_cast<uint4*>(&slab[tt][cc]) = w;
+    }
+    __syncthreads();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(slab[j][c]);
+    uint32_t packed[4], sc;
+    mx_block(v, packed, sc);
+    const int64_t tile = h * (n_pad / TILE) + tok0 / TILE;
+    const int kt = static_cast<int>(tok0 % TILE);
+    *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
+    if (fqh_t) {
+      const float s = __int_as_float(static_cast<int>(sc << 23));
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
+        if (fqh_bf16)
+          *reinterpret_cast<__nv_bfloat16*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2bfloat16_rn(fv);
+        else
+          *reinterpret_cast<__half*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2half_rn(fv);
+      }
+    }
+  }
+}
+
+template <int D>
+static void mx_cols(const void* v, int x_dt, int64_t heads, int64_t n_k, uint8_t* codes, uint8_t* sf, uint8_t* fqh,
+                    int fqh_bf16, cudaStream_t st) {
+  if (x_dt == kBF16 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    int64_t g = heads * (ceil_div(n_k, TILE) * TILE / 32);
+    if (g > 148 * 16) g = 148 * 16;
+    mx_cols_slab_kernel<D><<<static_cast<int>(g), D, 0, st>>>(static_cast<const __nv_bfloat16*>(v), heads, n_k, codes,
+                                                              sf, fqh, fqh_bf16);
+  } else {
+    const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * D);
+    mx_cols_tiled_kernel<D><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, codes, sf, fqh, fqh_bf16);
+  }
+}
+
 cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf, uint8_t* q_h,
                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* k_h, uint8_t* v_codes, uint8_t* v_sf,
@@ -961,11 +1022,11 @@ cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, 
   const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * d);
   // (the V^T codes / scales are a by-product here: the backward reads V^F only)
   if (d == 128) {
-    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1);
+    mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st);
     mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
     mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
   } else if (d == 64) {
-    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1);
+    mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st);
     mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
     mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
   } else {
@@ -984,11 +1045,11 @@ cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v,
   if (d == 128) {
     mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
     mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
-    mx_cols_tiled_kernel<128><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16);
+    mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16, 0, st);
   } else if (d == 64) {
     mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf);
     mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf);
-    mx_cols_tiled_kernel<64><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16);
+    mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, v_h16, 0, st);
   } else {
     return cudaErrorInvalidValue;
   }
