@@ -358,6 +358,15 @@ def _check_cfg(cfg, n_q, n_k, d, quantized, allow_mx=False):
         raise ShapeError("causal attention requires N_q <= N_k")
 
 
+def _check_finite(*xs):
+    """The quantizing reference functions reject non-finite operands
+    (codec.py:313-314 via fake_quantize / quantize in flash.py:195-198, 265-267)."""
+    for x in xs:
+        ok = bool(torch.isfinite(x).all()) if isinstance(x, torch.Tensor) else bool(np.all(np.isfinite(np.asarray(x))))
+        if not ok:
+            raise InvalidValue("quantize requires finite input")
+
+
 def _is_host(x):
     return not isinstance(x, torch.Tensor)
 
@@ -377,6 +386,8 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     from .codec import MXFP4
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
     _check_cfg(cfg, n_q, n_k, d, quantized, allow_mx=True)
+    if quantized:
+        _check_finite(Q, K, V)
     if quantized and cfg.spec == MXFP4:
         q, as_np = to_device(Q)
         k, _ = to_device(K)
@@ -442,6 +453,7 @@ def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
     from .codec import MXFP4
     n_q, n_k, d = _check_attention_shapes(Q, K, V)
     _check_cfg(cfg, n_q, n_k, d, True, allow_mx=True)
+    _check_finite(Q, K, V)
     if cfg.spec == MXFP4:
         q, as_np = to_device(Q)
         k, _ = to_device(K)
@@ -470,6 +482,8 @@ def flash_backward(Q, K, V, dO, outs, cfg, variant=BwdVariant.CORRECT, quantized
         raise ShapeError("outs.L has the wrong shape")
     if variant.uses_o_prime and outs.O_prime is None:
         raise MissingOPrime(f"variant {variant.value} needs O_prime; run the training forward")
+    if quantized:
+        _check_finite(Q, K, V)
     q, as_np = to_device(Q)
     k, _ = to_device(K)
     v, _ = to_device(V)

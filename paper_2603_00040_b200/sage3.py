@@ -82,6 +82,9 @@ def sage3_forward(Q, K, V, cfg, smooth_q=True, smooth_k=True, two_level_p=True, 
     _check_cfg(cfg, n_q, n_k, d, quantized)
     if cfg.b_q <= 0 or n_q % cfg.b_q:
         raise ShapeError(f"b_q ({cfg.b_q}) must divide N_q ({n_q})")  # sage3.py:50-53
+    if quantized:
+        from .flash import _check_finite
+        _check_finite(Q, K, V)
     q, as_np = to_device(Q)
     k, _ = to_device(K)
     v, _ = to_device(V)

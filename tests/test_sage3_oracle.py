@@ -86,3 +86,17 @@ def test_tracking_api():
             tracking.track(np.zeros(50))                    # 400 bytes, released on exit
         assert t.live == 800
     assert t.peak >= 1200
+
+
+def test_reference_api_rejects_non_finite_before_the_gpu():
+    # codec.py:313-314 through fake_quantize / quantize in the flash functions
+    import paper_2603_00040_b200 as aq
+    Q = np.zeros((128, 64))
+    bad = Q.copy()
+    bad[3, 5] = np.nan
+    cfg = aq.TileConfig(b_q=128, b_k=128)
+    for fn in (aq.flash_forward_training, aq.flash_forward_inference):
+        with pytest.raises(aq.InvalidValue):
+            fn(bad, Q, Q, cfg)
+    with pytest.raises(aq.InvalidValue):
+        aq.sage3_forward(Q, Q, np.where(Q == 0, np.inf, Q), cfg)
