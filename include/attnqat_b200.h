@@ -125,9 +125,10 @@ int aq_attn_fwd(const AqFwdArgs* args, void* stream);
 /* flash_forward_inference with cfg.spec = MXFP4 (flash.py:249-314,
  * codec.py:123-203): Q / K / V^T quantized in 32-element blocks with UE8M0
  * scales, P in 32-key blocks, S and PV on tcgen05.mma.kind::mxf4 block32.
- * args->train = 1 also writes O' (args->o_hp; flash.py:176-246). d % 32 == 0
- * (d in {64, 128}). Workspace: aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d,
- * train, 0). */
+ * args->train = 1 also writes O' (args->o_hp; flash.py:176-246); keep_for_bwd = 1
+ * also stages the backward's operands so aq_attn_bwd_mx can take this workspace.
+ * d % 32 == 0 (d in {64, 128}). Workspace: aq_attn_fwd_workspace_bytes(heads,
+ * n_q, n_k, d, train, keep_for_bwd). */
 int aq_attn_fwd_mx(const AqFwdArgs* args, void* stream);
 
 /* quantized=False (flash.py:195-200): plain softmax attention on the same
@@ -197,7 +198,8 @@ int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int
 int aq_attn_bwd(const AqBwdArgs* args, void* stream);
 /* The same for MXFP4 operands (cfg.spec = MXFP4): S recomputed on
  * tcgen05.mma.kind::mxf4 block32, P^F in 32-key UE8M0 blocks, Q^F / K^F / V^F
- * re-quantized from args->q / k / v (args->fwd_workspace is ignored); d % 32 == 0. */
+ * re-quantized from args->q / k / v, or taken from args->fwd_workspace (an
+ * aq_attn_fwd_mx workspace with keep_for_bwd = 1); d % 32 == 0. */
 int aq_attn_bwd_mx(const AqBwdArgs* args, void* stream);
 
 /* ---- measurement utilities (bench.py roofline denominators) ---------------

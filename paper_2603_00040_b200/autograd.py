@@ -18,9 +18,8 @@ from .flash import BwdVariant, attn_backward, attn_forward, attn_forward_mx
 class AttnQATFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, causal=False, variant=BwdVariant.CORRECT, quantized=True, mx=False):
-        if quantized and mx:   # MXFP4 (the backward re-quantizes from q / k / v)
-            o, lse, o_hp = attn_forward_mx(q, k, v, causal=causal, train=True)
-            ws = torch.empty(0, dtype=torch.uint8, device=q.device)
+        if quantized and mx:   # MXFP4: the staged operands are kept for the backward too
+            o, lse, o_hp, ws = attn_forward_mx(q, k, v, causal=causal, train=True, keep_for_bwd=True)
         else:
             o, lse, o_hp, ws = attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True,
                                             quantized=quantized)
@@ -36,7 +35,7 @@ class AttnQATFunction(torch.autograd.Function):
         q, k, v, o, o_hp, lse, ws = ctx.saved_tensors
         dq, dk, dv = attn_backward(q, k, v, d_o.contiguous(), o, o_hp, lse, causal=ctx.causal,
                                    variant=ctx.variant, grad_dtype=q.dtype,
-                                   fwd_workspace=None if ctx.mx else ws, quantized=ctx.quantized, mx=ctx.mx)
+                                   fwd_workspace=ws, quantized=ctx.quantized, mx=ctx.mx)
         return dq, dk, dv, None, None, None, None
 
 

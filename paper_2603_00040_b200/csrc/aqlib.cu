@@ -432,11 +432,15 @@ int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
   if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
   if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, 0);
+  const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, a->keep_for_bwd);
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
   const int d = static_cast<int>(a->d);
-  if (a->train) {  // padded token rows of the V^F tiles must read as zero
-    if (cudaMemsetAsync(ws + w.v_h16, 0, a->heads * ceil_div(a->n_k, TILE) * h_tile_bytes(d), st) != cudaSuccess)
+  if (a->keep_for_bwd) {
+    // the backward's operands too (aq_attn_bwd_mx with this workspace): bf16
+    // Q^F / K^F / V^F tiles next to the codes
+    if (launch_mx_bwd_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
+                               ws + w.q_sf, ws + w.q_hb, ws + w.k_codes, ws + w.k_sf, ws + w.k_hb, ws + w.v_codes,
+                               ws + w.v_sf, ws + w.v_hb, st) != cudaSuccess)
       return AQ_E_CUDA;
   }
   if (launch_mx_attn_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
@@ -573,7 +577,11 @@ static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx) {
   const FwdWs fw = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 1);
   const uint8_t* ops;
   FwdWs w;
-  if (mx) {
+  if (mx && a->fwd_workspace) {
+    if (a->d % 32) return AQ_E_SHAPE;
+    ops = static_cast<const uint8_t*>(a->fwd_workspace);  // aq_attn_fwd_mx with keep_for_bwd = 1
+    w = fw;
+  } else if (mx) {
     // MXFP4 (codec.py:123-203): Q / K codes + UE8M0 images for the S recompute,
     // bf16 Q^F / K^F / V^F tiles for the 16-bit MMAs
     if (a->d % 32) return AQ_E_SHAPE;

@@ -413,7 +413,7 @@ def flash_forward_training(Q, K, V, cfg, quantized=True, instrument=None, thread
     return AttnOutputs(O=o, L=lse, O_prime=o_hp)
 
 
-def attn_forward_mx(q, k, v, causal=False, out_dtype=None, train=False):
+def attn_forward_mx(q, k, v, causal=False, out_dtype=None, train=False, keep_for_bwd=False):
     """MXFP4 forward on CUDA tensors [..., N, d] -> (O, L), or (O, L, O') with
     train=True (flash.py:176-314 with cfg.spec = MXFP4; aq_attn_fwd_mx)."""
     _lib.require_cuda()
@@ -427,7 +427,7 @@ def attn_forward_mx(q, k, v, causal=False, out_dtype=None, train=False):
     heads = q3.shape[0]
     out_dtype = out_dtype or dt
     lib = _lib.load()
-    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, int(train), 0)
+    ws_bytes = lib.aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, int(train), int(keep_for_bwd))
     if ws_bytes <= 0:
         raise InvalidValue(f"unsupported head dim {d} (the B200 kernels take d in {{64, 128}})")
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
@@ -438,13 +438,14 @@ def attn_forward_mx(q, k, v, causal=False, out_dtype=None, train=False):
         q=q3.data_ptr(), k=k3.data_ptr(), v=v3.data_ptr(), in_dtype=_lib.DT_CODE[dt],
         heads=heads, n_q=n_q, n_k=n_k, d=d, causal=int(causal), train=int(train),
         o=o.data_ptr(), o_dtype=_lib.DT_CODE[out_dtype], o_hp=o_hp.data_ptr() if train else None,
-        o_hp_dtype=_lib.DT_CODE[out_dtype], lse=lse.data_ptr(), workspace=ws.data_ptr(), keep_for_bwd=0,
-        operands_staged=0)
+        o_hp_dtype=_lib.DT_CODE[out_dtype], lse=lse.data_ptr(), workspace=ws.data_ptr(),
+        keep_for_bwd=int(keep_for_bwd), operands_staged=0)
     _lib.check(lib.aq_attn_fwd_mx(args, _lib.stream_ptr()))
     lead = q.shape[:-2]
+    outs = (o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q))
     if train:
-        return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q), o_hp.reshape(*lead, n_q, d)
-    return o.reshape(*lead, n_q, d), lse.reshape(*lead, n_q)
+        outs = outs + (o_hp.reshape(*lead, n_q, d),)
+    return outs + (ws,) if keep_for_bwd else outs
 
 
 def flash_forward_inference(Q, K, V, cfg, instrument=None, threads=1):
