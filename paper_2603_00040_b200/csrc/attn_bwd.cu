@@ -417,14 +417,23 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
         for (int b32 = 0; b32 < KPT / 32; ++b32) {
           uint32_t cd[4], sc;
           quantize_p32_mx(pr + 32 * b32, cd, sc);
-          const float sv = __int_as_float(static_cast<int>(sc << 23));
+          // byte-permute lookups of the E2M1 values' bf16 bytes (as for NVFP4
+          // below), then an exact bf16x2 multiply by the power-of-two scale
+          const __nv_bfloat16 sb = __float2bfloat16_rn(__int_as_float(static_cast<int>(sc << 23)));
+          const __nv_bfloat162 s2 = __halves2bfloat162(sb, sb);
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             uint32_t o[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t c0 = (cd[g] >> (8 * e)) & 0xF, c1 = (cd[g] >> (8 * e + 4)) & 0xF;
-              o[e] = pack_bf16(e2m1_to_f32(c0) * sv, e2m1_to_f32(c1) * sv);
+            for (int q4 = 0; q4 < 2; ++q4) {
+              const uint32_t sel = (cd[g] >> (16 * q4)) & 0xFFFFu;
+              const uint32_t lo = __byte_perm(0xC0800000u, 0xC0804000u, sel);
+              const uint32_t hi = __byte_perm(0x3F3F3F00u, 0x40404040u, sel);
+              uint32_t v01 = __byte_perm(lo, hi, 0x5140), v23 = __byte_perm(lo, hi, 0x7362);
+              const __nv_bfloat162 p01 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v01), s2);
+              const __nv_bfloat162 p23 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v23), s2);
+              o[2 * q4] = *reinterpret_cast<const uint32_t*>(&p01);
+              o[2 * q4 + 1] = *reinterpret_cast<const uint32_t*>(&p23);
             }
             *reinterpret_cast<uint4*>(p_h + t8x8_off(row, kb + 32 * b32 + 8 * g)) = make_uint4(o[0], o[1], o[2], o[3]);
           }

@@ -82,10 +82,16 @@ __device__ __forceinline__ void quantize_p32_mx(const float* p, uint32_t (&codes
   const float raw = div_rn(amax, 6.0f, 0.16666667163372039795f);
   sc = 0u;
   if (raw > 0.f) {
-    int e;
-    const float m = frexpf(raw, &e);
-    const int c = ((2.0f * m < 1.5f) ? e - 1 : e) + 127;
-    sc = static_cast<uint32_t>(c < 0 ? 0 : (c > 254 ? 254 : c));
+    const uint32_t bits = __float_as_uint(raw);
+    const uint32_t be = bits >> 23;  // raw <= 1/6 < 2^127: no overflow, no clamp at 254
+    if (be != 0) {
+      sc = be + ((bits & 0x7FFFFFu) >= 0x400000u ? 1u : 0u);  // nearest power of two, ties up
+    } else {  // subnormal raw (codec.py:123-136 through frexp)
+      int e;
+      const float m = frexpf(raw, &e);
+      const int c = ((2.0f * m < 1.5f) ? e - 1 : e) + 127;
+      sc = static_cast<uint32_t>(c < 0 ? 0 : c);
+    }
   }
   const float rs = __int_as_float(static_cast<int>((254u - sc) << 23));
   float q[32];

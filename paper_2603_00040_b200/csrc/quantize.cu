@@ -986,14 +986,23 @@ __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
     if (fqh_t) {
+      // dequantized values back into the slab (16-bit, same element width),
+      // then 16-byte T8x8 stores of 8 columns per token
       const float s = __int_as_float(static_cast<int>(sc << 23));
+      __syncthreads();  // every column has read its tokens
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
-        if (fqh_bf16)
-          *reinterpret_cast<__nv_bfloat16*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2bfloat16_rn(fv);
-        else
-          *reinterpret_cast<__half*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + j, c)) = __float2half_rn(fv);
+        if (fqh_bf16) slab[j][c] = __float2bfloat16_rn(fv);
+        else *reinterpret_cast<__half*>(&slab[j][c]) = __float2half_rn(fv);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 32 * D / 8 / D; ++k) {
+        const int i = threadIdx.x + k * D;
+        const int tt = i % 32, c8 = (i / 32) * 8;
+        *reinterpret_cast<uint4*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + tt, c8)) =
+            *reinterpret_cast<const uint4*>(&slab[tt][c8]);
       }
     }
   }
