@@ -436,17 +436,20 @@ int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
   const int d = static_cast<int>(a->d);
   if (a->keep_for_bwd) {
-    // the backward's operands too (aq_attn_bwd_mx with this workspace): bf16
-    // Q^F / K^F / V^F tiles next to the codes
+    // the backward's operands too (aq_attn_bwd_mx with this workspace): the
+    // codes plus bf16 Q^F / K^F / V^F tiles, then the fp16 V^F tiles of O'
     if (launch_mx_bwd_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
                                ws + w.q_sf, ws + w.q_hb, ws + w.k_codes, ws + w.k_sf, ws + w.k_hb, ws + w.v_codes,
                                ws + w.v_sf, ws + w.v_hb, st) != cudaSuccess)
       return AQ_E_CUDA;
-  }
-  if (launch_mx_attn_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
-                              ws + w.q_sf, ws + w.k_codes, ws + w.k_sf, ws + w.v_codes, ws + w.v_sf,
-                              a->train ? ws + w.v_h16 : nullptr, st) != cudaSuccess)
+    if (a->train && launch_mx_v_tiles(a->v, a->in_dtype, a->heads, a->n_k, d, ws + w.v_codes, ws + w.v_sf,
+                                      ws + w.v_h16, 0, st) != cudaSuccess)
+      return AQ_E_CUDA;
+  } else if (launch_mx_attn_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
+                                     ws + w.q_sf, ws + w.k_codes, ws + w.k_sf, ws + w.v_codes, ws + w.v_sf,
+                                     a->train ? ws + w.v_h16 : nullptr, st) != cudaSuccess) {
     return AQ_E_CUDA;
+  }
   FwdParams p{};
   p.q_codes = ws + w.q_codes;
   p.q_sf = ws + w.q_sf;

@@ -1022,6 +1022,14 @@ static void mx_cols(const void* v, int x_dt, int64_t heads, int64_t n_k, uint8_t
   }
 }
 
+cudaError_t launch_mx_v_tiles(const void* v, int x_dt, int64_t heads, int64_t n_k, int d, uint8_t* v_codes,
+                              uint8_t* v_sf, uint8_t* fqh, int fqh_bf16, cudaStream_t st) {
+  if (d == 128) mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, fqh, fqh_bf16, st);
+  else if (d == 64) mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, fqh, fqh_bf16, st);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf, uint8_t* q_h,
                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* k_h, uint8_t* v_codes, uint8_t* v_sf,
