@@ -440,10 +440,7 @@ int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
     // codes plus bf16 Q^F / K^F / V^F tiles, then the fp16 V^F tiles of O'
     if (launch_mx_bwd_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
                                ws + w.q_sf, ws + w.q_hb, ws + w.k_codes, ws + w.k_sf, ws + w.k_hb, ws + w.v_codes,
-                               ws + w.v_sf, ws + w.v_hb, st) != cudaSuccess)
-      return AQ_E_CUDA;
-    if (a->train && launch_mx_v_tiles(a->v, a->in_dtype, a->heads, a->n_k, d, ws + w.v_codes, ws + w.v_sf,
-                                      ws + w.v_h16, 0, st) != cudaSuccess)
+                               ws + w.v_sf, ws + w.v_hb, st, a->train ? ws + w.v_h16 : nullptr) != cudaSuccess)
       return AQ_E_CUDA;
   } else if (launch_mx_attn_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, d, ws + w.q_codes,
                                      ws + w.q_sf, ws + w.k_codes, ws + w.k_sf, ws + w.v_codes, ws + w.v_sf,

@@ -93,14 +93,12 @@ cudaError_t launch_attn_fwd_plain(const FwdParams& p, cudaStream_t st);
 // MXFP4 inference forward on K4 (kind::mxf4 block32; the attention tiles from
 // launch_mx_attn_operands, P quantized in 32-key UE8M0 blocks)
 cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st);
-cudaError_t launch_mx_v_tiles(const void* v, int x_dt, int64_t heads, int64_t n_k, int d, uint8_t* v_codes,
-                              uint8_t* v_sf, uint8_t* fqh, int fqh_bf16, cudaStream_t st);
 // MXFP4 backward operands: Q / K codes + SF tiles with bf16 Q^F / K^F T8x8
 // tiles, V^F bf16 T8x8 tiles
 cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf, uint8_t* q_h,
                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* k_h, uint8_t* v_codes, uint8_t* v_sf,
-                                   uint8_t* v_h, cudaStream_t st);
+                                   uint8_t* v_h, cudaStream_t st, uint8_t* v_h16 = nullptr);
 cudaError_t launch_mx_attn_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                     int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf,
                                     uint8_t* k_codes, uint8_t* k_sf, uint8_t* v_codes, uint8_t* v_sf,

@@ -957,7 +957,8 @@ __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x
 // quantizes column c.
 template <int D>
 __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads, int64_t n,
-                                                         uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t, int fqh_bf16) {
+                                                         uint8_t* codes_t, uint8_t* sf_t, uint8_t* fqh_t, int fqh_bf16,
+                                                         uint8_t* fqh2_t = nullptr) {
   constexpr int PITCH = D + 8;
   __shared__ __align__(16) __nv_bfloat16 slab[32][PITCH];
   const int64_t n_pad = ceil_div(n, TILE) * TILE;
@@ -985,15 +986,19 @@ __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
-    if (fqh_t) {
-      // dequantized values back into the slab (16-bit, same element width),
-      // then 16-byte T8x8 stores of 8 columns per token
+    // dequantized values back into the slab (16-bit, same element width),
+    // then 16-byte T8x8 stores of 8 columns per token; fqh2_t gets the fp16
+    // copy when fqh_t takes bf16 (training + backward in one pass)
+    for (int pass = 0; pass < 2; ++pass) {
+      uint8_t* dst = pass == 0 ? fqh_t : fqh2_t;
+      if (!dst) continue;
+      const bool bf = pass == 0 && fqh_bf16;
       const float s = __int_as_float(static_cast<int>(sc << 23));
-      __syncthreads();  // every column has read its tokens
+      __syncthreads();  // every column has read its tokens / the previous copy is stored
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
-        if (fqh_bf16) slab[j][c] = __float2bfloat16_rn(fv);
+        if (bf) slab[j][c] = __float2bfloat16_rn(fv);
         else *reinterpret_cast<__half*>(&slab[j][c]) = __float2half_rn(fv);
       }
       __syncthreads();
@@ -1001,7 +1006,7 @@ __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __
       for (int k = 0; k < 32 * D / 8 / D; ++k) {
         const int i = threadIdx.x + k * D;
         const int tt = i % 32, c8 = (i / 32) * 8;
-        *reinterpret_cast<uint4*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(kt + tt, c8)) =
+        *reinterpret_cast<uint4*>(dst + tile * h_tile_bytes(D) + t8x8_off(kt + tt, c8)) =
             *reinterpret_cast<const uint4*>(&slab[tt][c8]);
       }
     }
@@ -1010,40 +1015,33 @@ __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __
 
 template <int D>
 static void mx_cols(const void* v, int x_dt, int64_t heads, int64_t n_k, uint8_t* codes, uint8_t* sf, uint8_t* fqh,
-                    int fqh_bf16, cudaStream_t st) {
+                    int fqh_bf16, cudaStream_t st, uint8_t* fqh2_f16 = nullptr) {
   if (x_dt == kBF16 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
     int64_t g = heads * (ceil_div(n_k, TILE) * TILE / 32);
     if (g > 148 * 16) g = 148 * 16;
     mx_cols_slab_kernel<D><<<static_cast<int>(g), D, 0, st>>>(static_cast<const __nv_bfloat16*>(v), heads, n_k, codes,
-                                                              sf, fqh, fqh_bf16);
+                                                              sf, fqh, fqh_bf16, fqh2_f16);
   } else {
     const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * D);
     mx_cols_tiled_kernel<D><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, codes, sf, fqh, fqh_bf16);
+    if (fqh2_f16) mx_cols_tiled_kernel<D><<<gv, 256, 0, st>>>(v, x_dt, heads, n_k, codes, sf, fqh2_f16, 0);
   }
-}
-
-cudaError_t launch_mx_v_tiles(const void* v, int x_dt, int64_t heads, int64_t n_k, int d, uint8_t* v_codes,
-                              uint8_t* v_sf, uint8_t* fqh, int fqh_bf16, cudaStream_t st) {
-  if (d == 128) mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, fqh, fqh_bf16, st);
-  else if (d == 64) mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, fqh, fqh_bf16, st);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
 }
 
 cudaError_t launch_mx_bwd_operands(const void* q, const void* k, const void* v, int x_dt, int64_t heads,
                                    int64_t n_q, int64_t n_k, int d, uint8_t* q_codes, uint8_t* q_sf, uint8_t* q_h,
                                    uint8_t* k_codes, uint8_t* k_sf, uint8_t* k_h, uint8_t* v_codes, uint8_t* v_sf,
-                                   uint8_t* v_h, cudaStream_t st) {
+                                   uint8_t* v_h, cudaStream_t st, uint8_t* v_h16) {
   const int gq = grid_for(heads * ceil_div(n_q, TILE) * TILE * (d / 32));
   const int gk = grid_for(heads * ceil_div(n_k, TILE) * TILE * (d / 32));
   const int gv = grid_for(heads * ceil_div(n_k, TILE) * 4 * d);
   // (the V^T codes / scales are a by-product here: the backward reads V^F only)
   if (d == 128) {
-    mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st);
+    mx_cols<128>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st, v_h16);
     mx_rows_tiled_kernel<128><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
     mx_rows_tiled_kernel<128><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
   } else if (d == 64) {
-    mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st);
+    mx_cols<64>(v, x_dt, heads, n_k, v_codes, v_sf, v_h, 1, st, v_h16);
     mx_rows_tiled_kernel<64><<<gq, 256, 0, st>>>(q, x_dt, heads, n_q, q_codes, q_sf, q_h);
     mx_rows_tiled_kernel<64><<<gk, 256, 0, st>>>(k, x_dt, heads, n_k, k_codes, k_sf, k_h);
   } else {
