@@ -27,6 +27,8 @@ for n, d, causal in ((200, 64, True), (77, 128, False)):
     aq.attn_forward_mx(q, k, v, causal=causal)
     o, lse, o_hp = aq.attn_forward_mx(q, k, v, causal=causal, train=True)
     aq.attn_backward(q, k, v, torch.randn_like(q), o, o_hp, lse, causal=causal, mx=True)
+    qg, kg, vg = (t.clone().requires_grad_() for t in (q, k, v))
+    aq.attn_qat(qg, kg, vg, causal=causal, spec=aq.MXFP4).backward(torch.randn_like(q))
     aq.fp4mm(aq.quantize(q[0, 0].float(), aq.MXFP4), aq.quantize(k[0, 0].float(), aq.MXFP4))
 x = torch.randn(37, 48, generator=g, device="cuda")
 aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))
