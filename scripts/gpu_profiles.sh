@@ -22,4 +22,6 @@ ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel 
     python scripts/prof_sage3.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel -s 1 -c 1 -o gpurun_out/prof/attn_fwd_plain_c2 \
     python scripts/prof_plain.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:attn_fwd_infer -c 1 -o gpurun_out/prof/attn_fwd_mx_c2 \
+    python scripts/prof_mx.py > /dev/null 2>&1
 ls -la gpurun_out/prof

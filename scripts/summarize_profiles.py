@@ -67,7 +67,7 @@ if os.path.exists(os.path.join(SRC, "launches_sage3_c2.csv")):
                 fh.write(f"{t:12.1f} us  {k[:110]}\n")
 
 for rep in ("attn_fwd_c2", "attn_fwd_train_c4", "attn_bwd_c4", "quantize_c2", "fp4mm_8k", "attn_fwd_sage3_c2",
-            "attn_fwd_plain_c2"):
+            "attn_fwd_plain_c2", "attn_fwd_mx_c2"):
     path = os.path.join(SRC, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
