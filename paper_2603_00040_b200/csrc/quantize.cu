@@ -896,18 +896,28 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, 32 * b, TILE)) =
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * sf_tile_bytes_qk(D) + sf512_off(rr, b)] = static_cast<uint8_t>(sc);
-    if (fqh_t) {  // the bf16 fake-quantized operand tile of the backward (T8x8)
-      const float s = __int_as_float(static_cast<int>(sc << 23));
+    if (fqh_t) {  // the bf16 fake-quantized operand tile of the backward (T8x8):
+      // byte-permute lookups of the E2M1 magnitudes' bf16 bytes, the sign bit
+      // from the code, then one exact bf16x2 multiply by the power-of-two scale
+      const __nv_bfloat16 sb = __float2bfloat16_rn(__int_as_float(static_cast<int>(sc << 23)));
+      const __nv_bfloat162 s2 = __halves2bfloat162(sb, sb);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         uint32_t w[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j0 = 8 * g + 2 * e;
-          const float a = e2m1_to_f32((packed[j0 >> 3] >> (4 * (j0 & 7))) & 0xF) * s;
-          const float c2 = e2m1_to_f32((packed[(j0 + 1) >> 3] >> (4 * ((j0 + 1) & 7))) & 0xF) * s;
-          const __nv_bfloat162 bv = __floats2bfloat162_rn(a, c2);
-          w[e] = *reinterpret_cast<const uint32_t*>(&bv);
+        for (int q4 = 0; q4 < 2; ++q4) {
+          const uint32_t cw = (packed[g] >> (16 * q4)) & 0xFFFFu;   // 4 codes
+          const uint32_t sel = cw & 0x7777u;                          // magnitudes
+          const uint32_t lo = __byte_perm(0xC0800000u, 0xC0804000u, sel);
+          const uint32_t hi = __byte_perm(0x3F3F3F00u, 0x40404040u, sel);
+          uint32_t v01 = __byte_perm(lo, hi, 0x5140), v23 = __byte_perm(lo, hi, 0x7362);
+          // signs: code bit 3 of each nibble -> bit 15 of each bf16 half
+          v01 |= ((cw & 0x8u) << 12) | ((cw & 0x80u) << 24);
+          v23 |= ((cw & 0x800u) << 4) | ((cw & 0x8000u) << 16);
+          const __nv_bfloat162 p01 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v01), s2);
+          const __nv_bfloat162 p23 = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&v23), s2);
+          w[2 * q4] = *reinterpret_cast<const uint32_t*>(&p01);
+          w[2 * q4 + 1] = *reinterpret_cast<const uint32_t*>(&p23);
         }
         *reinterpret_cast<uint4*>(fqh_t + tile * h_tile_bytes(D) + t8x8_off(rr, 32 * b + 8 * g)) =
             make_uint4(w[0], w[1], w[2], w[3]);
