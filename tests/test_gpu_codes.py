@@ -63,3 +63,21 @@ def test_quantize_dequantize_block():
         np.testing.assert_array_equal(aq.dequantize_block(blk), orc.dequantize(codes, scales, 16, np.float64)[0])
     with pytest.raises(aq.ShapeError):
         aq.quantize_block(np.zeros(8))
+
+
+@pytest.mark.parametrize("n,d", [(256, 128), (384, 64)])
+def test_staged_tiles_identical_across_input_paths(n, d):
+    # the bf16 fast paths of the tile quantizers (K1 / K2) and the general
+    # kernels (taken for fp32 / fp16 inputs) write the same bytes for the same values
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    q, k, v = (torch.randn(2, n, d, generator=g, device="cuda").bfloat16() for _ in range(3))
+    outs = []
+    from paper_2603_00040_b200 import _lib
+    nbytes = _lib.load().aq_attn_fwd_workspace_bytes(2, n, n, d, 0, 0)
+    for dt in (torch.bfloat16, torch.float32, torch.float16):
+        # zeroed: bytes no MMA reads (e.g. scale rows past d of a V^T image) stay equal
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        aq.attn_forward(q.to(dt), k.to(dt), v.to(dt), causal=True, train=False, workspace=ws)
+        outs.append(ws)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
