@@ -13,6 +13,7 @@
 // hardware cvt.rn.satfinite.{e4m3x2,e2m1x2}.f32 converts, and no FTZ (this
 // file is compiled without --use_fast_math).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "attn.h"
@@ -638,6 +639,44 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// K2 inference fast path (bf16, no 16-bit tiles): one CTA of D threads per
+// 32-token slab staged through shared memory with 16-byte loads; thread c
+// quantizes column c's two 16-token blocks and writes 16 code bytes + 2 scales.
+template <int D>
+__global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads,
+                                                               int64_t n, uint8_t* __restrict__ codes_t,
+                                                               uint8_t* __restrict__ sf_t) {
+  constexpr int PITCH = D + 8;
+  __shared__ __align__(16) __nv_bfloat16 slab[32][PITCH];
+  const int64_t nslabs = heads * (n / 32);
+  const int c = threadIdx.x;
+  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
+    const int64_t tok0 = sidx * 32;  // flat token index (n % 128 == 0: slabs never straddle heads)
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = threadIdx.x + k * D;
+      const int tt = i / (D / 8), cc = (i % (D / 8)) * 8;
+      *reinterpret_cast<uint4*>(&slab[tt][cc]) = *reinterpret_cast<const uint4*>(x + (tok0 + tt) * D + cc);
+    }
+    __syncthreads();
+    Block16 q[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __bfloat162float(slab[16 * b + j][c]);
+      quantize_block16<false, false>(v, q[b]);
+    }
+    const int64_t tile = tok0 / TILE;
+    const int kt = static_cast<int>(tok0 % TILE);
+    *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
+        make_uint4(q[0].packed[0], q[0].packed[1], q[1].packed[0], q[1].packed[1]);
+    *reinterpret_cast<uint16_t*>(sf_t + tile * kSfTileBytesV + sf512_off(c, kt / 16)) =
+        static_cast<uint16_t>(q[0].scale | (q[1].scale << 8));
+  }
+}
+
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
   const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
                     !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
@@ -650,6 +689,15 @@ cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
     auto* h1 = static_cast<uint8_t*>(a.fqh_t);
     auto* h2 = static_cast<uint8_t*>(a.fqh2_t);
     const int gg = static_cast<int>(g);
+    if (!fqh) {
+      int64_t gs = a.heads * (a.n / 32);
+      if (gs > 148 * 16) gs = 148 * 16;
+      if (a.cols == 128)
+        quantize_cols_slab_kernel<128><<<static_cast<int>(gs), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+      else
+        quantize_cols_slab_kernel<64><<<static_cast<int>(gs), 64, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+      return cudaGetLastError();
+    }
     if (a.cols == 128) {
       if (fqh) quantize_cols_tiled_kernel<128, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt);
       else quantize_cols_tiled_kernel<128, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0);
