@@ -897,7 +897,8 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 // Tuning-aid environment switches (read once): AQ_FWD_CS = 2 | 4 column
 // splits of the training forward (default 2: 8 softmax warps, 64 key columns
 // per thread);
-// AQ_FWD_DEBUG bit 32 = per-segment cycle counters (aq_debug_fwd_profile).
+// AQ_FWD_DEBUG bit 32 = per-segment cycle counters (aq_debug_fwd_profile),
+// bit 64 = no exact pass-2 early-out in the inference kernel (A/B timing).
 static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;

@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     const float sl2 = p.scale_log2;
     float x[CW];
     int su = 0, pc = 0, k = 0;
+    int chk_wait = 0, chk_pen = 0;  // early-out back-off (warp-uniform)
+    const bool early_out = (p.debug & 64) == 0;  // AQ_FWD_DEBUG bit 64 disables it (A/B timing)
     float* ml = reinterpret_cast<float*>(smem + C::ML);
     float* lb = reinterpret_cast<float*>(smem + C::LB);
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
         const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
         mbar_arrive(&bars[C::B_L_EMPTY + qs]);
+        const float thr = p_skip_thr(L2, sl2);
         for (int jj = 0; jj < nt; ++jj) {
           mbar_wait(&bars[C::B_SB_FULL], su & 1);
           ++su;
@@ -496,7 +499,43 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
                 make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
             scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
           };
-          if (lim >= CW - 1) {
+          // exact early-out (pquant.cuh): 16-key blocks whose P is below 2^-11 in
+          // every row of the warp get P^F = 0 with scale 0x01 without an exponential.
+          // Checked with exponential back-off, so workloads where blocks rarely
+          // qualify (short rows) pay for one check every ~16 tiles.
+          uint32_t sk = 0;
+          if constexpr (!MX) {
+            if (early_out && chk_wait == 0) {  // warp-uniform; lanes with masked keys vote 0
+              sk = __reduce_and_sync(0xffffffffu, lim >= CW - 1 ? p_skip_mask<CW / 16>(x, thr) : 0u);
+              if (sk == 0) {
+                chk_pen = min(2 * chk_pen + 1, 15);
+                chk_wait = chk_pen;
+              } else {
+                chk_pen = 0;
+              }
+            } else if (chk_wait > 0) {
+              --chk_wait;
+            }
+          }
+          if (sk != 0) {
+#pragma unroll
+            for (int blk = 0; blk < CW / 16; blk += 2) {
+              PBlock qa, qb;
+              qa.scale = qb.scale = 1u;
+              qa.codes[0] = qa.codes[1] = qb.codes[0] = qb.codes[1] = 0u;
+              if (!((sk >> blk) & 1u)) {
+                p_from_s<8>(x + blk * 16, cbase + blk * 16, sl2, L2);
+                qa = quantize_p16(x + blk * 16);
+              }
+              if (!((sk >> (blk + 1)) & 1u)) {
+                p_from_s<8>(x + blk * 16 + 16, cbase + blk * 16 + 16, sl2, L2);
+                qb = quantize_p16(x + blk * 16 + 16);
+              }
+              *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
+                  make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
+              scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+            }
+          } else if (lim >= CW - 1) {
 #pragma unroll
             for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, false);
           } else {

@@ -120,6 +120,35 @@ __device__ __forceinline__ void p_from_s(float* x, int c0, float sl2, float L2) 
   }
 }
 
+// Exact pass-2 early-out. A 16-key block whose scores all satisfy
+// S * sl2 - L2 <= -11.01 has P = exp2(S * sl2 - L2) <= 2^-11 for every key, for
+// MUFU.EX2 and for the FMA-pipe polynomial alike (relative error <= 2.2e-7, so
+// the 0.01 margin keeps P strictly below 2^-11). quantize_p16 then yields the
+// bumped scale code 0x01 (amax / 6 < 2^-10 rounds to E4M3 zero, amax > 0 since
+// every 16-key block holds one polynomial pair, which never returns 0) and
+// P / 2^-9 <= 0.25 rounds to the even code 0 everywhere: the block's P^F is
+// known without an exponential (codec.py:169-177, 196-202).
+// p_skip_thr gives the per-row bound on the raw score, p_skip_mask bit b marks
+// block b of this thread's columns as qualifying.
+static_assert(AQ_POLY_PAIRS_OF_8 >= 1, "the early-out relies on one polynomial pair per 16-key block");
+__device__ __forceinline__ float p_skip_thr(float L2, float sl2) {
+  return (L2 - 11.02f - fabsf(L2) * 1e-6f) / sl2;
+}
+template <int NB>
+__device__ __forceinline__ uint32_t p_skip_mask(const float* x, float thr) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const float* v = x + 16 * b;
+    const float m0 = fmaxf(fmaxf(v[0], v[1]), v[2]), m1 = fmaxf(fmaxf(v[3], v[4]), v[5]);
+    const float m2 = fmaxf(fmaxf(v[6], v[7]), v[8]), m3 = fmaxf(fmaxf(v[9], v[10]), v[11]);
+    const float m4 = fmaxf(fmaxf(v[12], v[13]), v[14]);
+    const float mx = fmaxf(fmaxf(fmaxf(m0, m1), m2), fmaxf(fmaxf(m3, m4), v[15]));
+    m |= (mx <= thr ? 1u : 0u) << b;
+  }
+  return m;
+}
+
 // decoded value of code e (0..15) of a quantized block
 __device__ __forceinline__ float pblock_value(const PBlock& b, int e) {
   return e2m1_to_f32((b.codes[e >> 3] >> (4 * (e & 7))) & 0xF) * b.sv;
