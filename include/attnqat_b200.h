@@ -8,6 +8,11 @@
  * workspaces sized by the *_workspace_bytes queries) and returns an AqStatus.
  *
  * dtype codes: 0 = float32, 1 = bfloat16, 2 = float16.
+ *
+ * ABI version 3 (aq_abi_version): per-tensor FP32 scales (two-level NVFP4),
+ * softmax scale, device non-finite flag and the P^F instrument dump. A scale
+ * argument of 0 means 1.0, i.e. the reference's single-level semantics
+ * (SPEC.md:129), which every kernel reproduces bit for bit.
  * Tensors are [heads][n][d] contiguous per head (head stride / row stride
  * given explicitly where noted). `heads` is the flattened batch*heads count.
  */
@@ -50,18 +55,20 @@ const char* aq_status_string(int status);
  * layout: codes [heads*n][cols/2] (low nibble = lower index), scales
  * [heads*n][cols/16] E4M3 codes; fq (optional) = dequantized values in
  * fq_dtype. nonfinite (optional, device int) is OR-ed with 1 when an input
- * is NaN/Inf (the reference raises InvalidValue, codec.py:313-314). */
+ * is NaN/Inf (the reference raises InvalidValue, codec.py:313-314).
+ * tensor_scale t (north_star's per-tensor FP32 scale; 0 or 1 = reference):
+ * blocks of x / t are quantized, so x ~ t * scale * code; fq includes t. */
 int aq_quantize_rows(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld,
-                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite,
-                     void* stream);
+                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, float tensor_scale,
+                     int* nonfinite, void* stream);
 
 /* Replaces quantize_padded(V.T) / fake_quantize_cols (codec.py:359-381):
  * blocks of 16 along the token axis of x [heads][n][cols]; the token tail is
  * zero-padded to n16 = ceil(n/16)*16. codes [heads][cols][n16/2], scales
  * [heads][cols][n16/16]; fq (optional) [heads][n][cols]. */
 int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld,
-                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite,
-                     void* stream);
+                     int64_t hs, uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, float tensor_scale,
+                     int* nonfinite, void* stream);
 
 /* Replaces attnqat.codec.round_to_fp4 (format 0, codec.py:76-88) and
  * round_to_e4m3 (format 1, codec.py:101-112): one code per element of x
@@ -81,9 +88,10 @@ int aq_dequantize_mx(const uint8_t* codes, const uint8_t* scales, int64_t rows, 
  * non-finite or non-positive input. */
 int aq_e8m0_codes(const void* x, int x_dtype, int64_t n, uint8_t* codes, int* invalid, void* stream);
 
-/* Replaces attnqat.codec.dequantize (codec.py:327-333). rows x cols. */
+/* Replaces attnqat.codec.dequantize (codec.py:327-333). rows x cols; values
+ * code * scale * tensor_scale (0 or 1 = reference). */
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
-                  int out_dtype, void* stream);
+                  int out_dtype, float tensor_scale, void* stream);
 
 /* Replaces attnqat.tensors.fp4mm (tensors.py:54-86): C = A B^T from two NVFP4
  * QuantTensors blocked along the shared contraction axis K (K % 16 == 0):
@@ -115,6 +123,19 @@ typedef struct {
   int keep_for_bwd;  /* also stage the bf16 operands the backward reuses */
   int operands_staged; /* 1: workspace already holds this Q/K/V's quantized tiles
                           (e.g. an FP4 KV cache); skip the quantizers */
+  /* --- ABI 3 --- */
+  float softmax_scale; /* 0: 1/sqrt(d) (flash.py:207) */
+  float q_scale, k_scale, v_scale; /* per-tensor FP32 scales t_q, t_k, t_v (0 or 1 = reference):
+                          S = t_q t_k Q^F K^F^T, O = t_v (P^F V^F) */
+  float p_scale;       /* t_p: P quantized as two-level NVFP4 P^F = t_p s code with the 16-key
+                          block scales over P / t_p. 0 or 1 = the reference (single level,
+                          2^-9 scale floor); e.g. 1/2688 keeps long-row P above the floor.
+                          Not parity for t_p != 1 (the reference has no tensor scale). */
+  int* nonfinite;      /* optional device int, OR-ed with 1 when Q / K / V hold NaN / Inf
+                          (codec.py:313-314); the caller reads it and raises InvalidValue */
+  uint8_t* pf_codes;   /* optional instrument dump (flash.py:117-124, PTileRecord): P^F of every
+                          row as quantize_padded(P) would store it, codes [heads][n_q][n16/2] */
+  uint8_t* pf_scales;  /* and scales [heads][n_q][n16/16], n16 = ceil(n_k/16)*16; both or neither */
 } AqFwdArgs;
 
 int64_t aq_attn_fwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train,
@@ -191,6 +212,13 @@ typedef struct {
   int g_dtype;
   void* workspace;   /* aq_attn_bwd_workspace_bytes() */
   const void* fwd_workspace; /* forward workspace with keep_for_bwd=1, or NULL to re-quantize */
+  /* --- ABI 3: as AqFwdArgs (the forward's values) --- */
+  float softmax_scale;
+  float q_scale, k_scale, v_scale, p_scale;
+  int* nonfinite;
+  uint8_t* pf_codes;   /* optional instrument dump of the recomputed P^F (flash.py:386-387; CORRECT /
+                          LOW_PREC_O only), layout as AqFwdArgs::pf_codes */
+  uint8_t* pf_scales;
 } AqBwdArgs;
 
 int64_t aq_attn_bwd_workspace_bytes(int64_t heads, int64_t n_q, int64_t n_k, int64_t d);

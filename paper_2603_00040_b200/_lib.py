@@ -20,6 +20,7 @@ DT_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
+c_f = ctypes.c_float
 c_vp = ctypes.c_void_p
 
 
@@ -30,6 +31,9 @@ class AqFwdArgs(ctypes.Structure):
         ("causal", c_int), ("train", c_int),
         ("o", c_vp), ("o_dtype", c_int), ("o_hp", c_vp), ("o_hp_dtype", c_int),
         ("lse", c_vp), ("workspace", c_vp), ("keep_for_bwd", c_int), ("operands_staged", c_int),
+        # ABI 3
+        ("softmax_scale", c_f), ("q_scale", c_f), ("k_scale", c_f), ("v_scale", c_f), ("p_scale", c_f),
+        ("nonfinite", c_vp), ("pf_codes", c_vp), ("pf_scales", c_vp),
     ]
 
 
@@ -53,6 +57,9 @@ class AqBwdArgs(ctypes.Structure):
         ("causal", c_int), ("variant", c_int),
         ("dq", c_vp), ("dk", c_vp), ("dv", c_vp), ("g_dtype", c_int),
         ("workspace", c_vp), ("fwd_workspace", c_vp),
+        # ABI 3
+        ("softmax_scale", c_f), ("q_scale", c_f), ("k_scale", c_f), ("v_scale", c_f), ("p_scale", c_f),
+        ("nonfinite", c_vp), ("pf_codes", c_vp), ("pf_scales", c_vp),
     ]
 
 
@@ -61,10 +68,10 @@ PROTOTYPES = {
     "aq_abi_version": (c_int, []),
     "aq_status_string": (ctypes.c_char_p, [c_int]),
     "aq_quantize_rows": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64,
-                                 c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
+                                 c_vp, c_vp, c_vp, c_int, c_f, c_vp, c_vp]),
     "aq_quantize_cols": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64,
-                                 c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
-    "aq_dequantize": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_vp]),
+                                 c_vp, c_vp, c_vp, c_int, c_f, c_vp, c_vp]),
+    "aq_dequantize": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_f, c_vp]),
     "aq_fp4mm_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64]),
     "aq_fp4mm": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "aq_fp4mm_mx": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),

@@ -58,20 +58,47 @@ class QuantTensor:
     spec: BlockSpec
     codes: object
     scales: object
+    # per-tensor FP32 scale of the two-level NVFP4 format (north_star): the
+    # value is tensor_scale * scale * code. 1.0 is the reference's format
+    # -- a QuantTensor from quantize() without the argument.
+    tensor_scale: float = 1.0
 
     @property
     def block_grid(self):
         return (self.rows, self.cols // self.spec.block_size)
 
     def row_slice(self, start, stop):
-        return QuantTensor(stop - start, self.cols, self.spec, self.codes[start:stop], self.scales[start:stop])
+        return QuantTensor(stop - start, self.cols, self.spec, self.codes[start:stop], self.scales[start:stop],
+                           self.tensor_scale)
 
     def col_slice(self, start, stop):
         bs = self.spec.block_size
         if start % bs or stop % bs:
             raise ShapeError("column slices must align to block boundaries")
         return QuantTensor(self.rows, stop - start, self.spec, self.codes[:, start // 2:stop // 2],
-                           self.scales[:, start // bs:stop // bs])
+                           self.scales[:, start // bs:stop // bs], self.tensor_scale)
+
+
+def auto_tensor_scale(x):
+    """The usual NVFP4 per-tensor scale amax(|x|) / (448 * 6): the largest block
+    scale lands on E4M3's maximum (one device reduction, read back to the host)."""
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+    amax = float(t.detach().abs().amax()) if t.numel() else 0.0
+    return amax / (E4M3_MAX * FP4_MAX) if amax > 0 and np.isfinite(amax) else 1.0
+
+
+def _ts(tensor_scale, x):
+    """Resolve a tensor_scale argument: None / 1.0 (reference), 'auto', or a positive float."""
+    if tensor_scale is None:
+        return 1.0
+    if isinstance(tensor_scale, str):
+        if tensor_scale != "auto":
+            raise InvalidValue(f"tensor_scale must be a positive float or 'auto', got {tensor_scale!r}")
+        return auto_tensor_scale(x)
+    ts = float(tensor_scale)
+    if not (ts > 0 and np.isfinite(ts)):
+        raise InvalidValue(f"tensor_scale must be positive and finite, got {tensor_scale}")
+    return ts
 
 
 def to_device(x, allow_f64=True):
@@ -109,8 +136,10 @@ def _quantize_mx(t, codes=None, scales=None, fq=None):
     _nonfinite_check(flag)
 
 
-def quantize(x, spec=NVFP4) -> QuantTensor:
-    """Block-row-wise NVFP4 / MXFP4 quantization (codec.py:302-324)."""
+def quantize(x, spec=NVFP4, tensor_scale=None) -> QuantTensor:
+    """Block-row-wise NVFP4 / MXFP4 quantization (codec.py:302-324).
+    ``tensor_scale`` (NVFP4 only; None = the reference's format) selects the
+    two-level format: blocks of x / tensor_scale are quantized."""
     if spec == MXFP4:
         t, was_np = to_device(x)
         if t.dim() != 2:
@@ -131,14 +160,15 @@ def quantize(x, spec=NVFP4) -> QuantTensor:
     if cols % spec.block_size:
         raise ShapeError(f"cols ({cols}) must be a multiple of block_size ({spec.block_size});"
                          " padding is the caller's responsibility")
+    ts = _ts(tensor_scale, t)
     codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=t.device)
     scales = torch.empty((rows, cols // 16), dtype=torch.uint8, device=t.device)
     flag = torch.zeros(1, dtype=torch.int32, device=t.device)
     _lib.check(_lib.load().aq_quantize_rows(
         _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, rows, cols, cols, rows * cols,
-        _lib.ptr(codes), _lib.ptr(scales), None, 0, _lib.ptr(flag), _lib.stream_ptr()))
+        _lib.ptr(codes), _lib.ptr(scales), None, 0, ts, _lib.ptr(flag), _lib.stream_ptr()))
     _nonfinite_check(flag)
-    return QuantTensor(rows, cols, spec, _out(codes, was_np), _out(scales, was_np))
+    return QuantTensor(rows, cols, spec, _out(codes, was_np), _out(scales, was_np), ts)
 
 
 _NP2T = {np.float32: torch.float32, np.float64: torch.float32, np.float16: torch.float16}
@@ -156,11 +186,12 @@ def dequantize(qt: QuantTensor, dtype=np.float32):
                                                 _lib.DT_CODE[tdt], _lib.stream_ptr()))
         return _out(out, was_np, None if isinstance(dtype, torch.dtype) else dtype)
     _lib.check(_lib.load().aq_dequantize(_lib.ptr(codes), _lib.ptr(scales), qt.rows, qt.cols,
-                                         _lib.ptr(out), _lib.DT_CODE[tdt], _lib.stream_ptr()))
+                                         _lib.ptr(out), _lib.DT_CODE[tdt], float(qt.tensor_scale),
+                                         _lib.stream_ptr()))
     return _out(out, was_np, None if isinstance(dtype, torch.dtype) else dtype)
 
 
-def fake_quantize(x, spec=NVFP4):
+def fake_quantize(x, spec=NVFP4, tensor_scale=None):
     """Quantize-then-dequantize, shape and dtype preserved (codec.py:336-340)."""
     if spec == MXFP4:
         t, was_np = to_device(x)
@@ -182,7 +213,8 @@ def fake_quantize(x, spec=NVFP4):
     flag = torch.zeros(1, dtype=torch.int32, device=t.device)
     _lib.check(_lib.load().aq_quantize_rows(
         _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, rows, cols, cols, rows * cols,
-        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _lib.ptr(flag), _lib.stream_ptr()))
+        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _ts(tensor_scale, t), _lib.ptr(flag),
+        _lib.stream_ptr()))
     _nonfinite_check(flag)
     np_dt = np.asarray(x).dtype if was_np else None
     return _out(out, was_np, np_dt)
@@ -213,7 +245,7 @@ def fake_quantize_padded(x, spec=NVFP4):
     return out[:, :n] if out.shape[1] != n else out
 
 
-def fake_quantize_cols(x, spec=NVFP4):
+def fake_quantize_cols(x, spec=NVFP4, tensor_scale=None):
     """Blocks along the token (row) axis, ragged tail zero-padded (codec.py:373-381)."""
     if spec == MXFP4:
         t, was_np = to_device(x)
@@ -229,26 +261,28 @@ def fake_quantize_cols(x, spec=NVFP4):
     flag = torch.zeros(1, dtype=torch.int32, device=t.device)
     _lib.check(_lib.load().aq_quantize_cols(
         _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, n, cols, cols, n * cols,
-        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _lib.ptr(flag), _lib.stream_ptr()))
+        None, None, _lib.ptr(out), _lib.DT_CODE[out.dtype], _ts(tensor_scale, t), _lib.ptr(flag),
+        _lib.stream_ptr()))
     _nonfinite_check(flag)
     np_dt = np.asarray(x).dtype if was_np else None
     return _out(out, was_np, np_dt)
 
 
-def quantize_cols(x, spec=NVFP4) -> QuantTensor:
+def quantize_cols(x, spec=NVFP4, tensor_scale=None) -> QuantTensor:
     """QuantTensor of x^T with the token axis zero-padded: quantize_padded(x.T) (flash.py:267)."""
     _require_nvfp4(spec)
     t, was_np = to_device(x)
     n, cols = t.shape
+    ts = _ts(tensor_scale, t)
     n16 = -(-n // 16) * 16
     codes = torch.empty((cols, n16 // 2), dtype=torch.uint8, device=t.device)
     scales = torch.empty((cols, n16 // 16), dtype=torch.uint8, device=t.device)
     flag = torch.zeros(1, dtype=torch.int32, device=t.device)
     _lib.check(_lib.load().aq_quantize_cols(
         _lib.ptr(t), _lib.DT_CODE[t.dtype], 1, n, cols, cols, n * cols,
-        _lib.ptr(codes), _lib.ptr(scales), None, 0, _lib.ptr(flag), _lib.stream_ptr()))
+        _lib.ptr(codes), _lib.ptr(scales), None, 0, ts, _lib.ptr(flag), _lib.stream_ptr()))
     _nonfinite_check(flag)
-    return QuantTensor(cols, n16, spec, _out(codes, was_np), _out(scales, was_np))
+    return QuantTensor(cols, n16, spec, _out(codes, was_np), _out(scales, was_np), ts)
 
 
 # ----------------------------------------------------------------------------

@@ -15,7 +15,7 @@ using namespace aq;
 
 namespace {
 
-constexpr int kAbiVersion = 2;
+constexpr int kAbiVersion = 3;
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
@@ -73,11 +73,55 @@ bool dtype_ok(int dt) { return dt == 0 || dt == 1 || dt == 2; }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? AQ_OK : AQ_E_CUDA; }
 
+// Per-tensor FP32 scales of the two-level NVFP4 format (0 = 1.0, the
+// reference's semantics) and the softmax scale (0 = 1/sqrt(d), flash.py:207).
+struct TScales {
+  float q = 1.f, k = 1.f, v = 1.f, p = 1.f;
+  double sm = 0.0;  // 0: default 1/sqrt(d)
+};
+
+bool take_scale(float x, float& out) {
+  if (x == 0.f) return true;  // keep 1.0
+  if (!(x > 0.f) || !std::isfinite(x)) return false;
+  out = x;
+  return true;
+}
+
+template <typename Args>
+bool read_scales(const Args* a, TScales& t) {
+  if (!take_scale(a->q_scale, t.q) || !take_scale(a->k_scale, t.k) || !take_scale(a->v_scale, t.v) ||
+      !take_scale(a->p_scale, t.p))
+    return false;
+  if (a->softmax_scale != 0.f) {
+    if (!(a->softmax_scale > 0.f) || !std::isfinite(a->softmax_scale)) return false;
+    t.sm = a->softmax_scale;
+  }
+  return true;
+}
+
+// log2(e) * softmax scale * t_q * t_k; the default expression is the one the
+// kernels were validated with (bit-identical L / P at unit scales)
+float scale_log2_of(const TScales& t, int64_t d) {
+  const double base = t.sm == 0.0 ? 1.4426950408889634 / std::sqrt(static_cast<double>(d)) : 1.4426950408889634 * t.sm;
+  return static_cast<float>(base * static_cast<double>(t.q) * static_cast<double>(t.k));
+}
+
+void apply_fwd_scales(FwdParams& p, const TScales& t, int64_t d) {
+  p.scale_log2 = scale_log2_of(t, d);
+  p.o_mul = t.v * t.p;
+  p.ohp_mul = t.v;
+  p.p_r = 1.f / t.p;
+  p.p_lshift = std::log2(t.p);
+}
+
 // Stage Q/K/V into the attention layouts (K1/K2 in tiled mode).
 int stage_operands(const void* q, const void* k, const void* v, int in_dt, int64_t heads, int64_t n_q, int64_t n_k,
-                   int64_t d, uint8_t* ws, const FwdWs& w, cudaStream_t st) {
+                   int64_t d, uint8_t* ws, const FwdWs& w, cudaStream_t st, const TScales& ts = TScales{},
+                   int* nonfinite = nullptr) {
   RowsArgs a{};
   a.x_dt = in_dt;
+  a.nonfinite = nonfinite;
+  a.inv_ts = 1.f / ts.q;
   a.heads = heads;
   a.cols = d;
   a.ld = d;
@@ -92,6 +136,7 @@ int stage_operands(const void* q, const void* k, const void* v, int in_dt, int64
   cudaError_t e = launch_quantize_rows(a, st);
   if (e != cudaSuccess) return AQ_E_CUDA;
   // K
+  a.inv_ts = 1.f / ts.k;
   a.x = k;
   a.n = n_k;
   a.hs = n_k * d;
@@ -101,6 +146,7 @@ int stage_operands(const void* q, const void* k, const void* v, int in_dt, int64
   e = launch_quantize_rows(a, st);
   if (e != cudaSuccess) return AQ_E_CUDA;
   // V (blocks along tokens): fp16 tiles for the O' MMA, bf16 tiles for the backward
+  a.inv_ts = 1.f / ts.v;
   a.x = v;
   a.codes_t = ws + w.v_codes;
   a.sf_t = ws + w.v_sf;
@@ -133,8 +179,11 @@ const char* aq_status_string(int s) {
 }
 
 int aq_quantize_rows(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld, int64_t hs,
-                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite, void* stream) {
+                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, float tensor_scale, int* nonfinite,
+                     void* stream) {
   if (!x || !dtype_ok(x_dtype) || (fq && !dtype_ok(fq_dtype))) return AQ_E_INVALID;
+  float ts = 1.f;
+  if (!take_scale(tensor_scale, ts)) return AQ_E_INVALID;
   if (heads < 0 || n < 0 || cols <= 0 || cols % 16 || ld < cols) return AQ_E_SHAPE;
   if (heads == 0 || n == 0) return AQ_OK;
   RowsArgs a{};
@@ -150,12 +199,17 @@ int aq_quantize_rows(const void* x, int x_dtype, int64_t heads, int64_t n, int64
   a.fq = fq;
   a.fq_dt = fq_dtype;
   a.nonfinite = nonfinite;
+  a.ts = ts;
+  a.inv_ts = 1.f / ts;
   return cuda_status(launch_quantize_rows(a, static_cast<cudaStream_t>(stream)));
 }
 
 int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64_t cols, int64_t ld, int64_t hs,
-                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, int* nonfinite, void* stream) {
+                     uint8_t* codes, uint8_t* scales, void* fq, int fq_dtype, float tensor_scale, int* nonfinite,
+                     void* stream) {
   if (!x || !dtype_ok(x_dtype) || (fq && !dtype_ok(fq_dtype))) return AQ_E_INVALID;
+  float ts = 1.f;
+  if (!take_scale(tensor_scale, ts)) return AQ_E_INVALID;
   if (heads < 0 || n < 0 || cols <= 0 || ld < cols) return AQ_E_SHAPE;
   if (heads == 0 || n == 0) return AQ_OK;
   RowsArgs a{};
@@ -171,6 +225,8 @@ int aq_quantize_cols(const void* x, int x_dtype, int64_t heads, int64_t n, int64
   a.fq = fq;
   a.fq_dt = fq_dtype;
   a.nonfinite = nonfinite;
+  a.ts = ts;
+  a.inv_ts = 1.f / ts;
   return cuda_status(launch_quantize_cols(a, static_cast<cudaStream_t>(stream)));
 }
 
@@ -206,11 +262,14 @@ int aq_e8m0_codes(const void* x, int x_dtype, int64_t n, uint8_t* codes, int* in
 }
 
 int aq_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out, int out_dtype,
-                  void* stream) {
+                  float tensor_scale, void* stream) {
   if (!codes || !scales || !out || !dtype_ok(out_dtype)) return AQ_E_INVALID;
+  float ts = 1.f;
+  if (!take_scale(tensor_scale, ts)) return AQ_E_INVALID;
   if (rows < 0 || cols <= 0 || cols % 16) return AQ_E_SHAPE;
   if (rows == 0) return AQ_OK;
-  return cuda_status(launch_dequantize(codes, scales, rows, cols, out, out_dtype, static_cast<cudaStream_t>(stream)));
+  return cuda_status(
+      launch_dequantize(codes, scales, rows, cols, out, out_dtype, static_cast<cudaStream_t>(stream), ts));
 }
 
 int64_t aq_fp4mm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
@@ -248,11 +307,15 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   if (a->d % 16) return AQ_E_SHAPE;  // flash.py:187-188
   if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
   if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;  // oracle.py:62-66
+  TScales ts;
+  if (!read_scales(a, ts)) return AQ_E_INVALID;
+  if ((a->pf_codes == nullptr) != (a->pf_scales == nullptr)) return AQ_E_INVALID;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const FwdWs w = fwd_ws(a->heads, a->n_q, a->n_k, a->d, a->train, a->keep_for_bwd);
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
   if (!a->operands_staged) {
-    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws, w, st);
+    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws, w, st, ts,
+                           a->nonfinite);
     if (s != AQ_OK) return s;
   }
   FwdParams p{};
@@ -274,7 +337,9 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   p.d = static_cast<int>(a->d);
   p.causal = a->causal;
   p.train = a->train;
-  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  apply_fwd_scales(p, ts, a->d);
+  p.pf_codes = a->pf_codes;
+  p.pf_scales = a->pf_scales;
   return cuda_status(launch_attn_fwd(p, st));
 }
 
@@ -571,6 +636,9 @@ static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx) {
   if (a->d % 16) return AQ_E_SHAPE;
   if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
   if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  TScales ts;
+  if (!read_scales(a, ts)) return AQ_E_INVALID;
+  if (mx && (ts.q != 1.f || ts.k != 1.f || ts.v != 1.f || ts.p != 1.f)) return AQ_E_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const BwdWs bw = bwd_ws(a->heads, a->n_q, a->n_k, a->d);
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
@@ -597,14 +665,15 @@ static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx) {
     w = fw;
   } else {
     // re-fake-quantize Q, K, V from the originals (flash.py:344-349)
-    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws + bw.fwd, fw, st);
+    int s = stage_operands(a->q, a->k, a->v, a->in_dtype, a->heads, a->n_q, a->n_k, a->d, ws + bw.fwd, fw, st, ts,
+                           a->nonfinite);
     if (s != AQ_OK) return s;
     ops = ws + bw.fwd;
     w = fw;
   }
   float* delta = reinterpret_cast<float*>(ws + bw.delta);
   cudaError_t e = launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, static_cast<int>(a->d),
-                                 delta, ws + bw.do_h, st);
+                                 delta, ws + bw.do_h, st, 1.f / ts.v);
   if (e != cudaSuccess) return AQ_E_CUDA;
   BwdParams p{};
   p.q_codes = ops + w.q_codes;
@@ -628,7 +697,18 @@ static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx) {
   p.causal = a->causal;
   p.fq_p = (a->variant == AQ_BWD_CORRECT || a->variant == AQ_BWD_LOW_PREC_O) ? 1 : 0;  // flash.py:93-95
   p.mx = mx ? 1 : 0;
-  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
-  p.inv_sqrt_d = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a->d)));
+  p.scale_log2 = scale_log2_of(ts, a->d);
+  // dS = P (t_v dP - D) * sm = P (dP - D / t_v) * (sm t_v); D arrives divided by t_v
+  p.inv_sqrt_d = static_cast<float>((ts.sm == 0.0 ? 1.0 / std::sqrt(static_cast<double>(a->d)) : ts.sm) *
+                                    static_cast<double>(ts.v));
+  p.p_r = 1.f / ts.p;
+  p.dq_mul = ts.k;
+  p.dk_mul = ts.q;
+  p.dv_mul = ts.p;
+  if ((a->pf_codes == nullptr) != (a->pf_scales == nullptr)) return AQ_E_INVALID;
+  if (!mx) {
+    p.pf_codes = a->pf_codes;
+    p.pf_scales = a->pf_scales;
+  }
   return cuda_status(launch_attn_bwd(p, st));
 }

@@ -20,6 +20,8 @@ struct RowsArgs {
   void* fqh2_t;   // optional second T8x8 copy in another 16-bit dtype (K2 only)
   int fqh2_dt;
   int* nonfinite;
+  float inv_ts = 1.f;  // per-tensor FP32 scale t: blocks of x / t are quantized (1 = reference semantics)
+  float ts = 1.f;      // t, applied to the dense fake-quant output (fq) only
 };
 
 struct FwdParams {
@@ -51,6 +53,14 @@ struct FwdParams {
   int64_t sage_bk;
   int plain_fmt;            // PLAIN instances: 16-bit operand format, 0 = fp16, 1 = bf16
   int head_group;           // causal item order: 0 = longest-first over all heads, G > 0 = within groups of G heads
+  // per-tensor FP32 scales (north_star two-level NVFP4; all 1 = reference semantics, bit for bit):
+  // scale_log2 already holds t_q t_k; O is multiplied by o_mul = t_v t_p, O' by ohp_mul = t_v, and P
+  // blocks are quantized as P * p_r (p_r = 1 / t_p; p_lshift = log2 t_p for the pass-2 early-out)
+  float o_mul = 1.f, ohp_mul = 1.f, p_r = 1.f, p_lshift = 0.f;
+  // instrument (flash.py:117-124, PTileRecord): when set, P^F of every visible row in the
+  // reference's quantize_padded(P) layout per row: codes [heads][n_q][n16/2], scales [heads][n_q][n16/16]
+  uint8_t* pf_codes = nullptr;
+  uint8_t* pf_scales = nullptr;
 };
 
 struct BwdParams {
@@ -73,14 +83,18 @@ struct BwdParams {
   int causal;
   int fq_p;              // quantize the recomputed P for dV
   int mx;                // MXFP4: S on kind::mxf4 block32, P^F in 32-key UE8M0 blocks
-  float scale_log2;      // log2(e)/sqrt(d)
-  float inv_sqrt_d;
+  float scale_log2;      // log2(e)/sqrt(d) (times t_q t_k)
+  float inv_sqrt_d;      // 1/sqrt(d) (times t_v: dS = P (t_v dP - D) / sqrt(d), D pre-divided by t_v)
+  float p_r = 1.f;       // 1 / t_p: P^F quantized as P * p_r (1 = reference semantics)
+  float dq_mul = 1.f, dk_mul = 1.f, dv_mul = 1.f;  // t_k, t_q, t_p (1 = reference semantics)
+  uint8_t* pf_codes = nullptr;   // instrument: the recomputed P^F, layout as FwdParams::pf_codes
+  uint8_t* pf_scales = nullptr;
 };
 
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st);
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st);
 cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
-                              int out_dt, cudaStream_t st);
+                              int out_dt, cudaStream_t st, float ts = 1.f);
 cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer_mx(const FwdParams& p, cudaStream_t st);
@@ -136,6 +150,6 @@ cudaError_t launch_pack_kv4(const uint8_t* k_codes, const uint8_t* k_scales, con
                             const uint8_t* vt_scales, int64_t heads, int64_t n, int d, uint8_t* k_codes_t,
                             uint8_t* k_sf_t, uint8_t* v_codes_t, uint8_t* v_sf_t, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
-                           int d, float* delta, uint8_t* do_h, cudaStream_t st);
+                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul = 1.f);
 
 }  // namespace aq

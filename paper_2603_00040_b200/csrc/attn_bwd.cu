@@ -82,7 +82,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 // N consecutive fp32 values -> dst[base, base+N) in dtype dt (0 fp32, 1 bf16, 2 fp16)
 template <int N>
-__device__ __forceinline__ void store_run(void* dst, int64_t base, int dt, const float* v) {
+__device__ __forceinline__ void store_run(void* dst, int64_t base, int dt, float* v, float mul = 1.f) {
+  if (mul != 1.f) {  // per-tensor scale of the other operand (two-level NVFP4; 1 = reference)
+#pragma unroll
+    for (int e = 0; e < N; ++e) v[e] *= mul;
+  }
   if (dt == 0) {
     float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
 #pragma unroll
@@ -444,7 +448,16 @@ if (!(MX && p.fq_p)) {
       for (int blk = 0; blk < KPT / 16; ++blk) {
         uint4 w[2];
         if (p.fq_p) {
-          const PBlock qb = quantize_p16(pr + blk * 16);
+          const PBlock qb = quantize_p16_s(pr + blk * 16, p.p_r);
+          if (p.pf_codes != nullptr && qvalid) {  // instrument (flash.py:386-387): the recomputed P^F
+            const int64_t n16 = ceil_div(p.n_k, 16);
+            const int64_t gb = (k0 + kb) / 16 + blk;
+            if (gb < n16) {
+              *reinterpret_cast<uint2*>(p.pf_codes + (head * p.n_q + q) * (n16 * 8) + gb * 8) =
+                  make_uint2(qb.codes[0], qb.codes[1]);
+              p.pf_scales[(head * p.n_q + q) * n16 + gb] = static_cast<uint8_t>(qb.scale);
+            }
+          }
           // P^F in bf16 straight from the codes: byte-permute lookups of the
           // E2M1 values' bf16 bytes, then one exact bf16x2 multiply by the
           // decoded scale (code x E4M3 has <= 5 significant bits)
@@ -513,7 +526,8 @@ if (!(MX && p.fq_p)) {
 #pragma unroll
         for (int e = 0; e < DH; ++e) g[e] = 0.f;  // no visible query: zero gradient
       }
-      if (key < p.n_k) store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + kg * DH, p.g_dt, g);
+      if (key < p.n_k)
+        store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + kg * DH, p.g_dt, g, which ? p.dv_mul : p.dk_mul);
     }
   }
 
@@ -783,7 +797,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 #pragma unroll
       for (int e = 0; e < DH; ++e) g[e] = 0.f;
     }
-    if (qvalid) store_run<DH>(p.dq, (head * p.n_q + q) * D + kg * DH, p.g_dt, g);
+    if (qvalid) store_run<DH>(p.dq, (head * p.n_q + q) * D + kg * DH, p.g_dt, g, p.dq_mul);
   }
 
   tc_fence_before();
@@ -828,7 +842,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
 // shuffles over the four lanes that share a row.
 template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt, const void* o_ref, int o_dt,
-                                                      int64_t heads, int64_t n_q, float* delta, uint8_t* do_h) {
+                                                      int64_t heads, int64_t n_q, float* delta, uint8_t* do_h,
+                                                      float delta_mul) {
   constexpr int NCG = D / 8;  // 16-byte column groups per row
   const int64_t q_tiles = ceil_div(n_q, TILE);
   const int64_t row_groups = heads * q_tiles * (TILE / 8);
@@ -888,7 +903,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 8);
     acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-    if (cg == 0) delta[rp] = acc;
+    if (cg == 0) delta[rp] = acc * delta_mul;  // D / t_v (1 = reference), see BwdParams::inv_sqrt_d
   }
 }
 
@@ -928,11 +943,11 @@ extern "C" int aq_debug_bwd_profile(unsigned long long* out, int reset) {
 }
 
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
-                           int d, float* delta, uint8_t* do_h, cudaStream_t st) {
+                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul) {
   const int64_t rows = heads * ceil_div(n_q, TILE) * TILE;
   const int g = bwd::grid_for(rows * 4);  // 4 threads per row
-  if (d == 128) bwd::bwd_pre_kernel<128><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h);
-  else if (d == 64) bwd::bwd_pre_kernel<64><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h);
+  if (d == 128) bwd::bwd_pre_kernel<128><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul);
+  else if (d == 64) bwd::bwd_pre_kernel<64><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

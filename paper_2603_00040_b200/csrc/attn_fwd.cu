@@ -723,9 +723,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
         }
 #pragma unroll
         for (int blk = 0; blk < ((PLAIN || MX) ? 0 : CW / 16); blk += 2) {
-          const PBlock qa = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16, bm[blk], rr[blk]) : quantize_p16(x + blk * 16);
-          const PBlock qb =
-              (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16 + 16, bm[blk + 1], rr[blk + 1]) : quantize_p16(x + blk * 16 + 16);
+          const PBlock qa = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16, bm[blk], rr[blk])
+                                            : quantize_p16_s(x + blk * 16, p.p_r);
+          const PBlock qb = (SAGE && TRAIN) ? quantize_p16_r(x + blk * 16 + 16, bm[blk + 1], rr[blk + 1])
+                                            : quantize_p16_s(x + blk * 16 + 16, p.p_r);
           *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
               make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
           scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
@@ -780,6 +781,21 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
             *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
           }
         }
+        if (!PLAIN && !MX && p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
+          const int64_t n16 = ceil_div(p.n_k, 16);
+          const int64_t c0 = static_cast<int64_t>(jj) * TILE + cbase;
+          uint8_t* dc = p.pf_codes + (head * p.n_q + grow) * (n16 * 8);
+          uint8_t* dsc = p.pf_scales + (head * p.n_q + grow) * n16;
+#pragma unroll
+          for (int b = 0; b < CW / 16; ++b) {
+            const int64_t blk = c0 / 16 + b;
+            if (blk < n16) {
+              *reinterpret_cast<uint2*>(dc + blk * 8) =
+                  *reinterpret_cast<const uint2*>(pcodes + t8x32_off(row, cbase + 16 * b, TILE));
+              dsc[blk] = psf[sf512_off(row, cbase / 16 + b)];
+            }
+          }
+        }
         AQ_PROF(const long long tm3 = clock64();)
         fence_async_smem();
         mbar_arrive(&bars[C::B_P_FULL + pb]);
@@ -819,7 +835,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
           void* dst = out ? p.o_hp : p.o;
           if (dst == nullptr) continue;
           const int dt = out ? p.o_hp_dt : p.o_dt;
-          const float mul = out ? inv_l : 1.f;
+          const float mul = out ? inv_l * p.ohp_mul : p.o_mul;  // per-tensor scales (1 = reference)
           const int64_t base = (head * p.n_q + grow) * D + half * DW;
           if (dt == 0) {
             float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);

@@ -37,6 +37,10 @@
 #ifndef AQ_FWDI_NP
 #define AQ_FWDI_NP 2
 #endif
+// how many pass-2 S tiles MMA B may issue ahead of the PV MMA it is waiting on
+#ifndef AQ_FWDI_SLEAD
+#define AQ_FWDI_SLEAD 1
+#endif
 
 namespace aq {
 namespace fwdi {
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       mbar_wait(&bars[C::B_QSF + qs], (k / C::NQ) & 1);
       tc_fence_after();
       for (int ns = 0, np = 0; np < nt;) {
-        if (ns < nt && ns <= np + 1) {
+        if (ns < nt && ns <= np + AQ_FWDI_SLEAD) {
           const int st = (it + ns) % C::NSB;
           mbar_wait(&bars[C::B_KB_FULL + st], ((it + ns) / C::NSB) & 1);
           if (su > 0) mbar_wait(&bars[C::B_SB_EMPTY], (su - 1) & 1);
@@ -354,6 +358,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     const int cbase = half * CW;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((gw & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
+    const float p_r = p.p_r;  // 1 / t_p (1 = the reference's P^F)
     float x[CW];
     int su = 0, pc = 0, k = 0;
     int chk_wait = 0, chk_pen = 0;  // early-out back-off (warp-uniform)
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
         const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
         mbar_arrive(&bars[C::B_L_EMPTY + qs]);
-        const float thr = p_skip_thr(L2, sl2);
+        const float thr = p_skip_thr(L2 + p.p_lshift, sl2);  // blocks of P * p_r below 2^-11
         for (int jj = 0; jj < nt; ++jj) {
           mbar_wait(&bars[C::B_SB_FULL], su & 1);
           ++su;
@@ -492,8 +497,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
               scw[0] |= sc << (8 * (blk / 2));
               return;
             }
-            const PBlock qa = quantize_p16(x + blk * 16);
-            const PBlock qb = quantize_p16(x + blk * 16 + 16);
+            const PBlock qa = quantize_p16_s(x + blk * 16, p_r);
+            const PBlock qb = quantize_p16_s(x + blk * 16 + 16, p_r);
 #endif
             *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
                 make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
@@ -525,11 +530,11 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
               qa.codes[0] = qa.codes[1] = qb.codes[0] = qb.codes[1] = 0u;
               if (!((sk >> blk) & 1u)) {
                 p_from_s<8>(x + blk * 16, cbase + blk * 16, sl2, L2);
-                qa = quantize_p16(x + blk * 16);
+                qa = quantize_p16_s(x + blk * 16, p_r);
               }
               if (!((sk >> (blk + 1)) & 1u)) {
                 p_from_s<8>(x + blk * 16 + 16, cbase + blk * 16 + 16, sl2, L2);
-                qb = quantize_p16(x + blk * 16 + 16);
+                qb = quantize_p16_s(x + blk * 16 + 16, p_r);
               }
               *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
                   make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
@@ -549,6 +554,21 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             for (int s = 0; s < CW / 64; ++s)
               *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
           }
+          if (p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
+            const int64_t n16 = ceil_div(p.n_k, 16);
+            const int64_t c0 = static_cast<int64_t>(jj) * TILE + cbase;  // first key of this thread
+            uint8_t* dc = p.pf_codes + (item.head * p.n_q + grow) * (n16 * 8);
+            uint8_t* ds = p.pf_scales + (item.head * p.n_q + grow) * n16;
+#pragma unroll
+            for (int b = 0; b < CW / 16; ++b) {
+              const int64_t blk = c0 / 16 + b;
+              if (blk < n16) {
+                *reinterpret_cast<uint2*>(dc + blk * 8) =
+                    *reinterpret_cast<const uint2*>(pcodes + t8x32_off(row, cbase + 16 * b, TILE));
+                ds[blk] = psf[sf512_off(row, cbase / 16 + b)];
+              }
+            }
+          }
           fence_async_smem();
           mbar_arrive(&bars[C::B_P_FULL + pb]);
         }
@@ -562,6 +582,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars[C::B_O_EMPTY]);
+        if (p.o_mul != 1.f) {  // per-tensor scales t_v t_p (two-level NVFP4)
+#pragma unroll
+          for (int c = 0; c < DW; ++c) o[c] *= p.o_mul;
+        }
         if (grow < p.n_q && p.o != nullptr) {
           const int64_t base = (item.head * p.n_q + grow) * D + half * DW;
           if (p.o_dt == 0) {

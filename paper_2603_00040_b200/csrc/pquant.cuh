@@ -68,6 +68,17 @@ __device__ __forceinline__ PBlock quantize_p16_r(const float* p, float amax, flo
   return b;
 }
 
+// NVFP4 P block under a per-tensor P scale t_p (r = 1 / t_p): the block of
+// P * r is quantized (two-level NVFP4: P^F = t_p * scale * code). r = 1 is the
+// reference's semantics and gives exactly quantize_p16's bits (amax * 1 and
+// rcp * 1 are exact), so the parity path is unchanged.
+__device__ __forceinline__ PBlock quantize_p16_s(const float* p, float r) {
+  float m0 = fmaxf(p[0], p[1]), m1 = fmaxf(p[2], p[3]), m2 = fmaxf(p[4], p[5]), m3 = fmaxf(p[6], p[7]);
+  float m4 = fmaxf(p[8], p[9]), m5 = fmaxf(p[10], p[11]), m6 = fmaxf(p[12], p[13]), m7 = fmaxf(p[14], p[15]);
+  const float amax = fmaxf(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)), fmaxf(fmaxf(m4, m5), fmaxf(m6, m7)));
+  return quantize_p16_r(p, amax, r);
+}
+
 // MXFP4 P block (32 keys, codec.py:123-203): UE8M0 scale = nearest power of
 // two of amax / 6 with ties up (0 for a zero block), codes = E2M1_RNE(p / scale)
 // with the exact power-of-two reciprocal. P >= 0.

@@ -121,6 +121,20 @@ __device__ __forceinline__ void quantize_block16(const float (&v)[16], Block16& 
   }
 }
 
+// Per-tensor FP32 scale t (two-level NVFP4): the block quantizer sees x / t,
+// applied as x * (1 / t). t = 1 multiplies by 1.0 (exact), so the reference's
+// bits are unchanged; the branch keeps that case free.
+__device__ __forceinline__ void scale16(float (&v)[16], float inv_ts) {
+  if (inv_ts != 1.f) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const float2 t = __fmul2_rn(make_float2(v[j], v[j + 1]), make_float2(inv_ts, inv_ts));
+      v[j] = t.x;
+      v[j + 1] = t.y;
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t h2_to(const __half2 h, int dt) {
   // f16 pair -> the same pair in dt (16-bit dtypes only); exact for fq values
   if (dt == kF16) return *reinterpret_cast<const uint32_t*>(&h);
@@ -129,7 +143,13 @@ __device__ __forceinline__ uint32_t h2_to(const __half2 h, int dt) {
   return *reinterpret_cast<const uint32_t*>(&b);
 }
 
-__device__ __forceinline__ void store_fq16(void* p, int64_t i0, int dt, const __half2 (&fq)[8]) {
+__device__ __forceinline__ void store_fq16(void* p, int64_t i0, int dt, const __half2 (&fq)[8], float ts = 1.f) {
+  if (ts != 1.f) {  // two-level NVFP4: dequantized value = t * scale * code
+    const __half* fh = reinterpret_cast<const __half*>(fq);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) store_elem(p, i0 + j, dt, __half2float(fh[j]) * ts);
+    return;
+  }
   if (dt == kF32) {
     float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + i0);
 #pragma unroll
@@ -197,13 +217,14 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
       }
       Block16 q;
+      scale16(v, a.inv_ts);
       quantize_block16<WANT_FQ>(v, q);
       if (real) {
         if (!q.finite && a.nonfinite) atomicOr(a.nonfinite, 1);
         if (a.codes_ref)
           *reinterpret_cast<uint2*>(a.codes_ref + row * (a.cols / 2) + b * 8) = make_uint2(q.packed[0], q.packed[1]);
         if (a.scales_ref) a.scales_ref[row * nb + b] = static_cast<uint8_t>(q.scale);
-        if (WANT_FQ && a.fq) store_fq16(a.fq, row * a.cols + b * 16, a.fq_dt, q.fq);
+        if (WANT_FQ && a.fq) store_fq16(a.fq, row * a.cols + b * 16, a.fq_dt, q.fq, a.ts);
       }
       if (a.codes_t)
         *reinterpret_cast<uint2*>(a.codes_t + tile * fp4_tile_bytes(D) + t8x32_off(rr, static_cast<int>(b) * 16, TILE)) =
@@ -231,7 +252,8 @@ template <int D, bool FQH, bool F32 = false>
 __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __restrict__ xv, int64_t rows,
                                                                   uint8_t* __restrict__ codes_t,
                                                                   uint8_t* __restrict__ sf_t,
-                                                                  uint8_t* __restrict__ fqh_t, int fqh_dt) {
+                                                                  uint8_t* __restrict__ fqh_t, int fqh_dt,
+                                                                  float inv_ts, int* __restrict__ nonfinite) {
   constexpr int NPAIR = D / 32;
   const int64_t total = rows * NPAIR;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -254,7 +276,8 @@ __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __
           v[4 * j + 2] = f.z;
           v[4 * j + 3] = f.w;
         }
-        quantize_block16<FQH, false>(v, q[h]);
+        scale16(v, inv_ts);
+        quantize_block16<FQH, true>(v, q[h]);
       }
     } else {
       const uint4* src =
@@ -270,9 +293,12 @@ __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __
           v[2 * j] = __uint_as_float(ww[j] << 16);
           v[2 * j + 1] = __uint_as_float(ww[j] & 0xFFFF0000u);
         }
-        quantize_block16<FQH, false>(v, q[h]);
+        scale16(v, inv_ts);
+        quantize_block16<FQH, true>(v, q[h]);
       }
     }
+    // NaN / Inf input (codec.py:313-314): flag it for the host to raise InvalidValue
+    if (nonfinite != nullptr && !(q[0].finite && q[1].finite)) atomicOr(nonfinite, 1);
     if (FQH) {
       // the 16-bit fake-quantized operand tile the backward reuses (T8x8)
       uint8_t* base = fqh_t + tile * h_tile_bytes(D);
@@ -318,7 +344,7 @@ __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfl
                                                                   int64_t n, uint8_t* __restrict__ codes_t,
                                                                   uint8_t* __restrict__ sf_t, uint8_t* __restrict__ fqh_t,
                                                                   int fqh_dt, uint8_t* __restrict__ fqh2_t,
-                                                                  int fqh2_dt) {
+                                                                  int fqh2_dt, float inv_ts, int* __restrict__ nonfinite) {
   constexpr int SLAB = 64, PITCH = D + 8;  // tokens per CTA step; padded row (16-bit elements)
   __shared__ __align__(16) __nv_bfloat16 slab[SLAB][PITCH];
   // training: the dequantized values, as f16 pairs, for the T8x8 operand tiles
@@ -352,9 +378,12 @@ __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfl
       Block16 q[2][2];  // [column][16-token block]
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
-        const float* v = cc ? v1 : v0;
-        quantize_block16<FQH, false>(*reinterpret_cast<const float(*)[16]>(v), q[cc][0]);
-        quantize_block16<FQH, false>(*reinterpret_cast<const float(*)[16]>(v + 16), q[cc][1]);
+        float* v = cc ? v1 : v0;
+        scale16(*reinterpret_cast<float(*)[16]>(v), inv_ts);
+        scale16(*reinterpret_cast<float(*)[16]>(v + 16), inv_ts);
+        quantize_block16<FQH, true>(*reinterpret_cast<const float(*)[16]>(v), q[cc][0]);
+        quantize_block16<FQH, true>(*reinterpret_cast<const float(*)[16]>(v + 16), q[cc][1]);
+        if (nonfinite != nullptr && !(q[cc][0].finite && q[cc][1].finite)) atomicOr(nonfinite, 1);
         const int col = 2 * cp + cc;
         *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(col, kt, D)) =
             make_uint4(q[cc][0].packed[0], q[cc][0].packed[1], q[cc][1].packed[0], q[cc][1].packed[1]);
@@ -460,6 +489,7 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = slab[tb + j][c];
             Block16 q;
+            scale16(v, a.inv_ts);
             quantize_block16<WANT_FQ>(v, q);
             codes[2 * hb] = q.packed[0];
             codes[2 * hb + 1] = q.packed[1];
@@ -476,7 +506,7 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
                 const __half* fh = reinterpret_cast<const __half*>(q.fq);
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                  if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + col, a.fq_dt, __half2float(fh[j]));
+                  if (b0 + j < a.n) store_elem(a.fq, (h * a.n + b0 + j) * a.cols + col, a.fq_dt, __half2float(fh[j]) * a.ts);
               }
             }
             if (WANT_FQ && (a.fqh_t || a.fqh2_t)) {
@@ -534,7 +564,7 @@ __global__ void __launch_bounds__(128) quantize_cols_kernel(RowsArgs a) {
 
 // K3: reference-layout codes + scales -> dense values. rows x cols.
 __global__ void __launch_bounds__(256) dequantize_kernel(const uint8_t* codes, const uint8_t* scales, int64_t rows,
-                                                         int64_t cols, void* out, int out_dt) {
+                                                         int64_t cols, void* out, int out_dt, float ts) {
   const int64_t nb = cols / 16;
   const int64_t total = rows * nb;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
@@ -546,7 +576,7 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const uint8_t* codes, c
     for (int j = 0; j < 16; ++j) {
       const uint32_t word = j < 8 ? w.x : w.y;
       const uint32_t code = (word >> (4 * (j & 7))) & 0xF;
-      store_elem(out, r * cols + b * 16 + j, out_dt, e2m1_to_f32(code) * s);
+      store_elem(out, r * cols + b * 16 + j, out_dt, e2m1_to_f32(code) * s * ts);  // ts = 1: exact
     }
   }
 }
@@ -601,13 +631,13 @@ cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
   const bool fast = (a.x_dt == kBF16 || a.x_dt == kF32) && a.codes_t && a.sf_t && !a.fq && !a.codes_ref &&
-                    !a.scales_ref && !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    !a.scales_ref && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
   if (fast && a.x_dt == kF32 && !a.fqh_t) {
     const int64_t rows = a.heads * a.n;
     const int g = grid_for(rows * (a.cols / 32));
-    if (a.cols == 128) quantize_rows_tiled_kernel<128, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0);
-    else quantize_rows_tiled_kernel<64, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0);
+    if (a.cols == 128) quantize_rows_tiled_kernel<128, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
+    else quantize_rows_tiled_kernel<64, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     return cudaGetLastError();
   }
   if (fast && a.x_dt == kBF16) {
@@ -616,11 +646,11 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
     const auto* x = a.x;
     uint8_t* fqh = static_cast<uint8_t*>(a.fqh_t);
     if (a.cols == 128) {
-      if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt);
-      else quantize_rows_tiled_kernel<128, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0);
+      if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
+      else quantize_rows_tiled_kernel<128, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     } else {
-      if (fqh) quantize_rows_tiled_kernel<64, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt);
-      else quantize_rows_tiled_kernel<64, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0);
+      if (fqh) quantize_rows_tiled_kernel<64, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
+      else quantize_rows_tiled_kernel<64, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     }
     return cudaGetLastError();
   }
@@ -645,7 +675,8 @@ cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
 template <int D>
 __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat16* __restrict__ x, int64_t heads,
                                                                int64_t n, uint8_t* __restrict__ codes_t,
-                                                               uint8_t* __restrict__ sf_t) {
+                                                               uint8_t* __restrict__ sf_t, float inv_ts,
+                                                               int* __restrict__ nonfinite) {
   constexpr int PITCH = D + 8;
   __shared__ __align__(16) __nv_bfloat16 slab[32][PITCH];
   const int64_t nslabs = heads * (n / 32);
@@ -666,8 +697,10 @@ __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat
       float v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __bfloat162float(slab[16 * b + j][c]);
-      quantize_block16<false, false>(v, q[b]);
+      scale16(v, inv_ts);
+      quantize_block16<false, true>(v, q[b]);
     }
+    if (nonfinite != nullptr && !(q[0].finite && q[1].finite)) atomicOr(nonfinite, 1);
     const int64_t tile = tok0 / TILE;
     const int kt = static_cast<int>(tok0 % TILE);
     *reinterpret_cast<uint4*>(codes_t + tile * fp4_tile_bytes(D) + t8x32_off(c, kt, D)) =
@@ -679,7 +712,7 @@ __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
   const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
-                    !a.nonfinite && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
   if (fast) {
     int64_t g = a.heads * (a.n / 64);
@@ -693,17 +726,17 @@ cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
       int64_t gs = a.heads * (a.n / 32);
       if (gs > 148 * 16) gs = 148 * 16;
       if (a.cols == 128)
-        quantize_cols_slab_kernel<128><<<static_cast<int>(gs), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+        quantize_cols_slab_kernel<128><<<static_cast<int>(gs), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, a.inv_ts, a.nonfinite);
       else
-        quantize_cols_slab_kernel<64><<<static_cast<int>(gs), 64, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t);
+        quantize_cols_slab_kernel<64><<<static_cast<int>(gs), 64, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, a.inv_ts, a.nonfinite);
       return cudaGetLastError();
     }
     if (a.cols == 128) {
-      if (fqh) quantize_cols_tiled_kernel<128, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt);
-      else quantize_cols_tiled_kernel<128, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0);
+      if (fqh) quantize_cols_tiled_kernel<128, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
+      else quantize_cols_tiled_kernel<128, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
     } else {
-      if (fqh) quantize_cols_tiled_kernel<64, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt);
-      else quantize_cols_tiled_kernel<64, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0);
+      if (fqh) quantize_cols_tiled_kernel<64, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
+      else quantize_cols_tiled_kernel<64, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
     }
     return cudaGetLastError();
   }
@@ -719,8 +752,8 @@ cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_dequantize(const uint8_t* codes, const uint8_t* scales, int64_t rows, int64_t cols, void* out,
-                              int out_dt, cudaStream_t st) {
-  dequantize_kernel<<<grid_for(rows * (cols / 16)), 256, 0, st>>>(codes, scales, rows, cols, out, out_dt);
+                              int out_dt, cudaStream_t st, float ts) {
+  dequantize_kernel<<<grid_for(rows * (cols / 16)), 256, 0, st>>>(codes, scales, rows, cols, out, out_dt, ts);
   return cudaGetLastError();
 }
 

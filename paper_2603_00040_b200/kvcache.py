@@ -87,9 +87,9 @@ def kv4_quantize(k, v) -> KV4Cache:
     lib = _lib.load()
     st = _lib.stream_ptr()
     _lib.check(lib.aq_quantize_rows(_lib.ptr(k3), _lib.DT_CODE[k3.dtype], heads, n, d, d, n * d, _lib.ptr(kc),
-                                    _lib.ptr(ks), None, 0, _lib.ptr(flag), st))
+                                    _lib.ptr(ks), None, 0, 1.0, _lib.ptr(flag), st))
     _lib.check(lib.aq_quantize_cols(_lib.ptr(v3), _lib.DT_CODE[v3.dtype], heads, n, d, d, n * d, _lib.ptr(vc),
-                                    _lib.ptr(vs), None, 0, _lib.ptr(flag), st))
+                                    _lib.ptr(vs), None, 0, 1.0, _lib.ptr(flag), st))
     if int(flag.item()):
         raise InvalidValue("quantize requires finite input")
     return KV4Cache(heads, n, d, kc, ks, vc, vs)

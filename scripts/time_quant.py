@@ -33,8 +33,8 @@ def t(fn, reps=20):
 n = x.numel()
 alg = n * 2 + n // 2 + n // 16
 rows = t(lambda: lib.aq_quantize_rows(x.data_ptr(), 1, B * H, N, d, d, N * d, codes.data_ptr(),
-                                      scales.data_ptr(), None, 0, None, st))
+                                      scales.data_ptr(), None, 0, 1.0, None, st))
 cols = t(lambda: lib.aq_quantize_cols(x.data_ptr(), 1, B * H, N, d, d, N * d, codes.data_ptr(),
-                                      scales.data_ptr(), None, 0, None, st))
+                                      scales.data_ptr(), None, 0, 1.0, None, st))
 print(json.dumps({"rows_ms": rows, "rows_GBs": alg / rows / 1e6, "cols_ms": cols, "cols_GBs": alg / cols / 1e6,
                   "alg_bytes": alg}))

@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.PROTOTYPES)
-    assert lib.aq_abi_version() == 2
+    assert lib.aq_abi_version() == 3
 
 
 def test_struct_fields_match_header():
@@ -91,3 +91,31 @@ def test_no_cpu_fallback():
     with pytest.raises(RuntimeError):
         aq.flash_forward_training(np.zeros((128, 64)), np.zeros((128, 64)), np.zeros((128, 64)),
                                   aq.TileConfig(b_q=128, b_k=128))
+
+
+def test_kernel_head_dim_padding_rule():
+    import paper_2603_00040_b200 as aq
+    assert [aq.kernel_head_dim(d) for d in (16, 32, 48, 64, 80, 96, 112, 128)] == [64] * 4 + [128] * 4
+    for bad in (8, 24, 136, 256):
+        with pytest.raises(aq.InvalidValue):
+            aq.kernel_head_dim(bad)
+
+
+def test_instrument_tile_walk_matches_reference_skips():
+    """flash.py:127-132, 154: fully masked tiles are skipped (right-aligned causal)."""
+    import paper_2603_00040_b200 as aq
+    from paper_2603_00040_b200.flash import _visited_tiles
+    cfg = aq.TileConfig(b_q=16, b_k=16, causal=True)
+    assert list(_visited_tiles(32, 32, cfg)) == [(0, 0), (1, 0), (1, 1)]
+    assert list(_visited_tiles(32, 64, cfg)) == [(0, 0), (0, 1), (0, 2), (1, 0), (1, 1), (1, 2), (1, 3)]
+    assert len(list(_visited_tiles(32, 64, aq.TileConfig(b_q=16, b_k=16)))) == 8
+
+
+def test_header_abi3_fields_default_to_reference_semantics():
+    """ABI 3: every new field's zero value is the reference's behaviour (ctypes zero-initialises)."""
+    from paper_2603_00040_b200 import _lib
+    a = _lib.AqFwdArgs()
+    assert (a.softmax_scale, a.q_scale, a.k_scale, a.v_scale, a.p_scale) == (0.0,) * 5
+    assert a.nonfinite is None and a.pf_codes is None and a.pf_scales is None
+    b = _lib.AqBwdArgs()
+    assert b.p_scale == 0.0 and b.pf_codes is None
