@@ -7,10 +7,18 @@ inference forward, B=4 H=32 N=8192 d=128 (FP4). One step = one call of the
 public operator (``attn_forward``: NVFP4 quantizers for Q/K/V + the fused
 two-pass tcgen05 attention kernel) on inputs already resident in HBM.
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the full per-GPU
-workload on its own batch (B x H heads are independent units; no
-communication on the attention path) -> "scaling": "weak"; the timed region
-is bracketed by barriers and the max over ranks is reported.
+Multi-GPU (one process per GPU; ``--gpus N`` relaunches itself under torchrun
+when WORLD_SIZE is unset): the NAMED config's B x H heads are split
+contiguously over the ranks (C2: 128 heads -> 16 per GPU at N=8; C3: 40 -> 5;
+every (b, h) pair is an independent unit, oracle.py:96-103), with no
+communication on the attention path -> "scaling": "strong" (the total work is
+fixed); value = the whole config's algorithmic FLOPs / the slowest rank's
+time (barrier-bracketed, max over ranks via an NCCL all-reduce).
+
+The 1-GPU C2 line also carries, nested under ``other_configs``, the tier's
+largest single-GPU config C3 (Wan 2.1, N = 32760) and the fwd+bwd half of the
+metric C4 (Llama training shape), each with its own roofline, and every entry
+carries the same-box BF16 comparator (cuDNN SDPA) with the FP4 / BF16 ratio.
 
 ``--impl reference`` times the reference algorithm on the host CPU cores (the
 oracle port in oracle/ -- the reference is pure NumPy), rank 0
@@ -26,7 +34,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from concurrent.futures import ProcessPoolExecutor
 
@@ -194,9 +201,9 @@ def run_reference_arm(args, cfg, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (numpy)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64 (numpy)",
         "data": "synthetic N(0,1)",
-        "config": {"workload": args.config, "B": B, "H": H, "N": N, "d": d, "causal": causal, "mode": mode},
+        "config": config_dict(args.config, cfg, world),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": ref.cores, "kind": "port",
                          "sample": ref.sample()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -225,6 +232,67 @@ def measure_mma_peaks(lib, torch):
     return out
 
 
+def shard_units(units, rank, world):
+    """Contiguous block split of the flattened B*H head index over the ranks
+    (SURVEY 8(e)): rank r owns heads [start, stop); every head is owned once."""
+    base, rem = divmod(units, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+def config_dict(name, cfg, world):
+    """The workload description both arms print (same keys, same values)."""
+    B, H, N, d, causal, mode = cfg
+    return {"workload": name, "B": B, "H": H, "N": N, "d": d, "causal": causal,
+            "mode": {"fwd": "inference fwd", "train": "training fwd+bwd", "layer": "QAT layer step"}[mode],
+            "global_batch": B, "parallelism": f"dp{world}: B*H heads sharded contiguously (no comms)"
+            if mode != "layer" else f"dp{world} batch-sharded + NCCL grad all-reduce",
+            "l2": "inputs larger than L2 (bf16 Q/K/V %.0f MB each)" % (B * H * N * d * 2 / 1e6)}
+
+
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def time_device(torch, fn, steps, warmup, st, barrier):
+    for _ in range(warmup):
+        fn()
+    barrier()
+    e0, e1 = _events(torch)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def bf16_comparator(torch, q, k, v, causal, mode, d_o=None, steps=5):
+    """Same-box BF16 FlashAttention on the same per-rank shape: cuDNN SDPA (the
+    strongest local bf16 attention); flash_attn 2.8 as the fallback."""
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    st = torch.cuda.current_stream()
+    for name, be in (("cudnn_sdpa", SDPBackend.CUDNN_ATTENTION), ("flash_sdpa", SDPBackend.FLASH_ATTENTION)):
+        try:
+            with sdpa_kernel(be):
+                if mode == "fwd":
+                    def fn():
+                        F.scaled_dot_product_attention(q, k, v, is_causal=causal)
+                else:
+                    qg, kg, vg = (t.detach().clone().requires_grad_() for t in (q, k, v))
+
+                    def fn():
+                        for t_ in (qg, kg, vg):
+                            t_.grad = None
+                        F.scaled_dot_product_attention(qg, kg, vg, is_causal=causal).backward(d_o)
+                ms = time_device(torch, fn, steps, 3, st, torch.cuda.synchronize)
+            return {"impl": name, "ms": ms}
+        except Exception as e:  # noqa: BLE001 - try the next backend
+            err = str(e)[:100]
+    return {"impl": None, "error": err}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -233,9 +301,19 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the nested C3 / C4 entries and the bf16 comparator")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = parse_config(args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (the driver launches torchrun itself)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
 
@@ -246,24 +324,55 @@ def main():
     import torch
     import torch.distributed as dist
 
-    import paper_2603_00040_b200 as aq
-    from paper_2603_00040_b200 import _lib
-
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")        # the communicator is visible in the logs
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B, H, N, d, causal, mode = cfg
     if mode == "layer":
         run_layer_mode(args, cfg, rank, world, local)
         return
+    rec = run_attention(args, args.config, cfg, rank, world, local, main_line=True)
+    if rank == 0:
+        print(json.dumps(rec), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_attention(args, name, cfg, rank, world, local, main_line=False):
+    """Time one attention config: the named config's B*H heads sharded over the
+    ranks, whole-job TFLOP/s over the slowest rank; roofline of the dominant
+    kernel; e2e through the host-buffer API; same-box bf16 comparator."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_00040_b200 as aq
+    from paper_2603_00040_b200 import _lib
+
+    B, H, N, d, causal, mode = cfg
+    units = B * H
+    h0, h1 = shard_units(units, rank, world)
+    heads = h1 - h0
     dev = torch.device("cuda", local)
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    q, k, v = (torch.randn(B, H, N, d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(3))
+    gen = torch.Generator(device=dev).manual_seed(1000 + h0)
+    q, k, v = (torch.randn(heads, N, d, generator=gen, device=dev).to(torch.bfloat16) for _ in range(3))
     lib = _lib.load()
     st = torch.cuda.current_stream()
-    heads = B * H
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    d_o = None
     if mode == "fwd":
         ws = torch.empty(lib.aq_attn_fwd_workspace_bytes(heads, N, N, d, 0, 0), dtype=torch.uint8, device=dev)
         o = torch.empty(heads, N, d, dtype=torch.bfloat16, device=dev)
@@ -273,7 +382,7 @@ def main():
             aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, out=o, lse_out=lse)
         launches_per_step = 4          # quantize Q, K (rows), V (cols), fused attention
     else:
-        d_o = torch.randn(B, H, N, d, generator=gen, device=dev).to(torch.bfloat16)
+        d_o = torch.randn(heads, N, d, generator=gen, device=dev).to(torch.bfloat16)
         qg, kg, vg = (t.clone().requires_grad_() for t in (q, k, v))
 
         def step():
@@ -283,16 +392,11 @@ def main():
             out.backward(d_o)
         launches_per_step = 4 + 2      # fwd (3 quantizers + attention) + bwd pre, fused bwd (dK/dV + dQ roles)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
     for _ in range(args.warmup):
         step()
     barrier()
     with ClockSampler(local) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = _events(torch)
         barrier()
         e0.record(st)
         for _ in range(args.steps):
@@ -301,129 +405,103 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     clocks = clk.summary()
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    flops_rank = alg_flops(B, H, N, d, causal, mode)
-    value = world * flops_rank / (ms_max * 1e-3) / 1e12
-    tokens_s = world * B * N / (ms_max * 1e-3)
+    ms_max = max_over_ranks(ms)
+    flops_job = alg_flops(B, H, N, d, causal, mode)
+    value = flops_job / (ms_max * 1e-3) / 1e12
+    tokens_s = B * N / (ms_max * 1e-3)
 
-    # ---- dominant kernel alone (attention on pre-staged operands) -> roofline
-    roof = None
+    # ---- dominant kernel alone -> roofline
     peaks = measure_mma_peaks(lib, torch)
+    flops_rank = flops_job * heads / units
+    reps = max(args.steps, 5)
     if mode == "fwd":
-        aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, out=o, lse_out=lse)
-        torch.cuda.synchronize()
-        reps = max(args.steps, 5)
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0.record(st)
-        for _ in range(reps):
-            aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, out=o, lse_out=lse,
-                            operands_staged=True)
-        k1.record(st)
-        k1.synchronize()
-        kms = k0.elapsed_time(k1) / reps
-        achieved = alg_flops(B, H, N, d, causal, "fwd") / (kms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "attn_fwd_infer_kernel<128>", "achieved": achieved,
+        kms = time_device(torch, lambda: aq.attn_forward(q, k, v, causal=causal, train=False, workspace=ws, out=o,
+                                                       lse_out=lse, operands_staged=True), reps, 2, st, barrier)
+        achieved = flops_rank / (kms * 1e-3) / 1e12
+        sfu = _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch)
+        roof = {"bound": "tensor", "kernel": f"attn_fwd_infer_kernel<{d}>", "achieved": achieved,
                 "peak": peaks["nvfp4"], "unit": "TFLOP/s", "frac": achieved / peaks["nvfp4"],
                 "peak_source": "measured live: tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak)",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                 "path_ceiling_frac": achieved / (peaks["nvfp4"] * 2.0 / 3.0),
-                # the binding unit is the SFU: 2 exponentials per score (7/8 on MUFU.EX2) plus one
-                # reciprocal per 16-key block = 1.81 MUFU ops per score (ncu: 1.87 incl. merges),
-                # at 16 MUFU/clk/SM; the algorithmic FLOPs per score are 4 d
-                "sfu_ceiling_tflops": _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch),
-                "sfu_frac": achieved / _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch),
-                "traffic": _traffic_from_profiles(args.config)}
+                # the MUFU-bound ceiling: 2 exponentials per score (7/8 on MUFU.EX2) plus one
+                # reciprocal per 16-key block, 1.87 MUFU ops per score, 16 MUFU/clk/SM
+                "sfu_ceiling_tflops": sfu, "sfu_frac": achieved / sfu,
+                "traffic": _traffic_from_profiles(name)}
     else:
-        roof = {"bound": "tensor", "kernel": "attn_fwd+attn_bwd", "achieved": value / world,
-                "peak": peaks["nvfp4"], "unit": "TFLOP/s", "frac": value / world / peaks["nvfp4"],
-                "peak_source": "measured live nvfp4 probe; mixed FP4/bf16 ceiling = 1.17 x bf16 peak",
-                "mixed_ceiling_frac": value / world / (1.17 * peaks["bf16"]),
-                "traffic": _traffic_from_profiles(args.config)}
+        o_f, lse_f, ohp_f, wsf = aq.attn_forward(q, k, v, causal=causal, train=True, keep_for_bwd=True)
+        wsb = torch.empty(lib.aq_attn_bwd_workspace_bytes(heads, N, N, d), dtype=torch.uint8, device=dev)
+        gq, gk, gv = (torch.empty_like(q) for _ in range(3))
+        bms = time_device(torch, lambda: aq.attn_backward(q, k, v, d_o, o_f, ohp_f, lse_f, causal=causal,
+                                                        fwd_workspace=wsf, workspace=wsb, grads_out=(gq, gk, gv)),
+                          reps, 2, st, barrier)
+        bflops = flops_rank * 2.5 / 3.5
+        achieved = bflops / (bms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": f"attn_bwd_kernel<{d}> (+bwd_pre)", "achieved": achieved,
+                "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16"],
+                "peak_source": "measured live: tcgen05 kind::f16 bf16 M128N256K16 probe (the backward's dense "
+                               "contractions are bf16; its S recompute is FP4)",
+                "kernel_ms": bms, "kernel_share_of_step": bms / ms,
+                "step_frac_of_fp4_peak": value / world / peaks["nvfp4"],
+                "step_frac_of_mixed_ceiling": value / world / (1.17 * peaks["bf16"]),
+                "traffic": _traffic_from_profiles(name)}
+
+    rec = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "nvfp4 (e2m1 + e4m3 block16) / fp32 accum",
+           "data": "synthetic N(0,1) bf16, generated on device",
+           "config": config_dict(name, cfg, world), "tokens_per_s": tokens_s, "roofline": roof,
+           "mma_peaks_tflops": peaks, "heads_per_rank": heads}
+    if not args.no_extras:
+        cmp_ = bf16_comparator(torch, q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0), causal, mode,
+                               d_o.unsqueeze(0) if d_o is not None else None)
+        if cmp_.get("ms"):
+            cms = max_over_ranks(cmp_["ms"])
+            cmp_.update({"ms": cms, "tflops": flops_job / (cms * 1e-3) / 1e12, "ratio": cms / ms_max,
+                         "target_ratio": 1.5 if mode == "fwd" else None})
+        rec["bf16_comparator"] = cmp_
+    if not main_line:
+        rec["clocks"] = clocks
+        return rec
 
     # ---- end to end through the public API with host buffers: pinned host
     # inputs in, host outputs back, every step; the host entry points stream
     # head chunks so H2D, kernels and D2H overlap (paper_2603_00040_b200/host.py)
-    e2e = None
     hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
     if mode == "fwd":
-        ho = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
-        hl = torch.empty(B, H, N, dtype=torch.float32).pin_memory()
+        ho = torch.empty(heads, N, d, dtype=torch.bfloat16).pin_memory()
+        hl = torch.empty(heads, N, dtype=torch.float32).pin_memory()
 
         def e2e_step():
             aq.attn_forward_host(hq, hk, hv, causal=causal, train=False, out=ho, lse_out=hl)
         h2d_b, d2h_b = 3 * q.numel() * 2, ho.numel() * 2 + hl.numel() * 4
     else:
         hdo = d_o.cpu().pin_memory()
-        ho = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
+        ho = torch.empty(heads, N, d, dtype=torch.bfloat16).pin_memory()
         hg = [torch.empty_like(h).pin_memory() for h in (hq, hk, hv)]
 
         def e2e_step():
             aq.attn_qat_host(hq, hk, hv, hdo, causal=causal, out=ho, grads_out=hg)
         h2d_b, d2h_b = 4 * q.numel() * 2, 4 * q.numel() * 2
-    for _ in range(2):
-        e2e_step()
-    barrier()
-    if os.environ.get("AQ_E2E_DEBUG"):
-        for i in range(4):
-            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0 = time.perf_counter()
-            b0.record(st)
-            e2e_step()
-            t1 = time.perf_counter()
-            b1.record(st)
-            barrier()
-            print(f"e2e debug step {i}: {b0.elapsed_time(b1):.2f} ms device, host enqueue {1e3*(t1-t0):.2f} ms",
-                  file=sys.stderr)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
-        evs[0].record(st)
-        for i in range(10):
-            e2e_step()
-            evs[i + 1].record(st)
-        barrier()
-        print("back-to-back:", [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(10)], file=sys.stderr)
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record(st)
-    for _ in range(args.steps):
-        e2e_step()
-    a1.record(st)
-    barrier()
-    ems = a0.elapsed_time(a1) / args.steps
-    et = torch.tensor([ems], device=dev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * flops_rank / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-           "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "ms_per_step": float(et.item()),
-           "api": "attn_forward_host (inference)" if mode == "fwd" else "attn_qat_host (fwd+bwd)",
-           "pcie_gbs": (h2d_b + d2h_b) / (float(et.item()) * 1e-3) / 1e9}
+    ems = max_over_ranks(time_device(torch, e2e_step, args.steps, 2, st, barrier))
+    rec["e2e"] = {"value": flops_job / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+                  "h2d_bytes_per_step": h2d_b * world, "d2h_bytes_per_step": d2h_b * world, "ms_per_step": ems,
+                  "api": "attn_forward_host (inference)" if mode == "fwd" else "attn_qat_host (fwd+bwd)",
+                  "pcie_gbs_per_rank": (h2d_b + d2h_b) / (ems * 1e-3) / 1e9}
 
     # ---- the same inference step serving from a stored FP4 KV cache (kvcache.py):
     # only Q (bf16) and the 4-bit K / V^T cross PCIe; the cache is built once,
     # outside the timed region, like a serving KV cache
-    e2e_kv4 = None
     if mode == "fwd":
         hcache = aq.kv4_quantize(k, v).pin_memory()
-
-        def kv4_step():
-            aq.attn_forward_kv4_host(hq, hcache, causal=causal, out=ho, lse_out=hl)
-        for _ in range(2):
-            kv4_step()
-        barrier()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record(st)
-        for _ in range(args.steps):
-            kv4_step()
-        b1.record(st)
-        barrier()
-        kms = b0.elapsed_time(b1) / args.steps
-        kt_ = torch.tensor([kms], device=dev)
-        if world > 1:
-            dist.all_reduce(kt_, op=dist.ReduceOp.MAX)
-        e2e_kv4 = {"value": world * flops_rank / (float(kt_.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-                   "ms_per_step": float(kt_.item()), "api": "attn_forward_kv4_host (NVFP4 KV cache)",
-                   "h2d_bytes_per_step": q.numel() * 2 + hcache.nbytes(), "d2h_bytes_per_step": d2h_b}
+        kms_ = max_over_ranks(time_device(
+            torch, lambda: aq.attn_forward_kv4_host(hq, hcache, causal=causal, out=ho, lse_out=hl),
+            args.steps, 2, st, barrier))
+        rec["e2e_fp4_kv_cache"] = {"value": flops_job / (kms_ * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                   "ms_per_step": kms_, "api": "attn_forward_kv4_host (NVFP4 KV cache)",
+                                   "h2d_bytes_per_step": (q.numel() * 2 + hcache.nbytes()) * world,
+                                   "d2h_bytes_per_step": d2h_b * world}
+    del hq, hk, hv, ho
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -432,23 +510,23 @@ def main():
         cpu = {"value": v_, "unit": "TFLOP/s", "cores": ref.cores, "kind": "port", "sample": ref.sample(),
                "seconds": dt_}
         ref.close()
+    rec["cpu_baseline"] = cpu
 
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "nvfp4 (e2m1 + e4m3 block16) / fp32 accum",
-            "data": "synthetic N(0,1) bf16, generated on device",
-            "config": {"workload": args.config, "B": B, "H": H, "N": N, "d": d, "causal": causal,
-                       "mode": "inference fwd" if mode == "fwd" else "training fwd+bwd",
-                       "global_batch": world * B, "parallelism": f"dp{world} over B*H (no comms)",
-                       "l2": "inputs larger than L2 (3 x %.0f MB bf16)" % (q.numel() * 2 / 1e6)},
-            "tokens_per_s": tokens_s,
-            "roofline": roof, "mma_peaks_tflops": peaks, "cpu_baseline": cpu, "e2e": e2e, "e2e_fp4_kv_cache": e2e_kv4,
-            "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
-        }), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    # ---- the other BASELINE configs, nested (1 GPU: the tier's largest single-GPU
+    # config C3 and the fwd+bwd half of the metric, C4), each with its own roofline
+    if world == 1 and not args.no_extras and name == "c2":
+        del q, k, v, o, lse, ws
+        torch.cuda.empty_cache()
+        extra = {}
+        for xname in ("c3", "c4"):
+            r = run_attention(args, xname, parse_config(xname), rank, world, local)
+            extra[xname] = {kk: r[kk] for kk in ("value", "unit", "ms_per_step", "tokens_per_s", "config",
+                                                 "roofline", "bf16_comparator", "clocks")}
+            torch.cuda.empty_cache()
+        rec["other_configs"] = extra
+    rec["clocks"] = clocks
+    rec["gpu_launches"] = launches_per_step * args.steps
+    return rec
 
 
 def run_layer_mode(args, cfg, rank, world, local):
@@ -525,9 +603,7 @@ def run_layer_mode(args, cfg, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "nvfp4 attention / bf16 projections / fp32 accum",
             "data": "synthetic N(0,1), generated on device",
-            "config": {"workload": args.config, "B": B, "H": H, "N": N, "d": d, "causal": causal,
-                       "mode": "QAT layer step (proj + attn fwd/bwd + NCCL grad all-reduce + AdamW)",
-                       "global_batch": B, "parallelism": f"dp{world} batch-sharded"},
+            "config": config_dict(args.config, cfg, world),
             "tokens_per_s": B * N / (ms_max * 1e-3),
             "flops_breakdown_per_rank": {"attention_alg": attn, "projections": proj},
             "e2e": {"value": world * (attn + proj) / (float(et.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",

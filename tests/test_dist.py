@@ -87,3 +87,56 @@ def test_make_task_copy_solution():
     X, t = T.make_task(3, 16, 32, 4)
     assert X.shape == (4, 16, 32) and t.shape == (4, 32)
     np.testing.assert_array_equal(X[:, -1], t)
+
+
+def _shard_worker(rank, world, port, out):
+    import importlib.util
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = importlib.util.spec_from_file_location(
+            "bench_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+        bench = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(bench)
+        owned = {}
+        for units in (128, 40, 7, 3, 1):   # C2 B*H, C3 B*H, ragged splits
+            h0, h1 = bench.shard_units(units, rank, world)
+            mine = torch.zeros(units, dtype=torch.int64)
+            mine[h0:h1] = 1
+            dist.all_reduce(mine)          # every head owned by exactly one rank
+            owned[units] = mine.numpy()
+        out[rank] = owned
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_shard_plan_covers_every_head_once_gloo():
+    """bench.py's multi-GPU plan: the named config's B*H heads split contiguously over
+    the ranks, each (b, h) exactly once; world_size 2 over gloo."""
+    world = 2
+    out = mp.Manager().dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for rank in range(world):
+        for units, owned in out[rank].items():
+            assert np.all(owned == 1), (units, owned)
+
+
+def test_bench_shard_plan_all_world_sizes():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for world in (1, 2, 4, 8):
+        for units in (128, 40, 32, 256, 5):
+            spans = [bench.shard_units(units, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == units
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    assert [bench.shard_units(128, r, 8) for r in range(8)][3] == (48, 64)   # C2: 16 heads per GPU
+    assert bench.shard_units(40, 7, 8) == (35, 40)                             # C3: 5 heads per GPU
+    # both arms print the same workload description
+    cfg = bench.parse_config("c2")
+    assert bench.config_dict("c2", cfg, 8) == bench.config_dict("c2", cfg, 8)
+    assert bench.config_dict("c2", cfg, 1)["parallelism"].startswith("dp1")

@@ -145,7 +145,9 @@ def test_nonfinite_batched_path_raises(where):
 @pytest.mark.parametrize("n_q,n_k,d,causal", [(64, 64, 32, False), (32, 64, 16, True), (48, 48, 48, False),
                                               (200, 200, 96, True), (128, 96, 112, False)])
 def test_small_head_dims_vs_oracle(n_q, n_k, d, causal):
-    Q, K, V = orc.make_qkv(11 + d, n_q, n_k, d)
+    # fp32-valued operands: the GPU quantizes fp32, so float64 inputs would be
+    # rounded before quantizing (one E2M1 midpoint straddle moves O by 1e-2 at N=64)
+    Q, K, V = (x.astype(np.float32).astype(np.float64) for x in orc.make_qkv(11 + d, n_q, n_k, d))
     dO = orc.randn((n_q, d), 12 + d)
     cfg = aq.TileConfig(b_q=n_q, b_k=n_k, causal=causal)
     outs = aq.flash_forward_training(Q, K, V, cfg)
@@ -166,7 +168,8 @@ def test_reference_quantized_false_d24_shape():
     cfg = aq.TileConfig(b_q=16, b_k=16)
     outs = aq.flash_forward_training(Q, K, V, cfg, quantized=False)
     O, L, Op = orc.forward_training(Q, K, V, False, 16, 16, 32, quantized=False)
-    assert orc.rel_l2(outs.O, O) <= 2e-3 and np.max(np.abs(outs.L - L)) <= 2e-5
+    # 16-bit tensor-core operands (plain.py): O and L carry fp16 operand rounding
+    assert orc.rel_l2(outs.O, O) <= 2e-3 and np.max(np.abs(outs.L - L)) <= 1e-3
 
 
 # ------------------------------------------------------------------ instrument records
