@@ -20,7 +20,8 @@ from .flash import (AttnGrads, AttnOutputs, BwdVariant, PTileRecord, RowState, T
                     nonfinite_flag, pf_buffers)
 from .kvcache import KV4Cache, attn_forward_kv4, attn_forward_kv4_host, kv4_quantize, load_kv4, save_kv4
 from .materialized import OracleTrace, QuantPoints, oracle_backward, oracle_forward
-from .sage3 import P_RESCALE_MAX, attn_forward_sage3, sage3_forward
+from .sage3 import (P_RESCALE_MAX, ScoreDecomposition, SmoothedPair, TwoLevelP, attn_forward_sage3,
+                    decompose_scores, quantize_p_two_level, sage3_forward, smooth)
 from . import tracking
 from .tensors import Rng, fp4mm, load_quant_tensor, load_tensor, matmul, randn, save_quant_tensor, save_tensor
 

@@ -853,6 +853,11 @@ __device__ __forceinline__ uint32_t e8m0_code(T raw) {  // raw > 0, finite (code
 }
 
 __device__ __forceinline__ float e8m0_value(uint32_t code) { return ldexpf(1.0f, static_cast<int>(code) - 127); }
+// the same value from the exponent bits; code 0 is 2^-127 (an fp32 subnormal),
+// as in the reference (codec.py:123-136), not the 0.0 that code << 23 would give
+__device__ __forceinline__ float e8m0_bits(uint32_t code) {
+  return code ? __int_as_float(static_cast<int>(code << 23)) : __int_as_float(0x00400000);
+}
 
 __global__ void __launch_bounds__(256) quantize_mx_kernel(const void* x, int x_dt, int64_t rows, int64_t cols,
                                                           uint8_t* codes, uint8_t* scales, void* fq, int fq_dt,
@@ -954,7 +959,7 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
     const int64_t rp = t / (D / 32);
     const int64_t h = rp / n_pad, r = rp % n_pad;
     float v[32];
-    if (x_dt == kBF16 && r < n) {  // 4 x 16-byte loads
+    if (x_dt == kBF16 && r < n && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {  // 4 x 16-byte loads
       const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + (h * n + r) * D + b * 32);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
@@ -980,7 +985,7 @@ __global__ void __launch_bounds__(256) mx_rows_tiled_kernel(const void* x, int x
     if (fqh_t) {  // the bf16 fake-quantized operand tile of the backward (T8x8):
       // byte-permute lookups of the E2M1 magnitudes' bf16 bytes, the sign bit
       // from the code, then one exact bf16x2 multiply by the power-of-two scale
-      const __nv_bfloat16 sb = __float2bfloat16_rn(__int_as_float(static_cast<int>(sc << 23)));
+      const __nv_bfloat16 sb = __float2bfloat16_rn(e8m0_bits(sc));
       const __nv_bfloat162 s2 = __halves2bfloat162(sb, sb);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -1029,7 +1034,7 @@ __global__ void __launch_bounds__(256) mx_cols_tiled_kernel(const void* x, int x
         make_uint4(packed[0], packed[1], packed[2], packed[3]);
     sf_t[tile * kSfTileBytesV + sf512_off(c, kt / 32)] = static_cast<uint8_t>(sc);
     if (fqh_t) {  // training: V^F as fp16 T8x8 tiles for the O' MMA (exact: E2M1 x power of two)
-      const float s = __int_as_float(static_cast<int>(sc << 23));
+      const float s = e8m0_bits(sc);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float fv = e2m1_to_f32((packed[j >> 3] >> (4 * (j & 7))) & 0xF) * s;
@@ -1084,7 +1089,7 @@ __global__ void __launch_bounds__(D) mx_cols_slab_kernel(const __nv_bfloat16* __
       uint8_t* dst = pass == 0 ? fqh_t : fqh2_t;
       if (!dst) continue;
       const bool bf = pass == 0 && fqh_bf16;
-      const float s = __int_as_float(static_cast<int>(sc << 23));
+      const float s = e8m0_bits(sc);
       __syncthreads();  // every column has read its tokens / the previous copy is stored
 #pragma unroll
       for (int j = 0; j < 32; ++j) {

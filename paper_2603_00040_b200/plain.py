@@ -41,13 +41,29 @@ def _flash():
 
 
 def _compute_dtype(*ts):
+    """16-bit operand format for float32 Q / K / V: fp16 (11-bit significand)
+    when the largest magnitude sits inside its normal range with headroom
+    (2^-10 <= amax < 6e4), else bf16 (fp32's exponent range). The forward and
+    the backward call this on the same Q / K / V, so they agree."""
     dt = ts[0].dtype
     if dt in (torch.float16, torch.bfloat16):
         return dt
     if dt != torch.float32:
         raise InvalidValue("plain attention takes float32 / bfloat16 / float16 operands")
     amax = max(float(t.abs().max()) for t in ts if t.numel())
-    return torch.float16 if amax < 6.0e4 else torch.bfloat16
+    return torch.float16 if 2.0 ** -10 <= amax < 6.0e4 else torch.bfloat16
+
+
+def _pow2_gain(t, dt, target=2.0 ** 10):
+    """Exact power-of-two gain that moves t's largest magnitude near ``target``
+    when t is cast to fp16 (dO of a mean loss is often far below fp16's normal
+    range); gradients are linear in dO, so dividing them by the gain is exact."""
+    if dt != torch.float16 or t.numel() == 0:
+        return 1.0
+    amax = float(t.abs().max())
+    if not (amax > 0.0) or not math.isfinite(amax):
+        return 1.0
+    return 2.0 ** max(-60, min(60, math.floor(math.log2(target / amax))))
 
 
 def _fa_view(t, dt):
@@ -100,11 +116,14 @@ def plain_forward(q3, k3, v3, causal):
 def plain_backward(q3, k3, v3, do3, o_ref3, lse2, causal, grad_dtype=None):
     """Unquantized attention backward -> (dQ, dK, dV) [heads, n, d] (flash.py:317-390, quantized=False)."""
     fa = _flash()
-    dt = _compute_dtype(q3, k3, v3, do3)
-    q, k, v, do, o = (_fa_view(t, dt) for t in (q3, k3, v3, do3, o_ref3))
+    dt = _compute_dtype(q3, k3, v3)   # the forward's choice (same Q / K / V)
+    gain = _pow2_gain(do3, dt)
+    q, k, v, o = (_fa_view(t, dt) for t in (q3, k3, v3, o_ref3))
+    do = _fa_view(do3 * gain if gain != 1.0 else do3, dt)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     scale = 1.0 / math.sqrt(q3.shape[-1])
     lse = lse2.float().unsqueeze(1).contiguous()
     fa._flash_attn_backward(do, q, k, v, o, lse, dq, dk, dv, 0.0, scale, bool(causal), -1, -1, 0.0, None, True)
     g = grad_dtype or q3.dtype
-    return dq.squeeze(2).to(g), dk.squeeze(2).to(g), dv.squeeze(2).to(g)
+    inv = 1.0 / gain
+    return tuple((t.squeeze(2).float() * inv).to(g) if gain != 1.0 else t.squeeze(2).to(g) for t in (dq, dk, dv))

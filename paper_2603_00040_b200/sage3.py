@@ -26,6 +26,9 @@ in exact arithmetic, sage3.py:117-120) and runs on the plain path.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
+import numpy as np
 import torch
 
 from . import _lib
@@ -34,6 +37,111 @@ from .errors import InvalidValue, ShapeError
 from .flash import AttnOutputs, _check_attention_shapes, _check_cfg, _heads_view, _np_out, _plain_forward
 
 P_RESCALE_MAX = 448.0 * 6.0  # sage3.py:27 (max E4M3 scale x max FP4 value)
+
+
+# ----------------------------------------------------------------------------
+# the reference's composable pieces (sage3.py:30-110), as device ops; NumPy in
+# gives NumPy out. The fused forward below does not call them -- it computes
+# the same quantities inside csrc/sage3.cu and the K4 SAGE instance.
+# ----------------------------------------------------------------------------
+
+@dataclass
+class SmoothedPair:
+    """Token-mean-removed Q and K plus the removed means (sage3.py:30-42):
+    q_bar one mean row per query tile (t_q, d), k_bar the global key mean (d,)."""
+
+    gamma_q: object
+    gamma_k: object
+    q_bar: object
+    k_bar: object
+    b_q: int
+
+
+def _dev64(x):
+    as_np = not isinstance(x, torch.Tensor)
+    t = torch.as_tensor(np.asarray(x)) if as_np else x
+    return t.to("cuda"), as_np
+
+
+def _host_like(t, as_np):
+    return t.cpu().numpy() if as_np else t
+
+
+def smooth(Q, K, b_q):
+    """Subtract token-dimension means: per b_q tile from Q, globally from K
+    (sage3.py:45-60). Means in float64 on the device; gamma keeps the promoted
+    dtype of (input, float64 mean) as NumPy does."""
+    _lib.require_cuda()
+    q, as_np = _dev64(Q)
+    k, _ = _dev64(K)
+    if q.dim() != 2 or k.dim() != 2 or q.shape[1] != k.shape[1]:
+        raise ShapeError("smooth expects 2-D Q and K with matching head dim")
+    if b_q <= 0 or q.shape[0] % b_q:
+        raise ShapeError(f"b_q ({b_q}) must divide N_q ({q.shape[0]})")
+    t_q = q.shape[0] // b_q
+    q_bar = q.reshape(t_q, b_q, -1).to(torch.float64).mean(dim=1)
+    k_bar = k.to(torch.float64).mean(dim=0)
+    gamma_q = q - q_bar.repeat_interleave(b_q, dim=0)
+    gamma_k = k - k_bar
+    return SmoothedPair(gamma_q=_host_like(gamma_q, as_np), gamma_k=_host_like(gamma_k, as_np),
+                        q_bar=_host_like(q_bar, as_np), k_bar=_host_like(k_bar, as_np), b_q=b_q)
+
+
+@dataclass
+class ScoreDecomposition:
+    """S_ij = main + delta_s + bias, exactly in exact arithmetic (sage3.py:63-71)."""
+
+    main: object     # gamma(Q_i) gamma(K_j)^T, the only FP4-bound term
+    delta_s: object  # q_bar_i gamma(K_j)^T, (1, b_k), broadcast down the rows
+    bias: object     # q_bar_i k_bar^T + gamma(Q_i) k_bar^T, (b_q, 1)
+
+    def reconstruct(self):
+        return self.main + self.delta_s + self.bias
+
+
+def decompose_scores(pair, i, j, b_k, accum_width=64):
+    """Score decomposition for query tile i against key tile j (sage3.py:74-88),
+    the products on the device in the accumulation width (tensors.matmul)."""
+    from .tensors import matmul
+    gq = pair.gamma_q[i * pair.b_q:(i + 1) * pair.b_q]
+    gk = pair.gamma_k[j * b_k:(j + 1) * b_k]
+    if min(int(np.prod(gq.shape)), int(np.prod(gk.shape))) == 0:
+        raise ShapeError("tile indices out of range")
+    qb = pair.q_bar[i]
+    main = matmul(gq, gk.T, accum_width)
+    delta_s = matmul(qb[None, :], gk.T, accum_width)
+    bias = matmul(qb[None, :], pair.k_bar[:, None], accum_width) + matmul(gq, pair.k_bar[:, None], accum_width)
+    return ScoreDecomposition(main=main, delta_s=delta_s, bias=bias)
+
+
+@dataclass
+class TwoLevelP:
+    """Row-rescaled quantized probabilities plus the per-row factor (sage3.py:91-95)."""
+
+    codes: object  # QuantTensor of quantize_padded(P * r)
+    row_factor: object
+
+
+def quantize_p_two_level(P_tile, spec=None):
+    """Rescale each row of P onto [0, 448*6], then block-quantize with the GPU
+    codec (sage3.py:98-110); rows of zeros keep factor 1. The scaled tile is
+    rounded to float32 before the codec (codec.to_device), which only matters
+    for values within one fp32 ulp of an E2M1 / E4M3 rounding midpoint."""
+    from .codec import NVFP4, quantize_padded
+    spec = spec or NVFP4
+    _lib.require_cuda()
+    p, as_np = _dev64(P_tile)
+    p = p.to(torch.float64)
+    if p.dim() != 2:
+        raise ShapeError("quantize_p_two_level expects a 2-D tile")
+    if bool((p < 0).any()):
+        raise InvalidValue("two-level quantization expects non-negative P")
+    rowmax = p.max(dim=1).values
+    r = torch.where(rowmax > 0, P_RESCALE_MAX / torch.where(rowmax > 0, rowmax, torch.ones_like(rowmax)),
+                    torch.ones_like(rowmax))
+    scaled = torch.clamp(p * r[:, None], max=P_RESCALE_MAX).to(torch.float32)
+    qt = quantize_padded(scaled.cpu().numpy() if as_np else scaled, spec)
+    return TwoLevelP(codes=qt, row_factor=_host_like(r, as_np))
 
 
 def attn_forward_sage3(q, k, v, causal=False, b_q=128, b_k=128, smooth_q=True, smooth_k=True, two_level_p=True,

@@ -78,8 +78,8 @@ class TrainConfig:
             problems.append(f"batch must be >= 1 and divisible by the world size {world}")
         if self.attn_mode not in ATTN_MODES:
             problems.append(f"attn_mode must be one of {sorted(ATTN_MODES)}")
-        if self.head_dim not in (64, 128):
-            problems.append("head_dim must be 64 or 128 (B200 kernels)")
+        if self.head_dim % 16 or not 0 < self.head_dim <= 128:
+            problems.append("head_dim must be a multiple of 16 up to 128 (B200 kernels; < 128 is zero-padded)")
         if self.d_model % 2:
             problems.append("d_model must be even")
         if self.compute_dtype not in ("bf16", "fp32"):

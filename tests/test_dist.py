@@ -69,7 +69,7 @@ def test_shard_is_contiguous_and_complete():
 
 
 def test_config_validation_lists_problems():
-    bad = T.TrainConfig(steps=0, lr=0, batch=3, head_dim=96, attn_mode="nope")
+    bad = T.TrainConfig(steps=0, lr=0, batch=3, head_dim=40, attn_mode="nope")
     probs = bad.validate(world=2)
     assert len(probs) >= 5
 

@@ -120,3 +120,37 @@ def test_sage3_input_dtypes_agree():
         o, l = aq.attn_forward_sage3(q.to(dt), k.to(dt), v.to(dt), causal=True, b_q=64, b_k=64,
                                      out_dtype=torch.float32)
         assert torch.equal(o, ref[0]) and torch.equal(l, ref[1]), dt
+
+
+def test_sage3_helpers_match_oracle():
+    """smooth / decompose_scores / quantize_p_two_level (sage3.py:45-110) on the
+    device vs the oracle restatement: means and gammas to fp64 rounding, the
+    decomposition reconstructs S, two-level codes byte-identical."""
+    rng = np.random.default_rng(7)
+    Q = rng.standard_normal((256, 64)) + 3.0
+    K = rng.standard_normal((192, 64)) - 1.0
+    pair = aq.smooth(Q, K, 128)
+    gq, gk, qb, kb = orc.smooth(Q, K, 128)
+    for got, want in ((pair.gamma_q, gq), (pair.gamma_k, gk), (pair.q_bar, qb), (pair.k_bar, kb)):
+        assert isinstance(got, np.ndarray) and got.dtype == np.float64
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-13)
+    dec = aq.decompose_scores(pair, 1, 1, 64)
+    assert dec.main.shape == (128, 64) and dec.delta_s.shape == (1, 64) and dec.bias.shape == (128, 1)
+    S = Q[128:256] @ K[64:128].T
+    np.testing.assert_allclose(dec.reconstruct(), S, rtol=0, atol=1e-10)
+    with pytest.raises(aq.ShapeError):
+        aq.decompose_scores(pair, 5, 0, 64)
+    with pytest.raises(aq.ShapeError):
+        aq.smooth(Q, K, 100)
+    # two-level P: a softmax-like tile with a zero row and a ragged width
+    P = np.exp(rng.standard_normal((64, 200)) * 3.0)
+    P /= P.sum(axis=1, keepdims=True)
+    P[5] = 0.0
+    tl = aq.quantize_p_two_level(P)
+    scaled, r = orc.two_level_scale(P)
+    codes, scales = orc.quantize_padded(scaled)
+    np.testing.assert_allclose(tl.row_factor, r, rtol=1e-15)
+    assert tl.row_factor[5] == 1.0
+    assert np.array_equal(np.asarray(tl.codes.codes), codes) and np.array_equal(np.asarray(tl.codes.scales), scales)
+    with pytest.raises(aq.InvalidValue):
+        aq.quantize_p_two_level(-P)
