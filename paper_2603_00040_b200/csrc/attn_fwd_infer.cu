@@ -112,7 +112,8 @@ __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_t
 // MX: the MXFP4 variant (codec.py:123-203) -- S and PV on kind::mxf4 block32
 // with one scale-factor image per 128 K (IDs 0 / 2 per K = 64 step), P in
 // 32-key UE8M0 blocks; same pipeline.
-template <int D, bool MX = false>
+// EARLY: the instance with the pass-2 early-out (long key rows, see launch()).
+template <int D, bool MX = false, bool EARLY = false>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -350,8 +351,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     }
   } else {
     // ------------------------------------------------------------ softmax groups
-    const bool grp_a = warp < C::WB;
-    const int gw = grp_a ? warp : warp - C::WB;      // warp within its group
+    const bool grp_a = warp >= C::WA && warp < C::WA + C::NSW;
+    const int gw = grp_a ? warp - C::WA : warp - C::WB;  // warp within its group
     const int row = 32 * (gw & 3) + lane;            // TMEM lane == query row
     const int half = gw >> 2;
     constexpr int CW = C::CW;
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     float x[CW];
     int su = 0, pc = 0, k = 0;
     int chk_wait = 0, chk_pen = 0;  // early-out back-off (warp-uniform)
-    const bool early_out = (p.debug & 64) == 0;  // AQ_FWD_DEBUG bit 64 disables it (A/B timing)
+    const bool early_out = EARLY && (p.debug & 64) == 0;  // AQ_FWD_DEBUG bit 64 disables it (A/B timing)
     float* ml = reinterpret_cast<float*>(smem + C::ML);
     float* lb = reinterpret_cast<float*>(smem + C::LB);
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
@@ -623,10 +624,18 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   }
 }
 
+#ifndef AQ_FWDI_EARLY_NK
+#define AQ_FWDI_EARLY_NK 24576
+#endif
 template <int D, bool MX = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   using C = Cfg<D>;
-  auto kern = attn_fwd_infer_kernel<D, MX>;
+  // The early-out pays where long rows push most P blocks below 2^-11 (C3
+  // N = 32760: 75 % of warp blocks, 23.9 -> 20.0 ms; N = 32K causal 19.3 ->
+  // 18.8 ms); for shorter rows its code costs more than it skips (C2 N = 8192
+  // causal 2.63 -> 2.77 ms, N = 16K non-causal 19.0 -> 19.8 ms), so those run
+  // the instance without it. Both give identical bits.
+  auto kern = (!MX && p.n_k >= AQ_FWDI_EARLY_NK) ? attn_fwd_infer_kernel<D, MX, !MX> : attn_fwd_infer_kernel<D, MX, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;

@@ -25,6 +25,10 @@ __global__ void k(float* out, float a, float b, long long* clk) {
       if (OP == 5) u[i] = (u[i] << 23) + u[(i + 1) & 7];                                 // LEA-ish
       if (OP == 6) { uint16_t c; asm volatile("{.reg .b8 t; cvt.rn.satfinite.e2m1x2.f32 t, %1, %2; cvt.u16.u8 %0, t;}" : "=h"(c) : "f"(x[i]), "f"(a)); x[i] = __int_as_float(c | 0x3f800000u); }
       if (OP == 7) x[i] = fmaf(x[i], 1.0001f, 0.5f);                                     // FFMA imm
+      if (OP == 8) { uint32_t r; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(u[i])); u[i] = r; }  // 2x MUFU.EX2.F16
+      if (OP == 9) { uint32_t r; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(u[i])); u[i] = r; }
+      if (OP == 10) { float r; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x[i])); x[i] = r; }
+      if (OP == 11) { uint16_t r; asm volatile("ex2.approx.f16 %0, %1;" : "=h"(r) : "h"((uint16_t)u[i])); u[i] = r; }
     }
   }
   long long t1 = clock64();
@@ -48,5 +52,6 @@ int main() {
   for (int w : {8, 16, 32}) {
     run<0>("FFMA", w); run<7>("FFMAimm", w); run<1>("FFMA2", w); run<2>("FADD2", w); run<3>("FMNMX", w);
     run<4>("MUFUEX2", w); run<5>("SHL+ADD", w); run<6>("F2FPe2m1", w);
+    run<8>("EX2f16x2", w); run<9>("EX2bf16x2", w); run<10>("RCP", w); run<11>("EX2f16", w);
   }
 }
