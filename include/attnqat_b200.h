@@ -156,7 +156,8 @@ int aq_attn_fwd_mx(const AqFwdArgs* args, void* stream);
  * kernel skeleton with 16-bit operands (fmt 0 = fp16, 1 = bf16; inputs are
  * converted), S and P^ V on kind::f16 MMAs with fp32 accumulation. Writes O
  * (args->o) and L; args->train / o_hp / keep_for_bwd / operands_staged are
- * ignored. Workspace: aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 1, 1). */
+ * ignored, and of the scale fields only softmax_scale (0 = 1/sqrt(d)).
+ * Workspace: aq_attn_fwd_workspace_bytes(heads, n_q, n_k, d, 1, 1). */
 int aq_attn_fwd_plain(const AqFwdArgs* args, int fmt, void* stream);
 
 /* FP4 KV cache: inference forward (flash_forward_inference, flash.py:249-314)
@@ -229,6 +230,14 @@ int aq_attn_bwd(const AqBwdArgs* args, void* stream);
  * re-quantized from args->q / k / v, or taken from args->fwd_workspace (an
  * aq_attn_fwd_mx workspace with keep_for_bwd = 1); d % 32 == 0. */
 int aq_attn_bwd_mx(const AqBwdArgs* args, void* stream);
+/* quantized=False backward (flash_backward with quantized=False,
+ * flash.py:344-349 -- every variant reduces to it): the K7 skeleton with S
+ * recomputed from bf16 Q / K tiles on kind::f16, P = exp(S - L) unquantized,
+ * D = rowsum(dO . O) with O = args->o_hp if set, else args->o (O' == O here).
+ * bf16 operands, fp32 accumulation; only softmax_scale of the scale fields is
+ * honoured (the others must be 0 / 1); fwd_workspace and pf_* are ignored.
+ * Workspace: aq_attn_bwd_workspace_bytes(). */
+int aq_attn_bwd_plain(const AqBwdArgs* args, void* stream);
 
 /* ---- measurement utilities (bench.py roofline denominators) ---------------
  * One CTA per SM issuing back-to-back tcgen05 MMAs from shared memory:

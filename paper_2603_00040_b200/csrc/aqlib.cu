@@ -564,13 +564,15 @@ int aq_attn_fwd_plain(const AqFwdArgs* a, int fmt, void* stream) {
   p.causal = a->causal;
   p.train = 1;
   p.plain_fmt = fmt;
+  TScales ts;
+  if (!read_scales(a, ts) || ts.q != 1.f || ts.k != 1.f || ts.v != 1.f || ts.p != 1.f) return AQ_E_INVALID;
   {
     // d = 128: the 16-bit K / V stream is HBM-bound in the global longest-first
     // order (22 GB read at C2); groups of 4 heads keep it in L2 (4.77 -> 4.15 ms)
     const char* e = std::getenv("AQ_PLAIN_HEAD_GROUP");
     p.head_group = e ? std::atoi(e) : (d == 128 ? 4 : 0);
   }
-  p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  p.scale_log2 = scale_log2_of(ts, a->d);
   return cuda_status(launch_attn_fwd_plain(p, st));
 }
 
@@ -619,6 +621,56 @@ static int attn_bwd_impl(const AqBwdArgs* a, void* stream, bool mx);
 int aq_attn_bwd(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stream, false); }
 
 int aq_attn_bwd_mx(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stream, true); }
+
+int aq_attn_bwd_plain(const AqBwdArgs* a, void* stream) {
+  if (!a || !a->q || !a->k || !a->v || !a->d_o || !a->lse || !a->dq || !a->dk || !a->dv || !a->workspace)
+    return AQ_E_INVALID;
+  if (!dtype_ok(a->in_dtype) || !dtype_ok(a->do_dtype) || !dtype_ok(a->o_dtype) || !dtype_ok(a->g_dtype))
+    return AQ_E_INVALID;
+  const void* o_ref = a->o_hp ? a->o_hp : a->o;  // O' == O without quantization (flash.py:195-200)
+  if (!o_ref) return AQ_E_INVALID;
+  if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
+  if (a->d != 64 && a->d != 128) return AQ_E_UNSUPPORTED;
+  if (a->causal && a->n_q > a->n_k) return AQ_E_SHAPE;
+  TScales ts;
+  if (!read_scales(a, ts) || ts.q != 1.f || ts.k != 1.f || ts.v != 1.f || ts.p != 1.f) return AQ_E_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const BwdWs bw = bwd_ws(a->heads, a->n_q, a->n_k, a->d);
+  const FwdWs fw = fwd_ws(a->heads, a->n_q, a->n_k, a->d, 0, 1);
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  uint8_t* b = ws + bw.fwd;
+  const int d = static_cast<int>(a->d);
+  // bf16 T8x8 tiles of Q / K / V (one copy serves K- and MN-major reads)
+  if (launch_tile16(a->q, a->in_dtype, a->heads, a->n_q, d, 1, b + fw.q_hb, st) != cudaSuccess ||
+      launch_tile16(a->k, a->in_dtype, a->heads, a->n_k, d, 1, b + fw.k_hb, st) != cudaSuccess ||
+      launch_tile16(a->v, a->in_dtype, a->heads, a->n_k, d, 1, b + fw.v_hb, st) != cudaSuccess)
+    return AQ_E_CUDA;
+  float* delta = reinterpret_cast<float*>(ws + bw.delta);
+  if (launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, d, delta, ws + bw.do_h, st, 1.f) !=
+      cudaSuccess)
+    return AQ_E_CUDA;
+  BwdParams p{};
+  p.q_h = b + fw.q_hb;
+  p.k_h = b + fw.k_hb;
+  p.v_h = b + fw.v_hb;
+  p.do_h = ws + bw.do_h;
+  p.lse = a->lse;
+  p.delta = delta;
+  p.dq = a->dq;
+  p.dk = a->dk;
+  p.dv = a->dv;
+  p.g_dt = a->g_dtype;
+  p.heads = a->heads;
+  p.n_q = a->n_q;
+  p.n_k = a->n_k;
+  p.d = d;
+  p.causal = a->causal;
+  p.fq_p = 0;
+  p.plain = 1;
+  p.scale_log2 = scale_log2_of(ts, a->d);
+  p.inv_sqrt_d = static_cast<float>(ts.sm == 0.0 ? 1.0 / std::sqrt(static_cast<double>(a->d)) : ts.sm);
+  return cuda_status(launch_attn_bwd(p, st));
+}
 
 }  // extern "C"
 

@@ -83,6 +83,7 @@ struct BwdParams {
   int causal;
   int fq_p;              // quantize the recomputed P for dV
   int mx;                // MXFP4: S on kind::mxf4 block32, P^F in 32-key UE8M0 blocks
+  int plain = 0;         // quantized=False: S on kind::f16 from bf16 Q / K tiles (q_h / k_h), P unquantized
   float scale_log2;      // log2(e)/sqrt(d) (times t_q t_k)
   float inv_sqrt_d;      // 1/sqrt(d) (times t_v: dS = P (t_v dP - D) / sqrt(d), D pre-divided by t_v)
   float p_r = 1.f;       // 1 / t_p: P^F quantized as P * p_r (1 = reference semantics)

@@ -131,16 +131,21 @@ __device__ __forceinline__ void store_ds(uint8_t* ds_h, int row, int kb, const f
 }
 
 // ============================================================================ K7a: dK, dV
-template <int D>
+// PLAIN (quantized=False, flash.py:344-349): S from 16-bit Q / K tiles on
+// kind::f16; the Q ring then carries bf16 Q tiles that serve both S and dK
+// (no separate Q^F stage) and the stationary K is a bf16 tile; one dO stage
+// keeps the layout inside 227 KB.
+template <int D, bool PLAIN = false>
 struct KvSmem {
-  static constexpr int K_CODES = 0;
+  static constexpr int K_CODES = 0;                                // FP4 K (bf16 K tile for PLAIN)
   static constexpr int K_SF = K_CODES + TILE * D / 2;
-  static constexpr int V_H = K_SF + (D / 64) * 512;
-  static constexpr int QC0 = V_H + TILE * D * 2;                  // Q codes + SF, 2 stages
-  static constexpr int QC_BYTES = TILE * D / 2 + (D / 64) * 512;
-  static constexpr int Q_H = QC0 + 2 * QC_BYTES;                  // Q^F, 1 stage
-  static constexpr int DO_H0 = Q_H + TILE * D * 2;                // dO, 2 stages
-  static constexpr int P_H = DO_H0 + 2 * TILE * D * 2;            // P^F bf16 [query][key]
+  static constexpr int V_H = PLAIN ? TILE * D * 2 : K_SF + (D / 64) * 512;
+  static constexpr int QC0 = V_H + TILE * D * 2;                  // Q codes + SF (bf16 Q for PLAIN), 2 stages
+  static constexpr int QC_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + (D / 64) * 512;
+  static constexpr int Q_H = QC0 + 2 * QC_BYTES;                  // Q^F, 1 stage (none for PLAIN)
+  static constexpr int NDO = PLAIN ? 1 : 2;
+  static constexpr int DO_H0 = Q_H + (PLAIN ? 0 : TILE * D * 2);   // dO, NDO stages
+  static constexpr int P_H = DO_H0 + NDO * TILE * D * 2;          // P^F bf16 [query][key]
   static constexpr int DS_H = P_H + TILE * TILE * 2;               // dS bf16 [query][key]
   static constexpr int BARS = DS_H + TILE * TILE * 2;
   static constexpr int NUM_BARS = 24;
@@ -163,9 +168,10 @@ enum KvBar {
 //   dP_i half 0 | S_{i+1} | dP_i half 1 | dV_i (once P^F_i is in SMEM) | dK_i (once dS_i is)
 // so S_{i+1} runs while the compute warps are still on tile i, and the Q
 // codes / dO / Q^F rings are released by the MMA that last reads them.
-template <int D, bool MX>
+template <int D, bool MX, bool PLAIN>
 __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head) {
-  using L = KvSmem<D>;
+  using L = KvSmem<D, PLAIN>;
+  constexpr int NDO = L::NDO;
   constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
   constexpr int PRODUCER = Cfg<D>::PRODUCER, MMA = Cfg<D>::MMA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BARS);
@@ -209,15 +215,24 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     // the stationary K / V^F tiles and the first query tile are requested
     // before the CTA-wide sync, so their latency overlaps TMEM allocation.
     // K (first S) and V^F (first dP) on separate barriers.
-    mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
-    bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
-    bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
+    if (PLAIN) {
+      mbar_expect_tx(&bars[KV_B_K], TILE * D * 2);
+      bulk_g2s(smem + L::K_CODES, p.k_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_K]);
+    } else {
+      mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
+      bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
+      bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
+    }
     if (ni > 0) {
       const int64_t qidx = head * q_tiles + i_begin;
       mbar_expect_tx(&bars[KV_B_QC_FULL], L::QC_BYTES);
-      bulk_g2s(smem + L::QC0, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_QC_FULL]);
-      bulk_g2s(smem + L::QC0 + TILE * D / 2, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512,
-               &bars[KV_B_QC_FULL]);
+      if (PLAIN) {
+        bulk_g2s(smem + L::QC0, p.q_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_QC_FULL]);
+      } else {
+        bulk_g2s(smem + L::QC0, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_QC_FULL]);
+        bulk_g2s(smem + L::QC0 + TILE * D / 2, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512,
+                 &bars[KV_B_QC_FULL]);
+      }
     }
     mbar_expect_tx(&bars[KV_B_V], TILE * D * 2);
     bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_V]);
@@ -243,14 +258,18 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       if (elect_one()) {
         uint8_t* dst = smem + L::QC0 + s * L::QC_BYTES;
         mbar_expect_tx(&bars[KV_B_QC_FULL + s], L::QC_BYTES);
-        bulk_g2s(dst, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_QC_FULL + s]);
-        bulk_g2s(dst + TILE * D / 2, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_QC_FULL + s]);
+        if (PLAIN) {
+          bulk_g2s(dst, p.q_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_QC_FULL + s]);
+        } else {
+          bulk_g2s(dst, p.q_codes + qidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_QC_FULL + s]);
+          bulk_g2s(dst + TILE * D / 2, p.q_sf + qidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_QC_FULL + s]);
+        }
       }
       __syncwarp();
     };
     auto load_do = [&](int t) {
-      const int s = t & 1;
-      if (t >= 2) mbar_wait(&bars[KV_B_DO_EMPTY + s], ((t >> 1) - 1) & 1);
+      const int s = t % NDO;
+      if (t >= NDO) mbar_wait(&bars[KV_B_DO_EMPTY + s], ((t / NDO) - 1) & 1);
       const int64_t qidx = head * q_tiles + i_begin + t;
       if (elect_one()) {
         mbar_expect_tx(&bars[KV_B_DO_FULL + s], TILE * D * 2);
@@ -264,6 +283,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
         load_qc(t + 1);
         load_do(t + 1);
       }
+      if (PLAIN) continue;  // the Q ring slot is the dK operand too
       if (t > 0) mbar_wait(&bars[KV_B_QH_EMPTY], (t - 1) & 1);
       const int64_t qidx = head * q_tiles + i_begin + t;
       if (elect_one()) {
@@ -275,6 +295,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   } else if (warp == MMA) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
+    constexpr uint32_t id_s16 = idesc_f16(128, 128, 1, 0, 0);  // PLAIN: Q (K-major) x K (K-major), bf16
     constexpr uint32_t id_dp = idesc_f16(128, HALF, 1, 0, 0);  // dO (K-major) x V^F half (K-major)
     constexpr uint32_t id_kv = idesc_f16(128, D, 1, 1, 1);     // P^F^T / dS^T (MN) x dO / Q^F (MN)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);        // FP4 codes, K-major T8x32
@@ -292,7 +313,11 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       tc_fence_after();
       if (elect_one()) {
         // S = Q K^T (FP4, same instruction sequence as the forward)
-        if constexpr (MX) {
+        if constexpr (PLAIN) {
+          for (int ks = 0; ks < D / 16; ++ks)
+            mma_f16_ss(tmem + KV_T_S, desc_at(t_kmaj, qc + ks * 4096), desc_at(t_kmaj, k_codes + ks * 4096), id_s16,
+                       ks > 0);
+        } else if constexpr (MX) {
           tmem_cp_32x128_x4(tmem + KV_T_QSF, desc_at(t_sf, qc + TILE * D / 2));
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint32_t sid = 2u * ks;
@@ -308,7 +333,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
                         tmem + KV_T_QSF + 4 * ks, tmem + KV_T_KSF + 4 * ks, ks > 0);
         }
         tc_commit(&bars[KV_B_S_FULL]);
-        tc_commit(&bars[KV_B_QC_EMPTY + s]);
+        if (!PLAIN) tc_commit(&bars[KV_B_QC_EMPTY + s]);  // PLAIN: released by dK
       }
       __syncwarp();
     };
@@ -324,7 +349,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     };
     mbar_wait(&bars[KV_B_K], 0);
     tc_fence_after();
-    if (elect_one()) {
+    if (!PLAIN && elect_one()) {
       for (int ks = 0; ks < D / 64; ++ks)
         tmem_cp_32x128_x4(tmem + KV_T_KSF + 4 * ks, desc_at(t_sf, s0 + L::K_SF + ks * 512));
     }
@@ -332,10 +357,10 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     if (ni > 0) issue_s(0);
     for (int ii = 0; ii < ni; ++ii) {
       const uint32_t ph = ii & 1;
-      const int s = ii & 1;
+      const int s = ii % NDO;
       const uint32_t do_h = s0 + L::DO_H0 + s * TILE * D * 2;
       // dP = dO V^F^T, one 64-key half at a time, with S_{i+1} in between
-      mbar_wait(&bars[KV_B_DO_FULL + s], (ii >> 1) & 1);
+      mbar_wait(&bars[KV_B_DO_FULL + s], (ii / NDO) & 1);
       if (ii > 0) mbar_wait(&bars[KV_B_DP_EMPTY + 1], ph ^ 1);
       else mbar_wait(&bars[KV_B_V], 0);
       issue_dp(ii, 0, do_h);
@@ -353,16 +378,17 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
         tc_commit(&bars[KV_B_DO_EMPTY + s]);
       }
       __syncwarp();
-      // dK += dS^T Q^F
+      // dK += dS^T Q^F (PLAIN: Q from its ring slot, already waited for by S_i)
       mbar_wait(&bars[KV_B_DS_FULL], ph);
-      mbar_wait(&bars[KV_B_QH_FULL], ph);
+      if (!PLAIN) mbar_wait(&bars[KV_B_QH_FULL], ph);
       tc_fence_after();
       if (elect_one()) {
+        const uint32_t qf = PLAIN ? s0 + L::QC0 + (ii & 1) * L::QC_BYTES : q_h;
         for (int ks = 0; ks < TILE / 16; ++ks)
-          mma_f16_ss(tmem + KV_T_DK, desc_at(t_mn, ds_h + ks * 256), desc_at(t_mn, q_h + ks * 256), id_kv,
+          mma_f16_ss(tmem + KV_T_DK, desc_at(t_mn, ds_h + ks * 256), desc_at(t_mn, qf + ks * 256), id_kv,
                      (ii > 0 || ks > 0));
         tc_commit(&bars[KV_B_DS_FREE]);
-        tc_commit(&bars[KV_B_QH_EMPTY]);
+        tc_commit(&bars[PLAIN ? KV_B_QC_EMPTY + (ii & 1) : KV_B_QH_EMPTY]);
       }
       __syncwarp();
     }
@@ -416,7 +442,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       if (ii > 0) mbar_wait(&bars[KV_B_PF_FREE], (ii - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       // P^F (or P) -> bf16 [query][key] T8x8
-      if (MX && p.fq_p) {  // MXFP4 P^F: 32-key UE8M0 blocks, dequantized exactly to bf16
+      if (!PLAIN && MX && p.fq_p) {  // MXFP4 P^F: 32-key UE8M0 blocks, dequantized exactly to bf16
 #pragma unroll
         for (int b32 = 0; b32 < KPT / 32; ++b32) {
           uint32_t cd[4], sc;
@@ -443,11 +469,11 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
           }
         }
       }
-if (!(MX && p.fq_p)) {
+if (PLAIN || !(MX && p.fq_p)) {
 #pragma unroll
       for (int blk = 0; blk < KPT / 16; ++blk) {
         uint4 w[2];
-        if (p.fq_p) {
+        if (!PLAIN && p.fq_p) {
           const PBlock qb = quantize_p16_s(pr + blk * 16, p.p_r);
           if (p.pf_codes != nullptr && qvalid) {  // instrument (flash.py:386-387): the recomputed P^F
             const int64_t n16 = ceil_div(p.n_k, 16);
@@ -540,18 +566,20 @@ if (!(MX && p.fq_p)) {
 }
 
 // ============================================================================ K7b: dQ
-template <int D>
+// PLAIN: bf16 Q tile stationary; the K ring carries bf16 K tiles that serve S
+// and dQ (no separate K^F ring).
+template <int D, bool PLAIN = false>
 struct QSmem {
-  static constexpr int Q_CODES = 0;
+  static constexpr int Q_CODES = 0;                                  // FP4 Q (bf16 Q tile for PLAIN)
   static constexpr int Q_SF = Q_CODES + TILE * D / 2;
-  static constexpr int DO_H = Q_SF + (D / 64) * 512;
+  static constexpr int DO_H = PLAIN ? TILE * D * 2 : Q_SF + (D / 64) * 512;
   // per-operand rings over key tiles, each released by the MMA that last reads it:
   // K codes + scale factors (S), V^F (dP), K^F (dQ)
-  static constexpr int KC_BYTES = TILE * D / 2 + (D / 64) * 512;
+  static constexpr int KC_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + (D / 64) * 512;
   static constexpr int KC0 = DO_H + TILE * D * 2;
   static constexpr int VH0 = KC0 + 2 * KC_BYTES;
   static constexpr int KH0 = VH0 + 2 * TILE * D * 2;
-  static constexpr int DS_H = KH0 + 2 * TILE * D * 2;               // dS bf16 [query][key]
+  static constexpr int DS_H = KH0 + (PLAIN ? 0 : 2 * TILE * D * 2);  // dS bf16 [query][key]
   static constexpr int BARS = DS_H + TILE * TILE * 2;
   static constexpr int NUM_BARS = 24;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
@@ -571,9 +599,9 @@ enum QBar {
 
 // MMA issue order: S_0 dP_0 | S_1 dP_1 dQ_0 | S_2 dP_2 dQ_1 | ... so S_{j+1} and
 // dP_{j+1} run while the compute warps turn S_j / dP_j into dS_j.
-template <int D, bool MX>
+template <int D, bool MX, bool PLAIN>
 __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, int qt, int64_t head) {
-  using L = QSmem<D>;
+  using L = QSmem<D, PLAIN>;
   constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
   constexpr int PRODUCER = Cfg<D>::PRODUCER, MMA = Cfg<D>::MMA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BARS);
@@ -611,15 +639,24 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     mbar_init(&bars[Q_B_DONE], 1);
     fence_mbar_init();
     // stationary Q codes / dO and key tile 0 requested before the CTA-wide sync
-    mbar_expect_tx(&bars[Q_B_Q], TILE * D / 2 + (D / 64) * 512);
-    bulk_g2s(smem + L::Q_CODES, p.q_codes + qidx0 * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_Q]);
-    bulk_g2s(smem + L::Q_SF, p.q_sf + qidx0 * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_Q]);
+    if (PLAIN) {
+      mbar_expect_tx(&bars[Q_B_Q], TILE * D * 2);
+      bulk_g2s(smem + L::Q_CODES, p.q_h + qidx0 * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_Q]);
+    } else {
+      mbar_expect_tx(&bars[Q_B_Q], TILE * D / 2 + (D / 64) * 512);
+      bulk_g2s(smem + L::Q_CODES, p.q_codes + qidx0 * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_Q]);
+      bulk_g2s(smem + L::Q_SF, p.q_sf + qidx0 * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_Q]);
+    }
     if (nt > 0) {
       const int64_t kidx = head * k_tiles;
       mbar_expect_tx(&bars[Q_B_KC_FULL], L::KC_BYTES);
-      bulk_g2s(smem + L::KC0, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL]);
-      bulk_g2s(smem + L::KC0 + TILE * D / 2, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512,
-               &bars[Q_B_KC_FULL]);
+      if (PLAIN) {
+        bulk_g2s(smem + L::KC0, p.k_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_KC_FULL]);
+      } else {
+        bulk_g2s(smem + L::KC0, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL]);
+        bulk_g2s(smem + L::KC0 + TILE * D / 2, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512,
+                 &bars[Q_B_KC_FULL]);
+      }
     }
     mbar_expect_tx(&bars[Q_B_DOH], TILE * D * 2);
     bulk_g2s(smem + L::DO_H, p.do_h + qidx0 * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_DOH]);
@@ -641,8 +678,12 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       if (j > 0 && elect_one()) {
         uint8_t* dst = smem + L::KC0 + st * L::KC_BYTES;
         mbar_expect_tx(&bars[Q_B_KC_FULL + st], L::KC_BYTES);
-        bulk_g2s(dst, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL + st]);
-        bulk_g2s(dst + TILE * D / 2, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_KC_FULL + st]);
+        if (PLAIN) {
+          bulk_g2s(dst, p.k_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[Q_B_KC_FULL + st]);
+        } else {
+          bulk_g2s(dst, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[Q_B_KC_FULL + st]);
+          bulk_g2s(dst + TILE * D / 2, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[Q_B_KC_FULL + st]);
+        }
       }
       __syncwarp();
       if (j >= 2) mbar_wait(&bars[Q_B_VH_EMPTY + st], pe);
@@ -652,6 +693,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
                  &bars[Q_B_VH_FULL + st]);
       }
       __syncwarp();
+      if (PLAIN) continue;  // the K ring slot is the dQ operand too
       if (j >= 2) mbar_wait(&bars[Q_B_KH_EMPTY + st], pe);
       if (elect_one()) {
         mbar_expect_tx(&bars[Q_B_KH_FULL + st], TILE * D * 2);
@@ -663,6 +705,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
   } else if (warp == MMA) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
+    constexpr uint32_t id_s16 = idesc_f16(128, 128, 1, 0, 0);  // PLAIN: Q (K-major) x K (K-major), bf16
     constexpr uint32_t id_dp = idesc_f16(128, 128, 1, 0, 0);  // dO (K-major) x V^F (K-major)
     constexpr uint32_t id_dq = idesc_f16(128, D, 1, 0, 1);    // dS (K-major) x K^F (MN-major)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);
@@ -673,7 +716,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     const uint32_t q_codes = s0 + L::Q_CODES, do_h = s0 + L::DO_H, ds_h = s0 + L::DS_H;
     mbar_wait(&bars[Q_B_Q], 0);
     tc_fence_after();
-    if (elect_one()) {
+    if (!PLAIN && elect_one()) {
       for (int ks = 0; ks < D / 64; ++ks)
         tmem_cp_32x128_x4(tmem + Q_T_QSF + 4 * ks, desc_at(t_sf, s0 + L::Q_SF + ks * 512));
     }
@@ -686,7 +729,11 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       if (j > 0) mbar_wait(&bars[Q_B_S_EMPTY], (j - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        if constexpr (MX) {
+        if constexpr (PLAIN) {
+          for (int ks = 0; ks < D / 16; ++ks)
+            mma_f16_ss(tmem + Q_T_S, desc_at(t_kmaj, q_codes + ks * 4096), desc_at(t_kmaj, kc + ks * 4096), id_s16,
+                       ks > 0);
+        } else if constexpr (MX) {
           tmem_cp_32x128_x4(tmem + Q_T_KSF + 8 * st, desc_at(t_sf, kc + TILE * D / 2));
           for (int ks = 0; ks < D / 64; ++ks) {
             const uint32_t sid = 2u * ks;
@@ -702,7 +749,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
                         tmem + Q_T_QSF + 4 * ks, tmem + Q_T_KSF + 8 * st + 4 * ks, ks > 0);
         }
         tc_commit(&bars[Q_B_S_FULL]);
-        tc_commit(&bars[Q_B_KC_EMPTY + st]);
+        if (!PLAIN) tc_commit(&bars[Q_B_KC_EMPTY + st]);  // PLAIN: released by dQ
       }
       __syncwarp();
       mbar_wait(&bars[Q_B_VH_FULL + st], pf);
@@ -723,15 +770,15 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       if (j + 1 < nt) issue_s_dp(j + 1);
       const int st = j & 1;
       mbar_wait(&bars[Q_B_DS_FULL], j & 1);
-      mbar_wait(&bars[Q_B_KH_FULL + st], (j >> 1) & 1);
+      if (!PLAIN) mbar_wait(&bars[Q_B_KH_FULL + st], (j >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t kh = s0 + L::KH0 + st * TILE * D * 2;
+        const uint32_t kh = PLAIN ? s0 + L::KC0 + st * L::KC_BYTES : s0 + L::KH0 + st * TILE * D * 2;
         for (int ks = 0; ks < TILE / 16; ++ks)
           mma_f16_ss(tmem + Q_T_DQ, desc_at(t_kmaj, ds_h + ks * 4096), desc_at(t_mn, kh + ks * 256), id_dq,
                      (j > 0 || ks > 0));
         tc_commit(&bars[Q_B_DS_EMPTY]);
-        tc_commit(&bars[Q_B_KH_EMPTY + st]);
+        tc_commit(&bars[PLAIN ? Q_B_KC_EMPTY + st : Q_B_KH_EMPTY + st]);
       }
       __syncwarp();
     }
@@ -816,7 +863,8 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 // is 18% slower at C4); KV and Q items share no barriers.
 // MX: the MXFP4 instance (S recomputed on kind::mxf4 block32, P^F in 32-key
 // UE8M0 blocks dequantized exactly to bf16; everything else is shared).
-template <int D, bool MX>
+// PLAIN: quantized=False (16-bit S recompute, P unquantized; flash.py:344-349).
+template <int D, bool MX, bool PLAIN = false>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t head = blockIdx.y;
@@ -831,8 +879,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
   } else {
     qt = q_tiles - 1 - (r - m);
   }
-  if (kv >= 0) bwd_kv_tile<D, MX>(p, smem, kv, head);
-  else bwd_q_tile<D, MX>(p, smem, qt, head);
+  if (kv >= 0) bwd_kv_tile<D, MX, PLAIN>(p, smem, kv, head);
+  else bwd_q_tile<D, MX, PLAIN>(p, smem, qt, head);
 }
 
 // K6: D = rowsum(dO . O_ref) (fp32) and dO -> bf16 T8x8 tiles (pad rows zero).
@@ -909,8 +957,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt
 
 template <int D>
 cudaError_t launch(const BwdParams& p, cudaStream_t st) {
-  auto kern = p.mx ? attn_bwd_kernel<D, true> : attn_bwd_kernel<D, false>;
-  constexpr int smem = KvSmem<D>::TOTAL > QSmem<D>::TOTAL ? KvSmem<D>::TOTAL : QSmem<D>::TOTAL;
+  auto kern = p.plain ? attn_bwd_kernel<D, false, true> : p.mx ? attn_bwd_kernel<D, true> : attn_bwd_kernel<D, false>;
+  constexpr int smem_q = KvSmem<D>::TOTAL > QSmem<D>::TOTAL ? KvSmem<D>::TOTAL : QSmem<D>::TOTAL;
+  constexpr int smem_p = KvSmem<D, true>::TOTAL > QSmem<D, true>::TOTAL ? KvSmem<D, true>::TOTAL : QSmem<D, true>::TOTAL;
+  const int smem = p.plain ? smem_p : smem_q;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int kv_tiles = static_cast<int>(ceil_div(p.n_k, TILE)), q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
