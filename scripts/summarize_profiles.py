@@ -28,19 +28,21 @@ def launches(name):
 
 
 summary = {}
-for cfg in ("c2", "c4"):
+for cfg in ("c2", "c3", "c4"):
+    if not os.path.exists(os.path.join(SRC, f"launches_{cfg}.csv")):
+        continue
     ls = launches(cfg)
     with open(os.path.join(DST, f"{TAG}_launches_{cfg}.txt"), "w") as fh:
         fh.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none, bench.py --config {cfg} "
                  "--steps 2 --warmup 3 (cold-cache, serialised launches)\n")
         ours = [(k, t) for k, t in ls if any(s in k for s in ("attn_", "quantize", "bwd_pre", "dq_convert"))]
-        per_step = {"c2": 4, "c4": 6}[cfg]
+        per_step = {"c2": 4, "c3": 4, "c4": 6}[cfg]
         # the full-size timed step: the launches ending at the longest attention launch
         # (later, shorter launches are the host-pipelined e2e chunks)
         # (a full step starts with the quantizers; the roofline loop re-runs the attention kernel alone)
         cand = [i for i in range(per_step - 1, len(ours)) if "attn_" in ours[i][0]
                 and "quantize" in ours[i - per_step + 1][0]
-                and sum("attn_" in ours[j][0] for j in range(i - per_step + 1, i + 1)) == {"c2": 1, "c4": 2}[cfg]]
+                and sum("attn_" in ours[j][0] for j in range(i - per_step + 1, i + 1)) == {"c2": 1, "c3": 1, "c4": 2}[cfg]]
         end = max(cand, key=lambda i: ours[i][1])
         step = ours[max(0, end + 1 - per_step):end + 1]
         tot = sum(t for _, t in step) or 1
@@ -66,8 +68,8 @@ if os.path.exists(os.path.join(SRC, "launches_sage3_c2.csv")):
             if "at::" not in k:
                 fh.write(f"{t:12.1f} us  {k[:110]}\n")
 
-for rep in ("attn_fwd_c2", "attn_fwd_train_c4", "attn_bwd_c4", "quantize_c2", "fp4mm_8k", "attn_fwd_sage3_c2",
-            "attn_fwd_plain_c2", "attn_fwd_mx_c2"):
+for rep in ("attn_fwd_c2", "attn_fwd_c3", "attn_fwd_train_c4", "attn_bwd_c4", "attn_bwd_plain_c4", "quantize_c2",
+            "fp4mm_8k", "attn_fwd_sage3_c2", "attn_fwd_plain_c2", "attn_fwd_mx_c2"):
     path = os.path.join(SRC, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -101,6 +103,8 @@ for rep in ("attn_fwd_c2", "attn_fwd_train_c4", "attn_bwd_c4", "quantize_c2", "f
 
 # bench.py reads profiles/ncu_summary.json for roofline.traffic (config -> dominant kernel)
 bench_map = {"c2": summary["attn_fwd_c2"][0], "c4": summary["attn_bwd_c4"][0]}
+if "attn_fwd_c3" in summary:
+    bench_map["c3"] = summary["attn_fwd_c3"][0]
 with open(os.path.join(DST, "ncu_summary.json"), "w") as fh:
     json.dump({"round": TAG, **bench_map, "all": summary}, fh, indent=1)
 print("wrote", sorted(os.listdir(DST)))
