@@ -10,7 +10,8 @@ Differences from the CPU reference, by design of the B200 path:
     validated exactly as the reference does (results are tiling-invariant,
     test_flash.py:72-84) and b_q / b_k are otherwise ignored;
   * accumulation is fp32 on the tensor cores (``accum_width=64`` raises
-    InvalidValue); ``instrument`` and ``threads`` are accepted and ignored.
+    InvalidValue); ``threads`` is accepted and ignored; ``instrument`` records
+    are rebuilt from the kernels' P^F dump (see _instrument_*).
 """
 
 from __future__ import annotations

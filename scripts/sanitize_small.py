@@ -1,4 +1,5 @@
-"""Small ragged cases of every GPU entry point (incl. sage3), for compute-sanitizer (memcheck / racecheck)."""
+"""Small ragged cases of every GPU entry point (incl. sage3, quantized=False, the ABI-3 scale / instrument
+arguments), for compute-sanitizer (memcheck / racecheck / synccheck)."""
 import os
 import sys
 
@@ -30,6 +31,16 @@ for n, d, causal in ((200, 64, True), (77, 128, False)):
     qg, kg, vg = (t.clone().requires_grad_() for t in (q, k, v))
     aq.attn_qat(qg, kg, vg, causal=causal, spec=aq.MXFP4).backward(torch.randn_like(q))
     aq.fp4mm(aq.quantize(q[0, 0].float(), aq.MXFP4), aq.quantize(k[0, 0].float(), aq.MXFP4))
+for n, d, causal in ((200, 64, True), (77, 128, False), (96, 24, True)):  # quantized=False fwd + bwd (K4 / K7 PLAIN)
+    q, k, v, do = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() for _ in range(4))
+    aq.attn_qat(q.requires_grad_(), k.requires_grad_(), v.requires_grad_(), causal=causal, quantized=False).backward(do)
+for n, d in ((200, 32), (77, 128)):  # tensor scales, P tensor scale, instrument dump, non-finite flag
+    q, k, v, do = (torch.randn(1, 2, n, d, generator=g, device="cuda").bfloat16() for _ in range(4))
+    pf = aq.pf_buffers(2, n, n)
+    o, lse, o_hp, ws = aq.attn_forward(q, k, v, causal=True, train=True, keep_for_bwd=True, q_scale="auto",
+                                       k_scale=0.5, v_scale=2.0, p_scale=1 / 2688, pf_out=pf)
+    aq.attn_backward(q, k, v, do, o, o_hp, lse, causal=True, fwd_workspace=ws, q_scale="auto", k_scale=0.5,
+                     v_scale=2.0, p_scale=1 / 2688, pf_out=aq.pf_buffers(2, n, n))
 x = torch.randn(37, 48, generator=g, device="cuda")
 aq.fp4mm(aq.quantize(x), aq.quantize(torch.randn(29, 48, generator=g, device="cuda")))
 aq.fake_quantize(torch.randn(5, 64, generator=g, device="cuda"), aq.MXFP4)
