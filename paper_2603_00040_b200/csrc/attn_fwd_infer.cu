@@ -20,6 +20,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// mbarrier waits inline in this kernel (ptx.cuh mode 0): the warp roles run
+// under different setmaxnreg limits, and an out-of-line wait routine would be
+// one function shared across them (ptxas cannot allocate it)
+#ifndef AQ_WAIT_MODE
+#define AQ_WAIT_MODE 3
+#endif
 #include "attn.h"
 #include "layouts.cuh"
 #include "pquant.cuh"
@@ -45,14 +51,40 @@
 namespace aq {
 namespace fwdi {
 
+#ifndef AQ_FWDI_CSB
+#define AQ_FWDI_CSB 4
+#endif
 template <int D>
 struct Cfg {
-  static constexpr int CS = 2;                       // column splits per softmax group
-  static constexpr int CW = TILE / CS;               // key columns per softmax thread
-  static constexpr int NSW = 4 * CS;                 // warps per softmax group
-  static constexpr int WA = 0, WB = NSW, PROD_A = 2 * NSW, PROD_B = PROD_A + 1, MMA_A = PROD_B + 1,
+  // column splits: pass 1 (group A) keeps 2 (its (m, l) merge order is shared
+  // with K4, so L and O stay bit-identical between the kernels); pass 2 (group
+  // B, the heavier half: exp + NVFP4 quantization) runs CSB splits, i.e. 4 x
+  // the warps per TMEM row quadrant for latency hiding at 32 keys per thread
+  static constexpr int CS = 2, CSB = AQ_FWDI_CSB;
+  static constexpr int CW = TILE / CS, CWB = TILE / CSB;  // key columns per softmax thread
+  static constexpr int NSW = 4 * CS, NSWB = 4 * CSB;      // warps per softmax group
+  static constexpr int WA = 0, WB = NSW, PROD_A = NSW + NSWB, PROD_B = PROD_A + 1, MMA_A = PROD_B + 1,
                        MMA_B = MMA_A + 1;
   static constexpr int NUM_THREADS = 32 * (MMA_B + 1);
+  // 896 threads launch at 72 registers; the producer / MMA warpgroup drops to 40,
+  // group B (32 keys per thread) to 56, and group A (64 live scores per thread)
+  // takes the rest, 120 (setmaxnreg; no spills anywhere)
+  static constexpr bool REALLOC = NUM_THREADS == 896;
+#ifndef AQ_FWDI_REGA
+#define AQ_FWDI_REGA 0
+#endif
+#ifndef AQ_FWDI_REGP
+#define AQ_FWDI_REGP 40
+#endif
+#ifndef AQ_FWDI_REGB
+#define AQ_FWDI_REGB 56
+#endif
+  // the CTA's register pool is what it launched with (72 x 896 = 64512): the
+  // three warpgroup limits must fit it exactly (an over-budget inc never returns)
+  static constexpr int POOL = (65536 / NUM_THREADS) / 8 * 8 * NUM_THREADS;
+  static constexpr int REG_P = AQ_FWDI_REGP, REG_B = AQ_FWDI_REGB,
+                       REG_A = AQ_FWDI_REGA ? AQ_FWDI_REGA : ((POOL - 128 * REG_P - 32 * NSWB * REG_B) / (32 * NSW)) / 8 * 8;
+  static_assert(!REALLOC || 128 * REG_P + 32 * NSWB * REG_B + 32 * NSW * REG_A <= POOL, "register pool");
   static constexpr int NSA = AQ_FWDI_NSA, NSB = AQ_FWDI_NSB, NP = AQ_FWDI_NP;  // ring depths
   static constexpr int NQ = AQ_FWDI_QSLOTS;           // Q slots: how far pass 1 may run ahead of pass 2
   // TMEM
@@ -124,22 +156,23 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   const int q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
   const int k_tiles = static_cast<int>(ceil_div(p.n_k, TILE));
   const int64_t n_items = p.heads * q_tiles;
-  constexpr int GRP = 32 * C::NSW;  // threads per softmax group
+  constexpr int GRP = 32 * C::NSW;   // threads of softmax group A (pass 1)
+  constexpr int GRPB = 32 * C::NSWB; // threads of softmax group B (pass 2)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NQ; ++s) {
       mbar_init(&bars[C::B_Q_FULL + s], 1);
       mbar_init(&bars[C::B_Q_EMPTY + s], 1);
       mbar_init(&bars[C::B_L_FULL + s], GRP);
-      mbar_init(&bars[C::B_L_EMPTY + s], GRP);
+      mbar_init(&bars[C::B_L_EMPTY + s], GRPB);
       mbar_init(&bars[C::B_QSF + s], 1);
     }
     mbar_init(&bars[C::B_O_FULL], 1);
-    mbar_init(&bars[C::B_O_EMPTY], GRP);
+    mbar_init(&bars[C::B_O_EMPTY], GRPB);
     mbar_init(&bars[C::B_SA_FULL], 1);
     mbar_init(&bars[C::B_SA_EMPTY], GRP);
     mbar_init(&bars[C::B_SB_FULL], 1);
-    mbar_init(&bars[C::B_SB_EMPTY], GRP);
+    mbar_init(&bars[C::B_SB_EMPTY], GRPB);
     for (int s = 0; s < C::NSA; ++s) {
       mbar_init(&bars[C::B_KA_FULL + s], 1);
       mbar_init(&bars[C::B_KA_EMPTY + s], 1);
@@ -149,7 +182,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       mbar_init(&bars[C::B_KB_EMPTY + s], 1);
     }
     for (int s = 0; s < C::NP; ++s) {
-      mbar_init(&bars[C::B_P_FULL + s], GRP);
+      mbar_init(&bars[C::B_P_FULL + s], GRPB);
       mbar_init(&bars[C::B_P_EMPTY + s], 1);
     }
     fence_mbar_init();
@@ -166,6 +199,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   constexpr uint32_t id_s = idesc_nvf4(128, 128);
   constexpr uint32_t id_pv = idesc_nvf4(128, D);
 
+  if (warp >= C::PROD_A) {
+  // producer / MMA warpgroup: few registers (setmaxnreg inside each role branch,
+  // so the limit applies to that branch only)
+  if constexpr (C::REALLOC) setmaxnreg_dec<C::REG_P>();
   if (warp == C::PROD_A) {
     // ------------------------------------------------------------ producer A: Q + K for pass 1
     int it = 0, k = 0;
@@ -349,6 +386,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       if (elect_one()) tc_commit(&bars[C::B_O_FULL]);
       __syncwarp();
     }
+  }
   } else {
     // ------------------------------------------------------------ softmax groups
     const bool grp_a = warp >= C::WA && warp < C::WA + C::NSW;
@@ -366,252 +404,277 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     const bool early_out = EARLY && (p.debug & 64) == 0;  // AQ_FWD_DEBUG bit 64 disables it (A/B timing)
     float* ml = reinterpret_cast<float*>(smem + C::ML);
     float* lb = reinterpret_cast<float*>(smem + C::LB);
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
-      const Item item = work_item(p, w, q_tiles, k_tiles);
-      const int nt = item.nt;
-      const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
-      int64_t kmax = p.n_k - 1;
-      if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
-      const int qs = k % C::NQ;
-      if (grp_a) {
-        // ---------------- pass 1: online (m, l) over this thread's 64 columns
-        // (log2 domain). Same code and merge order as the CS=2 column split of
-        // the training kernel (attn_fwd.cu), so L (hence P, P^F and O) is
-        // bit-identical between the two forward kernels.
-        float m = -INFINITY, l = 0.f;
-        for (int jj = 0; jj < nt; ++jj) {
-          mbar_wait(&bars[C::B_SA_FULL], su & 1);
-          ++su;
-          tc_fence_after();
-#pragma unroll
-          for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(t_lane + C::T_SA + cbase + c0, x + c0);
-          tmem_ld_wait();
-          tc_fence_before();
-          mbar_arrive(&bars[C::B_SA_EMPTY]);
-          const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
-          if (lim < CW - 1) {
-#pragma unroll
-            for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
-          }
-          auto expsum = [&](float base) {
-            float2 acc[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < CW / 2; ++i) {
-              const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
-                                          make_float2(-base, -base));
-#ifdef AQ_DBG_NOEXP1
-              const float2 e = t;
-#else
-              const float2 e = use_poly_p1(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
-#endif
-              acc[i & 3] = __fadd2_rn(acc[i & 3], e);
+    if (grp_a) {
+      if constexpr (C::REALLOC) setmaxnreg_inc<C::REG_A>();
+      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const Item item = work_item(p, w, q_tiles, k_tiles);
+        const int nt = item.nt;
+        const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
+        int64_t kmax = p.n_k - 1;
+        if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
+        const int qs = k % C::NQ;
+          // ---------------- pass 1: online (m, l) over this thread's 64 columns
+          // (log2 domain). Same code and merge order as the CS=2 column split of
+          // the training kernel (attn_fwd.cu), so L (hence P, P^F and O) is
+          // bit-identical between the two forward kernels.
+          float m = -INFINITY, l = 0.f;
+          for (int jj = 0; jj < nt; ++jj) {
+            mbar_wait(&bars[C::B_SA_FULL], su & 1);
+            ++su;
+            tc_fence_after();
+  #pragma unroll
+            for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(t_lane + C::T_SA + cbase + c0, x + c0);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bars[C::B_SA_EMPTY]);
+            const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+            if (lim < CW - 1) {
+  #pragma unroll
+              for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : -INFINITY;
             }
-            const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
-            const float2 s4 = __fadd2_rn(s01, s23);
-            return s4.x + s4.y;
-          };
-          float sum = expsum(m == -INFINITY ? 0.f : m);
-          // A rebase needs a term above 2^8, hence sum > 240 (or inf): only then (and
-          // while no column is visible yet) is the tile max needed. Same m sequence,
-          // hence the same bits, as taking the max of every tile.
-          if (!(sum <= 240.0f) || m == -INFINITY) {
-            float mx[8];
-#pragma unroll
-            for (int a = 0; a < 8; ++a) mx[a] = x[a];
-#pragma unroll
-            for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
-            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
-            if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
-              l = (m == -INFINITY) ? 0.f : l * ex2(m - mloc);
-              m = mloc;
-              sum = expsum(m);
-            }
-          }
-          l += sum;
-        }
-        // merge the column-split partials of each row
-        ml[(half * 2 + 0) * TILE + row] = m;
-        ml[(half * 2 + 1) * TILE + row] = l;
-        named_bar_sync(1, GRP);
-        float mt = -INFINITY;
-#pragma unroll
-        for (int h = 0; h < C::CS; ++h) mt = fmaxf(mt, ml[(h * 2) * TILE + row]);
-        float lt = 0.f;
-#pragma unroll
-        for (int h = 0; h < C::CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
-        named_bar_sync(1, GRP);
-        // natural-log L as the reference stores it (flash.py:217); group B
-        // rebuilds L2 = fl(L) * log2(e) exactly like the backward does
-        const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
-        if (half == 0 && grow < p.n_q) p.lse[item.head * p.n_q + grow] = L_nat;
-        if (k >= C::NQ) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k / C::NQ) - 1) & 1);
-        if (half == 0) lb[qs * TILE + row] = L_nat;
-        mbar_arrive(&bars[C::B_L_FULL + qs]);
-      } else {
-        // ---------------- pass 2: P, P^F, O
-        mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
-        const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
-        mbar_arrive(&bars[C::B_L_EMPTY + qs]);
-        const float thr = p_skip_thr(L2 + p.p_lshift, sl2);  // blocks of P * p_r below 2^-11
-        for (int jj = 0; jj < nt; ++jj) {
-          mbar_wait(&bars[C::B_SB_FULL], su & 1);
-          ++su;
-          tc_fence_after();
-#pragma unroll
-          for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(t_lane + C::T_SB + cbase + c0, x + c0);
-          tmem_ld_wait();
-          tc_fence_before();
-          mbar_arrive(&bars[C::B_SB_EMPTY]);
-          const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
-          // claim the P^F buffer first, so P = exp(S - L), its quantization and the
-          // stores form one straight-line block per 32 keys that the scheduler can
-          // interleave (MUFU work of one group overlaps ALU work of the previous)
-          const int pb = pc % C::NP;
-          if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
-          ++pc;
-          uint8_t* pcodes = smem + C::P0 + pb * C::P_BYTES;
-          uint8_t* psf = pcodes + C::PB_SF;
-          uint32_t scw[(CW + 63) / 64];
-#pragma unroll
-          for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
-          auto group32 = [&](int blk, bool masked) {
-#ifndef AQ_DBG_NOEXP2
-            p_from_s<16>(x + blk * 16, cbase + blk * 16, sl2, L2);
-#endif
-            if (masked) {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) x[blk * 16 + c] = (blk * 16 + c <= lim) ? x[blk * 16 + c] : 0.f;
-            }
-#ifdef AQ_DBG_NOQ2
-            PBlock qa, qb;
-            qa.scale = __float_as_uint(x[blk * 16]) & 0xff; qa.codes[0] = __float_as_uint(x[blk * 16 + 1]); qa.codes[1] = __float_as_uint(x[blk * 16 + 2]);
-            qb = qa;
-#else
-            if constexpr (MX) {
-              uint32_t cd[4], sc;
-              quantize_p32_mx(x + blk * 16, cd, sc);
-              *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
-                  make_uint4(cd[0], cd[1], cd[2], cd[3]);
-              scw[0] |= sc << (8 * (blk / 2));
-              return;
-            }
-            const PBlock qa = quantize_p16_s(x + blk * 16, p_r);
-            const PBlock qb = quantize_p16_s(x + blk * 16 + 16, p_r);
-#endif
-            *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
-                make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
-            scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
-          };
-          // exact early-out (pquant.cuh): 16-key blocks whose P is below 2^-11 in
-          // every row of the warp get P^F = 0 with scale 0x01 without an exponential.
-          // Checked with exponential back-off, so workloads where blocks rarely
-          // qualify (short rows) pay for one check every ~16 tiles.
-          uint32_t sk = 0;
-          if constexpr (!MX) {
-            if (early_out && chk_wait == 0) {  // warp-uniform; lanes with masked keys vote 0
-              sk = __reduce_and_sync(0xffffffffu, lim >= CW - 1 ? p_skip_mask<CW / 16>(x, thr) : 0u);
-              if (sk == 0) {
-                chk_pen = min(2 * chk_pen + 1, 15);
-                chk_wait = chk_pen;
-              } else {
-                chk_pen = 0;
+            auto expsum = [&](float base) {
+              float2 acc[4];
+  #pragma unroll
+              for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
+  #pragma unroll
+              for (int i = 0; i < CW / 2; ++i) {
+                const float2 t = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), make_float2(sl2, sl2),
+                                            make_float2(-base, -base));
+  #ifdef AQ_DBG_NOEXP1
+                const float2 e = t;
+  #else
+                const float2 e = use_poly_p1(cbase / 2 + i) ? ex2_pair<true>(t) : ex2_pair<false>(t);
+  #endif
+                acc[i & 3] = __fadd2_rn(acc[i & 3], e);
               }
-            } else if (chk_wait > 0) {
-              --chk_wait;
+              const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+              const float2 s4 = __fadd2_rn(s01, s23);
+              return s4.x + s4.y;
+            };
+            float sum = expsum(m == -INFINITY ? 0.f : m);
+            // A rebase needs a term above 2^8, hence sum > 240 (or inf): only then (and
+            // while no column is visible yet) is the tile max needed. Same m sequence,
+            // hence the same bits, as taking the max of every tile.
+            if (!(sum <= 240.0f) || m == -INFINITY) {
+              float mx[8];
+  #pragma unroll
+              for (int a = 0; a < 8; ++a) mx[a] = x[a];
+  #pragma unroll
+              for (int c = 8; c < CW; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+              const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+              if (mloc > m + 8.0f) {  // first visible tile, or a much larger max: rebase
+                l = (m == -INFINITY) ? 0.f : l * ex2(m - mloc);
+                m = mloc;
+                sum = expsum(m);
+              }
             }
+            l += sum;
           }
-          if (sk != 0) {
-#pragma unroll
-            for (int blk = 0; blk < CW / 16; blk += 2) {
+          // merge the column-split partials of each row
+          ml[(half * 2 + 0) * TILE + row] = m;
+          ml[(half * 2 + 1) * TILE + row] = l;
+          named_bar_sync(1, GRP);
+          float mt = -INFINITY;
+  #pragma unroll
+          for (int h = 0; h < C::CS; ++h) mt = fmaxf(mt, ml[(h * 2) * TILE + row]);
+          float lt = 0.f;
+  #pragma unroll
+          for (int h = 0; h < C::CS; ++h) lt += ml[(h * 2 + 1) * TILE + row] * ex2(ml[(h * 2) * TILE + row] - mt);
+          named_bar_sync(1, GRP);
+          // natural-log L as the reference stores it (flash.py:217); group B
+          // rebuilds L2 = fl(L) * log2(e) exactly like the backward does
+          const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
+          if (half == 0 && grow < p.n_q) p.lse[item.head * p.n_q + grow] = L_nat;
+          if (k >= C::NQ) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k / C::NQ) - 1) & 1);
+          if (half == 0) lb[qs * TILE + row] = L_nat;
+          mbar_arrive(&bars[C::B_L_FULL + qs]);
+      }
+    } else {
+      if constexpr (C::REALLOC) setmaxnreg_dec<C::REG_B>();
+      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const Item item = work_item(p, w, q_tiles, k_tiles);
+        const int nt = item.nt;
+        const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
+        int64_t kmax = p.n_k - 1;
+        if (p.causal) kmax = min(kmax, grow + (p.n_k - p.n_q));
+        const int qs = k % C::NQ;
+          // ---------------- pass 2: P, P^F, O (CSB column splits of CWB keys per thread)
+          constexpr int CW = C::CWB;
+          const int half = gw >> 2;  // column split of this thread (pass 2)
+          const int cbase = half * CW;
+          mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
+          const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
+          mbar_arrive(&bars[C::B_L_EMPTY + qs]);
+          const float thr = p_skip_thr(L2 + p.p_lshift, sl2);  // blocks of P * p_r below 2^-11
+          for (int jj = 0; jj < nt; ++jj) {
+            mbar_wait(&bars[C::B_SB_FULL], su & 1);
+            ++su;
+            tc_fence_after();
+  #pragma unroll
+            for (int c0 = 0; c0 < CW; c0 += 32) tmem_ld32f(t_lane + C::T_SB + cbase + c0, x + c0);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bars[C::B_SB_EMPTY]);
+            const int64_t lim = kmax - (static_cast<int64_t>(jj) * TILE + cbase);
+            // claim the P^F buffer first, so P = exp(S - L), its quantization and the
+            // stores form one straight-line block per 32 keys that the scheduler can
+            // interleave (MUFU work of one group overlaps ALU work of the previous)
+            const int pb = pc % C::NP;
+            if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
+            ++pc;
+            uint8_t* pcodes = smem + C::P0 + pb * C::P_BYTES;
+            uint8_t* psf = pcodes + C::PB_SF;
+            uint32_t scw[(CW + 63) / 64];
+  #pragma unroll
+            for (int s = 0; s < (CW + 63) / 64; ++s) scw[s] = 0;
+            auto group32 = [&](int blk, bool masked) {
+  #ifndef AQ_DBG_NOEXP2
+              p_from_s<16>(x + blk * 16, cbase + blk * 16, sl2, L2);
+  #endif
+              if (masked) {
+  #pragma unroll
+                for (int c = 0; c < 32; ++c) x[blk * 16 + c] = (blk * 16 + c <= lim) ? x[blk * 16 + c] : 0.f;
+              }
+  #ifdef AQ_DBG_NOQ2
               PBlock qa, qb;
-              qa.scale = qb.scale = 1u;
-              qa.codes[0] = qa.codes[1] = qb.codes[0] = qb.codes[1] = 0u;
-              if (!((sk >> blk) & 1u)) {
-                p_from_s<8>(x + blk * 16, cbase + blk * 16, sl2, L2);
-                qa = quantize_p16_s(x + blk * 16, p_r);
+              qa.scale = __float_as_uint(x[blk * 16]) & 0xff; qa.codes[0] = __float_as_uint(x[blk * 16 + 1]); qa.codes[1] = __float_as_uint(x[blk * 16 + 2]);
+              qb = qa;
+  #else
+              if constexpr (MX) {
+                uint32_t cd[4], sc;
+                quantize_p32_mx(x + blk * 16, cd, sc);
+                *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
+                    make_uint4(cd[0], cd[1], cd[2], cd[3]);
+                scw[0] |= sc << (8 * (blk / 2));
+                return;
               }
-              if (!((sk >> (blk + 1)) & 1u)) {
-                p_from_s<8>(x + blk * 16 + 16, cbase + blk * 16 + 16, sl2, L2);
-                qb = quantize_p16_s(x + blk * 16 + 16, p_r);
-              }
+              const PBlock qa = quantize_p16_s(x + blk * 16, p_r);
+              const PBlock qb = quantize_p16_s(x + blk * 16 + 16, p_r);
+  #endif
               *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
                   make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
               scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
-            }
-          } else if (lim >= CW - 1) {
-#pragma unroll
-            for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, false);
-          } else {
-#pragma unroll
-            for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, true);
-          }
-          if constexpr (MX) {
-            *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 32)) = static_cast<uint16_t>(scw[0]);
-          } else {
-#pragma unroll
-            for (int s = 0; s < CW / 64; ++s)
-              *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
-          }
-          if (p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
-            const int64_t n16 = ceil_div(p.n_k, 16);
-            const int64_t c0 = static_cast<int64_t>(jj) * TILE + cbase;  // first key of this thread
-            uint8_t* dc = p.pf_codes + (item.head * p.n_q + grow) * (n16 * 8);
-            uint8_t* ds = p.pf_scales + (item.head * p.n_q + grow) * n16;
-#pragma unroll
-            for (int b = 0; b < CW / 16; ++b) {
-              const int64_t blk = c0 / 16 + b;
-              if (blk < n16) {
-                *reinterpret_cast<uint2*>(dc + blk * 8) =
-                    *reinterpret_cast<const uint2*>(pcodes + t8x32_off(row, cbase + 16 * b, TILE));
-                ds[blk] = psf[sf512_off(row, cbase / 16 + b)];
+            };
+            // exact early-out (pquant.cuh): 16-key blocks whose P is below 2^-11 in
+            // every row of the warp get P^F = 0 with scale 0x01 without an exponential.
+            // Checked with exponential back-off, so workloads where blocks rarely
+            // qualify (short rows) pay for one check every ~16 tiles.
+            uint32_t sk = 0;
+            if constexpr (!MX) {
+              if (early_out && chk_wait == 0) {  // warp-uniform; lanes with masked keys vote 0
+                sk = __reduce_and_sync(0xffffffffu, lim >= CW - 1 ? p_skip_mask<CW / 16>(x, thr) : 0u);
+                if (sk == 0) {
+                  chk_pen = min(2 * chk_pen + 1, 15);
+                  chk_wait = chk_pen;
+                } else {
+                  chk_pen = 0;
+                }
+              } else if (chk_wait > 0) {
+                --chk_wait;
               }
             }
-          }
-          fence_async_smem();
-          mbar_arrive(&bars[C::B_P_FULL + pb]);
-        }
-        // epilogue: O rows -> registers, release O, store
-        mbar_wait(&bars[C::B_O_FULL], k & 1);
-        tc_fence_after();
-        constexpr int DW = D / C::CS;
-        float o[DW];
-#pragma unroll
-        for (int c = 0; c < DW; c += 32) tmem_ld32f(t_lane + C::T_O + half * DW + c, o + c);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&bars[C::B_O_EMPTY]);
-        if (p.o_mul != 1.f) {  // per-tensor scales t_v t_p (two-level NVFP4)
-#pragma unroll
-          for (int c = 0; c < DW; ++c) o[c] *= p.o_mul;
-        }
-        if (grow < p.n_q && p.o != nullptr) {
-          const int64_t base = (item.head * p.n_q + grow) * D + half * DW;
-          if (p.o_dt == 0) {
-            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + base);
-#pragma unroll
-            for (int e = 0; e < DW; e += 4) d4[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
-          } else {
-            uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.o) + base);
-#pragma unroll
-            for (int e = 0; e < DW; e += 8) {
-              uint32_t h[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (p.o_dt == 1) {
-                  const __nv_bfloat162 v = __floats2bfloat162_rn(o[e + 2 * q], o[e + 2 * q + 1]);
-                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
-                } else {
-                  const __half2 v = __floats2half2_rn(o[e + 2 * q], o[e + 2 * q + 1]);
-                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
+            if (sk != 0) {
+  #pragma unroll
+              for (int blk = 0; blk < CW / 16; blk += 2) {
+                PBlock qa, qb;
+                qa.scale = qb.scale = 1u;
+                qa.codes[0] = qa.codes[1] = qb.codes[0] = qb.codes[1] = 0u;
+                if (!((sk >> blk) & 1u)) {
+                  p_from_s<8>(x + blk * 16, cbase + blk * 16, sl2, L2);
+                  qa = quantize_p16_s(x + blk * 16, p_r);
+                }
+                if (!((sk >> (blk + 1)) & 1u)) {
+                  p_from_s<8>(x + blk * 16 + 16, cbase + blk * 16 + 16, sl2, L2);
+                  qb = quantize_p16_s(x + blk * 16 + 16, p_r);
+                }
+                *reinterpret_cast<uint4*>(pcodes + t8x32_off(row, cbase + blk * 16, TILE)) =
+                    make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
+                scw[blk / 4] |= (qa.scale << (8 * (blk & 3))) | (qb.scale << (8 * ((blk + 1) & 3)));
+              }
+            } else if (lim >= CW - 1) {
+  #pragma unroll
+              for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, false);
+            } else {
+  #pragma unroll
+              for (int blk = 0; blk < CW / 16; blk += 2) group32(blk, true);
+            }
+            if constexpr (MX) {
+              if constexpr (CW >= 64)
+                *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 32)) = static_cast<uint16_t>(scw[0]);
+              else
+                psf[sf512_off(row, cbase / 32)] = static_cast<uint8_t>(scw[0]);
+            } else if constexpr (CW >= 64) {
+  #pragma unroll
+              for (int s = 0; s < CW / 64; ++s)
+                *reinterpret_cast<uint32_t*>(psf + sf512_off(row, cbase / 16 + 4 * s)) = scw[s];
+            } else {
+              *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) = static_cast<uint16_t>(scw[0]);
+            }
+            if (p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
+              const int64_t n16 = ceil_div(p.n_k, 16);
+              const int64_t c0 = static_cast<int64_t>(jj) * TILE + cbase;  // first key of this thread
+              uint8_t* dc = p.pf_codes + (item.head * p.n_q + grow) * (n16 * 8);
+              uint8_t* ds = p.pf_scales + (item.head * p.n_q + grow) * n16;
+  #pragma unroll
+              for (int b = 0; b < CW / 16; ++b) {
+                const int64_t blk = c0 / 16 + b;
+                if (blk < n16) {
+                  *reinterpret_cast<uint2*>(dc + blk * 8) =
+                      *reinterpret_cast<const uint2*>(pcodes + t8x32_off(row, cbase + 16 * b, TILE));
+                  ds[blk] = psf[sf512_off(row, cbase / 16 + b)];
                 }
               }
-              d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+            }
+            fence_async_smem();
+            mbar_arrive(&bars[C::B_P_FULL + pb]);
+          }
+          // epilogue: O rows -> registers, release O, store
+          mbar_wait(&bars[C::B_O_FULL], k & 1);
+          tc_fence_after();
+          constexpr int DW = D / C::CSB;
+          float o[DW];
+          if constexpr (DW >= 32) {
+  #pragma unroll
+            for (int c = 0; c < DW; c += 32) tmem_ld32f(t_lane + C::T_O + half * DW + c, o + c);
+          } else {
+            uint32_t r16[16];
+            tmem_ld16(t_lane + C::T_O + half * DW, r16);
+  #pragma unroll
+            for (int c = 0; c < 16; ++c) o[c] = __uint_as_float(r16[c]);
+          }
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&bars[C::B_O_EMPTY]);
+          if (p.o_mul != 1.f) {  // per-tensor scales t_v t_p (two-level NVFP4)
+  #pragma unroll
+            for (int c = 0; c < DW; ++c) o[c] *= p.o_mul;
+          }
+          if (grow < p.n_q && p.o != nullptr) {
+            const int64_t base = (item.head * p.n_q + grow) * D + half * DW;
+            if (p.o_dt == 0) {
+              float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + base);
+  #pragma unroll
+              for (int e = 0; e < DW; e += 4) d4[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+            } else {
+              uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.o) + base);
+  #pragma unroll
+              for (int e = 0; e < DW; e += 8) {
+                uint32_t h[4];
+  #pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  if (p.o_dt == 1) {
+                    const __nv_bfloat162 v = __floats2bfloat162_rn(o[e + 2 * q], o[e + 2 * q + 1]);
+                    h[q] = *reinterpret_cast<const uint32_t*>(&v);
+                  } else {
+                    const __half2 v = __floats2half2_rn(o[e + 2 * q], o[e + 2 * q + 1]);
+                    h[q] = *reinterpret_cast<const uint32_t*>(&v);
+                  }
+                }
+                d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+              }
             }
           }
-        }
       }
     }
   }

@@ -78,6 +78,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 //   mode 0: inline sleeping loop with a retry counter
 //   mode 1: inline sleeping loop, no counter (no hang protection; tuning only)
 //   mode 2: inline blocking probe, out-of-line retry loop with counter
+//   mode 3: mode 2's probe with the retry loop inline (kernels whose warp roles
+//           run under different setmaxnreg limits cannot share a called routine)
 //   mode 5: inline non-blocking probe, out-of-line sleeping loop with counter
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
@@ -93,6 +95,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 #elif AQ_WAIT_MODE == 1
   while (!mbar_try_wait(bar, parity)) {
+  }
+#elif AQ_WAIT_MODE == 3
+  // mode 2's probe (no suspend hint) with the retry loop inline
+  uint32_t spins = 0;
+  while (!mbar_try_wait_t<false>(bar, parity)) {
+    if (++spins == (1u << 22)) __trap();
   }
 #elif AQ_WAIT_MODE == 5
   if (!mbar_test_wait(bar, parity)) mbar_wait_slow(bar, parity);
@@ -300,6 +308,15 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(const float* v) {
       : "=r"(r)
       : "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
   return r;
+}
+// warpgroup register reallocation (all 128 threads of a warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
