@@ -424,8 +424,9 @@ def run_attention(args, name, cfg, rank, world, local, main_line=False):
                 "peak_source": "measured live: tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak)",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                 "path_ceiling_frac": achieved / (peaks["nvfp4"] * 2.0 / 3.0),
-                # the MUFU-bound ceiling: 2 exponentials per score (7/8 on MUFU.EX2) plus one
-                # reciprocal per 16-key block, 1.87 MUFU ops per score, 16 MUFU/clk/SM
+                # the MUFU-bound ceiling: 2 exponentials per score (pass 1 7/8, pass 2 6/8 on
+                # MUFU.EX2, the rest on the FMA pipe) plus one reciprocal per 16-key block,
+                # 1.69 MUFU ops per score, 16 MUFU/clk/SM
                 "sfu_ceiling_tflops": sfu, "sfu_frac": achieved / sfu,
                 "traffic": _traffic_from_profiles(name)}
     else:
@@ -617,10 +618,11 @@ def run_layer_mode(args, cfg, rank, world, local):
 
 def _sfu_ceiling(d, sm_mhz, torch):
     """Forward TFLOP/s at which the MUFU (SFU) pipe saturates: 4 d algorithmic FLOPs per
-    score over 1.87 MUFU ops per score (ncu, profiles/) at 16 MUFU results / clk / SM."""
+    score over 1.69 MUFU ops per score (7/8 + 6/8 exponentials + 1/16 reciprocal; the pipe
+    rate is measured in profiles/r02_pipe_probe.txt) at 16 MUFU results / clk / SM."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     mufu_per_s = 16.0 * sms * sm_mhz * 1e6
-    return 4.0 * d * mufu_per_s / 1.87 / 1e12
+    return 4.0 * d * mufu_per_s / (0.875 + 0.75 + 0.0625) / 1e12
 
 
 def _traffic_from_profiles(config):

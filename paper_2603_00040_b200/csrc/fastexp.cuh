@@ -45,7 +45,7 @@ __device__ __forceinline__ float2 ex2_pair(float2 t) {
 // Which element pairs of a 16-pair group use the polynomial: pairs whose
 // index mod 8 is < POLY_PAIRS_OF_8 (compile-time split of the exp work).
 #ifndef AQ_POLY_PAIRS_OF_8
-#define AQ_POLY_PAIRS_OF_8 1
+#define AQ_POLY_PAIRS_OF_8 2
 #endif
 __host__ __device__ constexpr bool use_poly(int pair) { return (pair & 7) < AQ_POLY_PAIRS_OF_8; }
 
