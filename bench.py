@@ -421,7 +421,8 @@ def run_attention(args, name, cfg, rank, world, local, main_line=False):
         sfu = _sfu_ceiling(d, clocks.get("sm_mhz") or 1965.0, torch)
         roof = {"bound": "tensor", "kernel": f"attn_fwd_infer_kernel<{d}>", "achieved": achieved,
                 "peak": peaks["nvfp4"], "unit": "TFLOP/s", "frac": achieved / peaks["nvfp4"],
-                "peak_source": "measured live: tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak)",
+                "peak_source": "live tcgen05 kind::mxf4nvf4 M128N256K64 issue-rate probe (aq_probe_mma_peak): "
+                               "MEASURED_PEAKS.json has no FP4 entry; the nominal dense FP4 peak is 9 PF/s",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms,
                 "path_ceiling_frac": achieved / (peaks["nvfp4"] * 2.0 / 3.0),
                 # the MUFU-bound ceiling: 2 exponentials per score (pass 1 7/8, pass 2 6/8 on
@@ -438,10 +439,17 @@ def run_attention(args, name, cfg, rank, world, local, main_line=False):
                           reps, 2, st, barrier)
         bflops = flops_rank * 2.5 / 3.5
         achieved = bflops / (bms * 1e-3) / 1e12
+        # denominator: the driver's measured bf16 GEMM (MEASURED_PEAKS.json, burst: a kernel timed
+        # alone), as B200_PROFILING.md prescribes; the live tcgen05 issue probe is reported beside it
+        mp = _measured_peaks()
+        bf16_peak = mp.get("bf16_tflops") or peaks["bf16"]
         roof = {"bound": "tensor", "kernel": f"attn_bwd_kernel<{d}> (+bwd_pre)", "achieved": achieved,
-                "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16"],
-                "peak_source": "measured live: tcgen05 kind::f16 bf16 M128N256K16 probe (the backward's dense "
-                               "contractions are bf16; its S recompute is FP4)",
+                "peak": bf16_peak, "unit": "TFLOP/s", "frac": achieved / bf16_peak,
+                "peak_source": ("of measured: MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 GEMM, burst)"
+                                if mp.get("bf16_tflops") else
+                                "live tcgen05 kind::f16 bf16 M128N256K16 probe (MEASURED_PEAKS.json absent)")
+                + "; the backward's dense contractions are bf16, its S recompute FP4",
+                "frac_of_tcgen05_probe": achieved / peaks["bf16"],
                 "kernel_ms": bms, "kernel_share_of_step": bms / ms,
                 "step_frac_of_fp4_peak": value / world / peaks["nvfp4"],
                 "step_frac_of_mixed_ceiling": value / world / (1.17 * peaks["bf16"]),
@@ -614,6 +622,15 @@ def run_layer_mode(args, cfg, rank, world, local):
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _measured_peaks():
+    """The driver-written MEASURED_PEAKS.json (roofline denominators), or {}."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
 
 def _sfu_ceiling(d, sm_mhz, torch):

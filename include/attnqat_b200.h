@@ -232,12 +232,15 @@ int aq_attn_bwd(const AqBwdArgs* args, void* stream);
 int aq_attn_bwd_mx(const AqBwdArgs* args, void* stream);
 /* quantized=False backward (flash_backward with quantized=False,
  * flash.py:344-349 -- every variant reduces to it): the K7 skeleton with S
- * recomputed from bf16 Q / K tiles on kind::f16, P = exp(S - L) unquantized,
+ * recomputed from 16-bit Q / K tiles on kind::f16, P = exp(S - L) unquantized,
  * D = rowsum(dO . O) with O = args->o_hp if set, else args->o (O' == O here).
- * bf16 operands, fp32 accumulation; only softmax_scale of the scale fields is
- * honoured (the others must be 0 / 1); fwd_workspace and pf_* are ignored.
- * Workspace: aq_attn_bwd_workspace_bytes(). */
-int aq_attn_bwd_plain(const AqBwdArgs* args, void* stream);
+ * fmt as for aq_attn_fwd_plain (0 = fp16, 1 = bf16: every 16-bit operand --
+ * Q, K, V, dO, P, dS -- in that format; pass the forward's format so S and L
+ * agree; for fp16 the caller keeps dO inside fp16's range, e.g. by an exact
+ * power-of-two gain it divides out of the gradients), fp32 accumulation; only
+ * softmax_scale of the scale fields is honoured (the others must be 0 / 1);
+ * fwd_workspace and pf_* are ignored. Workspace: aq_attn_bwd_workspace_bytes(). */
+int aq_attn_bwd_plain(const AqBwdArgs* args, int fmt, void* stream);
 
 /* ---- measurement utilities (bench.py roofline denominators) ---------------
  * One CTA per SM issuing back-to-back tcgen05 MMAs from shared memory:

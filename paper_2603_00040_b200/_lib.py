@@ -85,7 +85,7 @@ PROTOTYPES = {
     "aq_attn_fwd_plain": (c_int, [ctypes.POINTER(AqFwdArgs), c_int, c_vp]),
     "aq_attn_fwd_mx": (c_int, [ctypes.POINTER(AqFwdArgs), c_vp]),
     "aq_attn_bwd_mx": (c_int, [ctypes.POINTER(AqBwdArgs), c_vp]),
-    "aq_attn_bwd_plain": (c_int, [ctypes.POINTER(AqBwdArgs), c_vp]),
+    "aq_attn_bwd_plain": (c_int, [ctypes.POINTER(AqBwdArgs), c_int, c_vp]),
     "aq_attn_fwd_sage3_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64]),
     "aq_attn_fwd_sage3": (c_int, [ctypes.POINTER(AqSage3Args), c_vp]),
     "aq_attn_bwd_workspace_bytes": (c_i64, [c_i64, c_i64, c_i64, c_i64]),

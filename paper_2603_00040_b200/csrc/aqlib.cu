@@ -622,11 +622,12 @@ int aq_attn_bwd(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stre
 
 int aq_attn_bwd_mx(const AqBwdArgs* a, void* stream) { return attn_bwd_impl(a, stream, true); }
 
-int aq_attn_bwd_plain(const AqBwdArgs* a, void* stream) {
+int aq_attn_bwd_plain(const AqBwdArgs* a, int fmt, void* stream) {
   if (!a || !a->q || !a->k || !a->v || !a->d_o || !a->lse || !a->dq || !a->dk || !a->dv || !a->workspace)
     return AQ_E_INVALID;
   if (!dtype_ok(a->in_dtype) || !dtype_ok(a->do_dtype) || !dtype_ok(a->o_dtype) || !dtype_ok(a->g_dtype))
     return AQ_E_INVALID;
+  if (fmt != 0 && fmt != 1) return AQ_E_INVALID;
   const void* o_ref = a->o_hp ? a->o_hp : a->o;  // O' == O without quantization (flash.py:195-200)
   if (!o_ref) return AQ_E_INVALID;
   if (a->heads <= 0 || a->n_q <= 0 || a->n_k <= 0) return AQ_E_SHAPE;
@@ -640,14 +641,14 @@ int aq_attn_bwd_plain(const AqBwdArgs* a, void* stream) {
   uint8_t* ws = static_cast<uint8_t*>(a->workspace);
   uint8_t* b = ws + bw.fwd;
   const int d = static_cast<int>(a->d);
-  // bf16 T8x8 tiles of Q / K / V (one copy serves K- and MN-major reads)
-  if (launch_tile16(a->q, a->in_dtype, a->heads, a->n_q, d, 1, b + fw.q_hb, st) != cudaSuccess ||
-      launch_tile16(a->k, a->in_dtype, a->heads, a->n_k, d, 1, b + fw.k_hb, st) != cudaSuccess ||
-      launch_tile16(a->v, a->in_dtype, a->heads, a->n_k, d, 1, b + fw.v_hb, st) != cudaSuccess)
+  // 16-bit T8x8 tiles of Q / K / V in the forward's format (one copy serves K- and MN-major reads)
+  if (launch_tile16(a->q, a->in_dtype, a->heads, a->n_q, d, fmt, b + fw.q_hb, st) != cudaSuccess ||
+      launch_tile16(a->k, a->in_dtype, a->heads, a->n_k, d, fmt, b + fw.k_hb, st) != cudaSuccess ||
+      launch_tile16(a->v, a->in_dtype, a->heads, a->n_k, d, fmt, b + fw.v_hb, st) != cudaSuccess)
     return AQ_E_CUDA;
   float* delta = reinterpret_cast<float*>(ws + bw.delta);
-  if (launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, d, delta, ws + bw.do_h, st, 1.f) !=
-      cudaSuccess)
+  if (launch_bwd_pre(a->d_o, a->do_dtype, o_ref, a->o_dtype, a->heads, a->n_q, d, delta, ws + bw.do_h, st, 1.f,
+                     fmt == 0 ? 1 : 0) != cudaSuccess)
     return AQ_E_CUDA;
   BwdParams p{};
   p.q_h = b + fw.q_hb;
@@ -667,6 +668,7 @@ int aq_attn_bwd_plain(const AqBwdArgs* a, void* stream) {
   p.causal = a->causal;
   p.fq_p = 0;
   p.plain = 1;
+  p.plain_fmt = fmt;
   p.scale_log2 = scale_log2_of(ts, a->d);
   p.inv_sqrt_d = static_cast<float>(ts.sm == 0.0 ? 1.0 / std::sqrt(static_cast<double>(a->d)) : ts.sm);
   return cuda_status(launch_attn_bwd(p, st));

@@ -83,7 +83,8 @@ struct BwdParams {
   int causal;
   int fq_p;              // quantize the recomputed P for dV
   int mx;                // MXFP4: S on kind::mxf4 block32, P^F in 32-key UE8M0 blocks
-  int plain = 0;         // quantized=False: S on kind::f16 from bf16 Q / K tiles (q_h / k_h), P unquantized
+  int plain = 0;         // quantized=False: S on kind::f16 from 16-bit Q / K tiles (q_h / k_h), P unquantized
+  int plain_fmt = 1;     // PLAIN operand format: 1 = bf16, 0 = fp16 (every 16-bit tile and MMA)
   float scale_log2;      // log2(e)/sqrt(d) (times t_q t_k)
   float inv_sqrt_d;      // 1/sqrt(d) (times t_v: dS = P (t_v dP - D) / sqrt(d), D pre-divided by t_v)
   float p_r = 1.f;       // 1 / t_p: P^F quantized as P * p_r (1 = reference semantics)
@@ -151,6 +152,7 @@ cudaError_t launch_pack_kv4(const uint8_t* k_codes, const uint8_t* k_scales, con
                             const uint8_t* vt_scales, int64_t heads, int64_t n, int d, uint8_t* k_codes_t,
                             uint8_t* k_sf_t, uint8_t* v_codes_t, uint8_t* v_sf_t, cudaStream_t st);
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
-                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul = 1.f);
+                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul = 1.f,
+                           int tile_f16 = 0);
 
 }  // namespace aq

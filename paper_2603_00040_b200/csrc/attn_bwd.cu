@@ -79,6 +79,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&v);
 }
+// 16-bit pair in the MMA operand format: fp16 (f16 = true, the PLAIN instance's
+// fp16 mode) or bf16
+__device__ __forceinline__ uint32_t pack16(float a, float b, bool f16) {
+  if (f16) {
+    const __half2 v = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+  }
+  return pack_bf16(a, b);
+}
 
 // N consecutive fp32 values -> dst[base, base+N) in dtype dt (0 fp32, 1 bf16, 2 fp16)
 template <int N>
@@ -113,7 +122,7 @@ __device__ __forceinline__ void store_run(void* dst, int64_t base, int dt, float
 // dS = (dP - D) . P / sqrt(d) for a KPT-key run -> bf16 [query][key] T8x8
 template <int KPT>
 __device__ __forceinline__ void store_ds(uint8_t* ds_h, int row, int kb, const float* dp, const float* pr, float Dq,
-                                         float inv_sqrt_d) {
+                                         float inv_sqrt_d, bool f16 = false) {
 #pragma unroll
   for (int c8 = 0; c8 < KPT; c8 += 8) {
     float ds[8];
@@ -126,7 +135,8 @@ __device__ __forceinline__ void store_ds(uint8_t* ds_h, int row, int kb, const f
       ds[e + 1] = dd.y;
     }
     *reinterpret_cast<uint4*>(ds_h + t8x8_off(row, kb + c8)) =
-        make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]), pack_bf16(ds[6], ds[7]));
+        make_uint4(pack16(ds[0], ds[1], f16), pack16(ds[2], ds[3], f16), pack16(ds[4], ds[5], f16),
+                   pack16(ds[6], ds[7], f16));
   }
 }
 
@@ -295,9 +305,11 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   } else if (warp == MMA) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
-    constexpr uint32_t id_s16 = idesc_f16(128, 128, 1, 0, 0);  // PLAIN: Q (K-major) x K (K-major), bf16
-    constexpr uint32_t id_dp = idesc_f16(128, HALF, 1, 0, 0);  // dO (K-major) x V^F half (K-major)
-    constexpr uint32_t id_kv = idesc_f16(128, D, 1, 1, 1);     // P^F^T / dS^T (MN) x dO / Q^F (MN)
+    // 16-bit operand format: bf16, or the PLAIN instance's p.plain_fmt (0 = fp16)
+    const uint32_t f16f = PLAIN ? static_cast<uint32_t>(p.plain_fmt) : 1u;
+    const uint32_t id_s16 = idesc_f16(128, 128, f16f, 0, 0);  // PLAIN: Q (K-major) x K (K-major)
+    const uint32_t id_dp = idesc_f16(128, HALF, f16f, 0, 0);  // dO (K-major) x V^F half (K-major)
+    const uint32_t id_kv = idesc_f16(128, D, f16f, 1, 1);     // P^F^T / dS^T (MN) x dO / Q^F (MN)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);        // FP4 codes, K-major T8x32
     constexpr uint64_t t_sf = desc_template(0, 128);
     constexpr uint64_t t_kmaj = desc_template(2048, 128);       // bf16 T8x8 read K-major
@@ -402,6 +414,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     const int dph = kb / HALF;    // dP half holding those keys
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
+    const bool f16 = PLAIN && p.plain_fmt == 0;  // fp16 operand tiles (PLAIN fp16 mode)
     uint8_t* p_h = smem + L::P_H;
     uint8_t* ds_h = smem + L::DS_H;
     AQ_BPROF(unsigned long long pr_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long tq_ = clock64();)
@@ -509,8 +522,8 @@ if (PLAIN || !(MX && p.fq_p)) {
 #pragma unroll
           for (int h8 = 0; h8 < 2; ++h8) {
             const float* v = pr + blk * 16 + h8 * 8;
-            w[h8] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                               pack_bf16(v[6], v[7]));
+            w[h8] = make_uint4(pack16(v[0], v[1], f16), pack16(v[2], v[3], f16), pack16(v[4], v[5], f16),
+                               pack16(v[6], v[7], f16));
           }
         }
         *reinterpret_cast<uint4*>(p_h + t8x8_off(row, kb + blk * 16)) = w[0];
@@ -530,7 +543,7 @@ if (PLAIN || !(MX && p.fq_p)) {
       AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
       if (ii > 0) mbar_wait(&bars[KV_B_DS_FREE], (ii - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[5] += tn_ - tq_; tq_ = tn_;)
-      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
+      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d, f16);
       fence_async_smem();
       mbar_arrive(&bars[KV_B_DS_FULL]);
       AQ_BPROF(tn_ = clock64(); pr_[6] += tn_ - tq_; tq_ = tn_;)
@@ -705,9 +718,10 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
   } else if (warp == MMA) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_nvf4(128, 128);
-    constexpr uint32_t id_s16 = idesc_f16(128, 128, 1, 0, 0);  // PLAIN: Q (K-major) x K (K-major), bf16
-    constexpr uint32_t id_dp = idesc_f16(128, 128, 1, 0, 0);  // dO (K-major) x V^F (K-major)
-    constexpr uint32_t id_dq = idesc_f16(128, D, 1, 0, 1);    // dS (K-major) x K^F (MN-major)
+    const uint32_t f16f = PLAIN ? static_cast<uint32_t>(p.plain_fmt) : 1u;
+    const uint32_t id_s16 = idesc_f16(128, 128, f16f, 0, 0);  // PLAIN: Q (K-major) x K (K-major)
+    const uint32_t id_dp = idesc_f16(128, 128, f16f, 0, 0);  // dO (K-major) x V^F (K-major)
+    const uint32_t id_dq = idesc_f16(128, D, f16f, 0, 1);    // dS (K-major) x K^F (MN-major)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);
     constexpr uint64_t t_sf = desc_template(0, 128);
     constexpr uint64_t t_kmaj = desc_template(2048, 128);
@@ -791,6 +805,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
     const int kb = kg * KPT;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
+    const bool f16 = PLAIN && p.plain_fmt == 0;
     const int64_t q = q0 + row;
     const bool qvalid = q < p.n_q;
     const float L2 = qvalid ? p.lse[head * p.n_q + q] * 1.44269504088896340736f : 0.f;
@@ -825,7 +840,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       if (j > 0) mbar_wait(&bars[Q_B_DS_EMPTY], (j - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[3] += tn_ - tq_; tq_ = tn_;)
-      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d);
+      store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d, f16);
       fence_async_smem();
       mbar_arrive(&bars[Q_B_DS_FULL]);
       AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
@@ -891,7 +906,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
 template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt, const void* o_ref, int o_dt,
                                                       int64_t heads, int64_t n_q, float* delta, uint8_t* do_h,
-                                                      float delta_mul) {
+                                                      float delta_mul, int tile_f16) {
   constexpr int NCG = D / 8;  // 16-byte column groups per row
   const int64_t q_tiles = ceil_div(n_q, TILE);
   const int64_t row_groups = heads * q_tiles * (TILE / 8);
@@ -944,10 +959,17 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt
                              : reinterpret_cast<const float*>(o_ref)[base + e];
         }
       }
+      // D from the dO the dP MMA sees: round dO to the tile format first, so
+      // dP - D cancels exactly where the softmax is sharp (dP ~ D) instead of
+      // exposing dO's 16-bit rounding (round-2 fix; D = rowsum(dO . O_ref))
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        g[e] = tile_f16 ? __half2float(__float2half_rn(g[e])) : __bfloat162float(__float2bfloat16_rn(g[e]));
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc = fmaf(g[e], o[e], acc);
       *reinterpret_cast<uint4*>(tdst + t8x8_off(static_cast<int>(q % TILE), c8 * 8)) =
-          make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+          make_uint4(pack16(g[0], g[1], tile_f16), pack16(g[2], g[3], tile_f16), pack16(g[4], g[5], tile_f16),
+                     pack16(g[6], g[7], tile_f16));
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 8);
     acc += __shfl_xor_sync(0xffffffffu, acc, 16);
@@ -993,11 +1015,13 @@ extern "C" int aq_debug_bwd_profile(unsigned long long* out, int reset) {
 }
 
 cudaError_t launch_bwd_pre(const void* d_o, int do_dt, const void* o_ref, int o_dt, int64_t heads, int64_t n_q,
-                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul) {
+                           int d, float* delta, uint8_t* do_h, cudaStream_t st, float delta_mul, int tile_f16) {
   const int64_t rows = heads * ceil_div(n_q, TILE) * TILE;
   const int g = bwd::grid_for(rows * 4);  // 4 threads per row
-  if (d == 128) bwd::bwd_pre_kernel<128><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul);
-  else if (d == 64) bwd::bwd_pre_kernel<64><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul);
+  if (d == 128)
+    bwd::bwd_pre_kernel<128><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul, tile_f16);
+  else if (d == 64)
+    bwd::bwd_pre_kernel<64><<<g, 256, 0, st>>>(d_o, do_dt, o_ref, o_dt, heads, n_q, delta, do_h, delta_mul, tile_f16);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

@@ -11,8 +11,10 @@ hand-written sm_100a kernels (no library attention):
   S and P^ V on ``kind::f16`` MMAs with fp32 accumulation, the two-pass
   softmax of the FP4 path (L final before the P V pass, 1/l in the epilogue);
 * backward (``aq_attn_bwd_plain``): the K7 skeleton with S recomputed from
-  bf16 Q / K tiles on ``kind::f16``, P = exp(S - L) unquantized for dV and dS,
-  D = rowsum(dO . O) (flash.py:333-351); dQ / dK / dV in TMEM, deterministic;
+  Q / K tiles in the forward's 16-bit format on ``kind::f16`` (so S and L
+  agree), P = exp(S - L) unquantized for dV and dS, D = rowsum(dO . O)
+  (flash.py:333-351), every operand in that format (fp16 with an exact
+  power-of-two gain on dO, or bf16); dQ / dK / dV in TMEM, deterministic;
 * head dims other than 64 / 128 (any d <= 128, e.g. the reference tests' 16 /
   24 / 32) are zero-padded to the next kernel width -- exact: zero Q / K
   columns add nothing to S, zero V columns give zero O columns -- with the
@@ -90,20 +92,42 @@ def plain_forward(q3, k3, v3, causal):
     return o.to(q3.dtype) if o.dtype != q3.dtype else o, lse
 
 
+def _fp16_gain(do3, v3, o3, d):
+    """Exact power-of-two gain for dO in the fp16 backward: every fp16 operand
+    it feeds stays in range -- dO itself and dS = P (dP - D) / sqrt(d), with
+    |dS| <= sqrt(d) |dO| (|V| + |O|) -- while small values keep fp16's
+    precision. The gradients are linear in dO, so dividing them by the gain is
+    exact."""
+    a_do = float(do3.abs().max()) if do3.numel() else 0.0
+    if not (a_do > 0.0) or not math.isfinite(a_do):
+        return 1.0
+    a_vo = max(float(v3.abs().max()) + float(o3.abs().max()), 1e-30)
+    k = min(math.floor(math.log2(2.0 ** 15 / (math.sqrt(d) * a_do * a_vo))), math.floor(math.log2(2.0 ** 15 / a_do)))
+    return 2.0 ** max(-60, min(60, k))
+
+
 def plain_backward(q3, k3, v3, do3, o_ref3, lse2, causal, grad_dtype=None):
     """Unquantized attention backward -> (dQ, dK, dV) [heads, n, d]
-    (flash.py:317-390 with quantized=False) on aq_attn_bwd_plain."""
+    (flash.py:317-390 with quantized=False) on aq_attn_bwd_plain, in the
+    forward's 16-bit format (_compute_dtype on the same Q / K / V): fp16
+    operands with an exact power-of-two gain on dO, or bf16."""
     from . import _lib
     lib = _lib.load()
     heads, n_q, d = q3.shape
     n_k = k3.shape[1]
     if causal and n_q > n_k:
         raise ShapeError("causal attention requires N_q <= N_k")
+    fp16 = _compute_dtype(q3, k3, v3) == torch.float16
+    gain = _fp16_gain(do3, v3, o_ref3, d) if fp16 else 1.0
+    if gain != 1.0:
+        do3 = do3.float() * gain
     D = _kernel_d(d)
     q3, k3, v3 = (_pad(t, D) for t in _operands(q3, k3, v3))
     do3, o_ref3 = (_pad(t, D) for t in _operands(do3, o_ref3))
     lse = lse2.reshape(heads, n_q).to(torch.float32).contiguous()
     g = grad_dtype or q3.dtype
+    if gain != 1.0:
+        g_out, g = g, torch.float32   # divide the gain out in fp32, then round once
     if g not in _lib.DT_CODE:
         raise InvalidValue(f"grad dtype {g} is not float32 / bfloat16 / float16")
     dq = torch.empty((heads, n_q, D), dtype=g, device=q3.device)
@@ -116,7 +140,9 @@ def plain_backward(q3, k3, v3, do3, o_ref3, lse2, causal, grad_dtype=None):
         o_dtype=_lib.DT_CODE[o_ref3.dtype], lse=lse.data_ptr(), heads=heads, n_q=n_q, n_k=n_k, d=D,
         causal=int(causal), variant=0, dq=dq.data_ptr(), dk=dk.data_ptr(), dv=dv.data_ptr(),
         g_dtype=_lib.DT_CODE[g], workspace=ws.data_ptr(), fwd_workspace=None, softmax_scale=1.0 / math.sqrt(d))
-    _lib.check(lib.aq_attn_bwd_plain(args, _lib.stream_ptr()))
+    _lib.check(lib.aq_attn_bwd_plain(args, 0 if fp16 else 1, _lib.stream_ptr()))
     if D != d:
         dq, dk, dv = (t[..., :d].contiguous() for t in (dq, dk, dv))
+    if gain != 1.0:
+        dq, dk, dv = ((t * (1.0 / gain)).to(g_out) for t in (dq, dk, dv))
     return dq, dk, dv

@@ -80,3 +80,16 @@ def test_shape_errors():
         aq.quantize(torch.zeros(4, 12).cuda())
     with pytest.raises(aq.ShapeError):
         aq.quantize(torch.zeros(16).cuda())
+
+
+def test_quantize_cols_c3_ragged_tail_vs_oracle():
+    """C3's N = 32760 (not a multiple of 16): V^T blocked along tokens with the
+    zero-padded tail (quantize_padded(V.T), codec.py:359-361, flash.py:267),
+    byte-identical to the oracle for a full C3 head."""
+    g = torch.Generator().manual_seed(3)
+    v = torch.randn(32760, 128, generator=g).to(torch.bfloat16)
+    qt = aq.quantize_cols(v.cuda())
+    c, s = orc.quantize_padded(v.double().numpy().T)
+    assert qt.codes.shape[-1] * 2 == 32768
+    np.testing.assert_array_equal(qt.codes.cpu().numpy(), c)
+    np.testing.assert_array_equal(qt.scales.cpu().numpy(), s)

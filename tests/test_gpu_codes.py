@@ -65,7 +65,7 @@ def test_quantize_dequantize_block():
         aq.quantize_block(np.zeros(8))
 
 
-@pytest.mark.parametrize("n,d", [(256, 128), (384, 64)])
+@pytest.mark.parametrize("n,d", [(256, 128), (384, 64), (32760, 128)])
 def test_staged_tiles_identical_across_input_paths(n, d):
     # the bf16 fast paths of the tile quantizers (K1 / K2) and the general
     # kernels (taken for fp32 / fp16 inputs) write the same bytes for the same values
