@@ -124,8 +124,19 @@ struct Item {
   int qt, nt;
 };
 
+#ifndef AQ_FWD_SNAKE_ROUNDS
+#define AQ_FWD_SNAKE_ROUNDS 24
+#endif
 __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_tiles, int k_tiles) {
   Item it;
+  if (p.causal && p.heads * q_tiles < AQ_FWD_SNAKE_ROUNDS * static_cast<int64_t>(gridDim.x)) {
+    // few rounds per CTA (e.g. a head shard on one of 8 GPUs): boustrophedon over
+    // the CTAs as in K5, so the per-CTA sums of causal row lengths balance
+    // (32 heads x 32 tiles: makespan / mean 1.14 -> 1.02); with many rounds the
+    // plain order balances by itself and keeps consecutive heads together in L2
+    const int64_t G = gridDim.x, r = w / G;
+    if ((r & 1) && (r + 1) * G <= p.heads * q_tiles) w = r * G + (G - 1 - (w - r * G));
+  }
   if (p.causal && p.head_group > 0) {
     // longest-first within groups of G heads, so the CTAs in flight share the
     // K / V tiles of a few heads in L2 (the 16-bit PLAIN operands are 4x the
