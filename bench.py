@@ -325,11 +325,18 @@ def main():
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("AQ_BENCH_SHARE_DEVICE") == "1":
+        # test hook: several ranks on one GPU (exercises the multi-rank path on a 1-GPU box)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")        # the communicator is visible in the logs
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("AQ_BENCH_BACKEND", "nccl")  # test hook: gloo for ranks sharing a GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     B, H, N, d, causal, mode = cfg
     if mode == "layer":
         run_layer_mode(args, cfg, rank, world, local)

@@ -36,3 +36,19 @@ def test_reference_arm_line():
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+
+
+def test_two_rank_launch_shards_heads():
+    """The --gpus N path end to end on one GPU (two ranks share the device over
+    gloo -- test hooks AQ_BENCH_SHARE_DEVICE / AQ_BENCH_BACKEND; the driver runs
+    NCCL on N GPUs): torchrun self-launch, head sharding, max over ranks, one
+    line from rank 0."""
+    env = dict(os.environ, AQ_BENCH_SHARE_DEVICE="1", AQ_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c1",
+                          "--steps", "3", "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["heads_per_rank"] == 1 and d["scaling"] == "strong" and d["value"] > 0
