@@ -20,7 +20,7 @@ constexpr int kAbiVersion = 3;
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct FwdWs {
-  int64_t q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, v_h16, q_hb, k_hb, v_hb, total;
+  int64_t q_codes, q_sf, k_codes, k_sf, v_codes, v_sf, v_h16, q_hb, k_hb, v_hb, sched, total;
 };
 
 FwdWs fwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int keep) {
@@ -44,6 +44,7 @@ FwdWs fwd_ws(int64_t heads, int64_t n_q, int64_t n_k, int64_t d, int train, int 
   w.q_hb = keep ? take(heads * qt * h_tile_bytes(static_cast<int>(d))) : -1;
   w.k_hb = keep ? take(heads * kt * h_tile_bytes(static_cast<int>(d))) : -1;
   w.v_hb = keep ? take(heads * kt * h_tile_bytes(static_cast<int>(d))) : -1;
+  w.sched = take(256);  // the training kernel's item counter
   w.total = off;
   return w;
 }
@@ -340,6 +341,7 @@ int aq_attn_fwd(const AqFwdArgs* a, void* stream) {
   apply_fwd_scales(p, ts, a->d);
   p.pf_codes = a->pf_codes;
   p.pf_scales = a->pf_scales;
+  p.item_ctr = reinterpret_cast<int*>(ws + w.sched);
   return cuda_status(launch_attn_fwd(p, st));
 }
 

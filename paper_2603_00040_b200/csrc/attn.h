@@ -61,6 +61,9 @@ struct FwdParams {
   // reference's quantize_padded(P) layout per row: codes [heads][n_q][n16/2], scales [heads][n_q][n16/16]
   uint8_t* pf_codes = nullptr;
   uint8_t* pf_scales = nullptr;
+  // K4 dynamic item queue: a workspace int the launch zeroes, or null (static order)
+  int* item_ctr = nullptr;
+  int item_band = 8;  // query tiles per band of the dynamic order
 };
 
 struct BwdParams {

@@ -29,6 +29,7 @@
 // (quantized=False: 16-bit S and P^V on kind::f16) and MX (MXFP4 operands on
 // kind::mxf4 block32, 32-key UE8M0 P blocks).
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -97,9 +98,11 @@ struct Cfg {
   // SAGE: per softmax warp, two 512-byte delta buffers (up to two q_bar rows x 64 keys)
   static constexpr int DL = K1_0 + NK1 * K1_BYTES;
   static constexpr int BARS = DL + (SAGE ? NSW * 1024 : 0);
-  static constexpr int NUM_BARS = 40;
+  static constexpr int NUM_BARS = 48;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
-  static constexpr int USED = TMEM_SLOT + 16;
+  static constexpr int NIQ = 4;                      // dynamic-schedule item ring (ItemQ)
+  static constexpr int IQ = TMEM_SLOT + 16;
+  static constexpr int USED = IQ + NIQ * 8;
   // one CTA per SM (the kernel owns all 512 TMEM columns)
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
   static constexpr int Q_BYTES = PLAIN ? TILE * D * 2 : TILE * D / 2 + (D / 64) * 512;
@@ -109,7 +112,8 @@ struct Cfg {
   static constexpr int B_Q_FULL = 0, B_Q_EMPTY = 1, B_O_FULL = 2, B_O_EMPTY = 3, B_KV_FULL = 4,
                        B_KV_EMPTY = B_KV_FULL + NS, B_S_FULL = B_KV_EMPTY + NS, B_S_EMPTY = B_S_FULL + NB1,
                        B_P_FULL = B_S_EMPTY + NB1, B_P_EMPTY = B_P_FULL + NP, B_K1_FULL = B_P_EMPTY + NP,
-                       B_K1_EMPTY = B_K1_FULL + NK1, B_END = B_K1_EMPTY + NK1;
+                       B_K1_EMPTY = B_K1_FULL + NK1, B_IQ_FULL = B_K1_EMPTY + NK1, B_IQ_EMPTY = B_IQ_FULL + NIQ,
+                       B_END = B_IQ_EMPTY + NIQ;
   static_assert(B_END <= NUM_BARS, "barrier slots");
   static_assert(USED <= 227 * 1024, "shared memory");
   static_assert(T_KSF1 + 8 * NK1 <= 512, "TMEM columns");
@@ -129,7 +133,7 @@ struct Item {
 #endif
 __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_tiles, int k_tiles) {
   Item it;
-  if (p.causal && p.heads * q_tiles < AQ_FWD_SNAKE_ROUNDS * static_cast<int64_t>(gridDim.x)) {
+  if (p.causal && !p.item_ctr && p.heads * q_tiles < AQ_FWD_SNAKE_ROUNDS * static_cast<int64_t>(gridDim.x)) {
     // few rounds per CTA (e.g. a head shard on one of 8 GPUs): boustrophedon over
     // the CTAs as in K5, so the per-CTA sums of causal row lengths balance
     // (32 heads x 32 tiles: makespan / mean 1.14 -> 1.02); with many rounds the
@@ -146,6 +150,27 @@ __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_t
     const int64_t G = min(static_cast<int64_t>(p.head_group), p.heads - g * p.head_group);
     it.qt = q_tiles - 1 - static_cast<int>(r / G);
     it.head = g * p.head_group + r % G;
+    const int64_t last =
+        static_cast<int64_t>(min(it.qt * TILE + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
+    it.nt = min(k_tiles, static_cast<int>(last / TILE) + 1);
+  } else if (p.causal && p.item_ctr) {
+    // dynamic schedule (see next_item): bands of item_band query tiles,
+    // longest band first; inside a band head-major, longest row first. The
+    // CTAs in flight then share each head's K / V / V^F tiles item_band ways in
+    // L2, and the rows left for the queue's tail are at most item_band tiles
+    const int64_t band = min(p.item_band, q_tiles), full = q_tiles / band;
+    int64_t b, r, bs;
+    if (w < full * band * p.heads) {
+      b = w / (band * p.heads);
+      r = w % (band * p.heads);
+      bs = band;
+    } else {
+      b = full;
+      r = w - full * band * p.heads;
+      bs = q_tiles - full * band;
+    }
+    it.head = r / bs;
+    it.qt = q_tiles - 1 - static_cast<int>(b * band + r % bs);
     const int64_t last =
         static_cast<int64_t>(min(it.qt * TILE + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
     it.nt = min(k_tiles, static_cast<int>(last / TILE) + 1);
@@ -222,6 +247,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       mbar_init(&bars[C::B_K1_FULL + s], 1);
       mbar_init(&bars[C::B_K1_EMPTY + s], 1);
     }
+    for (int s = 0; s < C::NIQ; ++s) {
+      mbar_init(&bars[C::B_IQ_FULL + s], 1);
+      mbar_init(&bars[C::B_IQ_EMPTY + s], 2 + C::NSW);  // producer, MMA and softmax warps
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -230,10 +259,31 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Work items. Static: the CTA's k-th item is blockIdx.x + k * gridDim.x.
+  // Dynamic (p.item_ctr, causal rows; work_item's head-major order): producer
+  // 1, the role that runs furthest ahead, claims items from a global counter
+  // (zeroed before the launch; the first item is blockIdx.x, one claim in
+  // flight ahead of use) and publishes them through an NIQ-slot ring; every
+  // other warp reads the ring and releases its slot. -1 = no more items.
+  const bool dyn = p.item_ctr != nullptr;
+  int64_t* iq = reinterpret_cast<int64_t*>(smem + C::IQ);
+  auto next_item = [&](int kk) -> int64_t {
+    if (!dyn) {
+      const int64_t w = blockIdx.x + static_cast<int64_t>(kk) * gridDim.x;
+      return w < n_items ? w : -1;
+    }
+    const int s = kk % C::NIQ;
+    mbar_wait(&bars[C::B_IQ_FULL + s], (kk / C::NIQ) & 1);
+    const int64_t w = iq[s];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[C::B_IQ_EMPTY + s]);
+    return w;
+  };
+
   if (warp == C::PRODUCER) {
     // ------------------------------------------------------------ producer
     int it = 0, k = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
       const Item item = work_item(p, w, q_tiles, k_tiles);
       const int64_t qtile_idx = item.head * q_tiles + item.qt;
       if (k > 0) mbar_wait(&bars[C::B_Q_EMPTY], (k - 1) & 1);
@@ -270,7 +320,25 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
     // K codes + scale factors only (9 KB per tile), NK1 deep, for the S MMAs of
     // both passes, running ahead independently of the large pass-2 stages
     int i1 = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    int claim = 0;  // lane 0: the next claimed item (dynamic)
+    if (dyn && lane == 0) claim = static_cast<int>(gridDim.x) + atomicAdd(p.item_ctr, 1);
+    for (int kk = 0;; ++kk) {
+      int64_t w;
+      if (!dyn) {
+        w = blockIdx.x + static_cast<int64_t>(kk) * gridDim.x;
+        if (w >= n_items) break;
+      } else {
+        w = kk == 0 ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(__shfl_sync(~0u, claim, 0));
+        if (kk > 0 && lane == 0 && w < n_items) claim = static_cast<int>(gridDim.x) + atomicAdd(p.item_ctr, 1);
+        const int s = kk % C::NIQ;
+        if (kk >= C::NIQ) mbar_wait(&bars[C::B_IQ_EMPTY + s], ((kk / C::NIQ) - 1) & 1);
+        if (lane == 0) {
+          iq[s] = w < n_items ? w : -1;
+          mbar_arrive(&bars[C::B_IQ_FULL + s]);
+        }
+        __syncwarp();
+        if (w >= n_items) break;
+      }
       const Item item = work_item(p, w, q_tiles, k_tiles);
       for (int jp = 0; jp < 2 * item.nt; ++jp, ++i1) {
         const int j = jp % item.nt;  // pass 1 then pass 2 re-read the same K tiles
@@ -345,7 +413,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       __syncwarp();
       ++i1;
     };
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
       mbar_wait(&bars[C::B_Q_FULL], k & 1);
       tc_fence_after();
@@ -452,7 +520,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
     AQ_PROF(prof_wait += t1__ - t0__; prof_ld += clock64() - t1__;)           \
   } while (0)
 
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
       const Item item = work_item(p, w, q_tiles, k_tiles);
       const int nt = item.nt;
       const int64_t head = item.head;
@@ -915,6 +983,10 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = p.heads * ceil_div(p.n_q, TILE);
   const int grid = static_cast<int>(items < sms ? items : sms);
+  if (p.item_ctr) {
+    e = cudaMemsetAsync(p.item_ctr, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
   kern<<<grid, C::NUM_THREADS, C::TOTAL, st>>>(p);
   return cudaGetLastError();
 }
@@ -975,9 +1047,24 @@ cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st) {
 cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
   FwdParams p = p_in;
   p.debug = fwd_debug();
+  p.item_band = std::max(1, env_int("AQ_FWD_BAND", 8));
+  const int64_t q_tiles = ceil_div(p.n_q, TILE);
   // inference: the split-pass kernel (attn_fwd_infer.cu); AQ_FWD_INFER=0 keeps
   // it on this kernel (tuning comparisons)
-  if (!p.train && env_int("AQ_FWD_INFER", 1)) return launch_attn_fwd_infer(p, st);
+  if (!p.train && env_int("AQ_FWD_INFER", 1)) {
+    // K5 reads less per tile (no V^F) and is not L2-bound: the dynamic order
+    // pays only for very long causal rows (32 K: 18.3 -> 17.6 ms; 8 K: 1 %
+    // slower, so the snake-ordered static schedule stays below 256 query tiles)
+    if (!p.causal || !env_int("AQ_FWDI_DYN", 1) || q_tiles < env_int("AQ_FWDI_DYN_MIN_QT", 256)) p.item_ctr = nullptr;
+    return launch_attn_fwd_infer(p, st);
+  }
+  // the dynamic item queue serves long causal rows of the training kernel, where
+  // the banded head-major order keeps K / V / V^F in L2 (8 K keys: 4.45 -> 3.89
+  // ms, 16 K: 16.7 -> 14.7 ms at 64 K tokens x 32 heads); below 32 query tiles
+  // the static longest-first order is as fast or faster (1 K keys: -6 % dynamic).
+  // AQ_FWD_DYN=0: static order always; AQ_FWD_BAND: query tiles per band
+  if (!p.causal || !p.train || !env_int("AQ_FWD_DYN", 1) || q_tiles < env_int("AQ_FWD_DYN_MIN_QT", 32))
+    p.item_ctr = nullptr;
   if (fwd_cs() == 2) {
     if (p.d == 64) return p.train ? fwd::launch<64, true, 2>(p, st) : fwd::launch<64, false, 2>(p, st);
     if (p.d == 128) return p.train ? fwd::launch<128, true, 2>(p, st) : fwd::launch<128, false, 2>(p, st);

@@ -106,6 +106,23 @@ def test_c3_early_out_is_exact():
     assert torch.equal(o_t, o_i) and torch.equal(l_t, l_i)
 
 
+@pytest.mark.parametrize("shape", [(8, 32, 4096), (1, 3, 32768)])
+def test_dynamic_item_queue_covers_every_item(shape, monkeypatch):
+    """Causal rows of >= 32 query tiles run K4 on the dynamic item queue (>= 256
+    for K5): every (head, query tile) must be computed exactly once, so O / O' / L
+    equal the static schedule's bit for bit, and K4's O equals K5's."""
+    q, k, v = _inputs(*shape, seed=5)
+    o_d, l_d, ohp_d, _ = aq.attn_forward(q, k, v, causal=True, train=True)
+    oi_d, li_d, _, _ = aq.attn_forward(q, k, v, causal=True, train=False)
+    monkeypatch.setenv("AQ_FWD_DYN", "0")
+    monkeypatch.setenv("AQ_FWDI_DYN", "0")
+    o_s, l_s, ohp_s, _ = aq.attn_forward(q, k, v, causal=True, train=True)
+    oi_s, li_s, _, _ = aq.attn_forward(q, k, v, causal=True, train=False)
+    assert torch.equal(o_d, o_s) and torch.equal(l_d, l_s) and torch.equal(ohp_d, ohp_s)
+    assert torch.equal(oi_d, oi_s) and torch.equal(li_d, li_s)
+    assert torch.equal(o_d, oi_d) and torch.equal(l_d, li_d)
+
+
 @pytest.mark.parametrize("causal", [True, False])
 def test_c4_training_fwd_bwd_full_heads(causal):
     """C4: B8 H32 N4096 d128, fwd + bwd through the autograd Function; two heads
