@@ -37,6 +37,7 @@
 #include "layouts.cuh"
 #include "pquant.cuh"
 #include "ptx.cuh"
+#include "rowstore.cuh"
 
 namespace aq {
 
@@ -501,7 +502,8 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
     SUses su;
     int pc = 0, k = 0;
     AQ_PROF(long long prof_wait = 0, prof_ld = 0, prof_p1 = 0, prof_p2m = 0, prof_pw = 0, prof_q = 0, prof_f = 0;)
-    AQ_PROF(long long p1_wait = 0, p1_ld = 0, tiles = 0;)
+    AQ_PROF(long long p1_wait = 0, p1_ld = 0, tiles = 0, prof_merge = 0, prof_ofull = 0, prof_epi = 0, prof_top = 0, prof_top2 = 0;)
+    AQ_PROF(long long t_item = clock64();)
     AQ_PROF(const long long prof_start = clock64();)
 
 #define AQ_ACQUIRE_S(b_)                                                      \
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
   } while (0)
 
     for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+      AQ_PROF(prof_top += clock64() - t_item;)
       const Item item = work_item(p, w, q_tiles, k_tiles);
       const int nt = item.nt;
       const int64_t head = item.head;
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
         sage_post(jj);
         AQ_PROF(prof_p1 += clock64() - tp1;)
       }
-      AQ_PROF(p1_wait = prof_wait; p1_ld = prof_ld;)
+      AQ_PROF(p1_wait = prof_wait; p1_ld = prof_ld; const long long t_m0 = clock64();)
       // merge the CS column-split partials of each row
       float* ml = reinterpret_cast<float*>(smem + C::ML);
       ml[(half * 2 + 0) * TILE + row] = m;
@@ -712,6 +715,7 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       const float L2 = L_nat * 1.44269504088896340736f;
       const float l_scale = lt;  // P^ = exp(S - m) = P * l
 
+      AQ_PROF(prof_merge += clock64() - t_m0;)
       // pass 2 -- P, P^F (NVFP4 over 16-key blocks), P^ for O'
       for (int jj = 0; jj < nt; ++jj) {
         sage_pre(jj);
@@ -885,8 +889,10 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
 
       // epilogue: this thread's D/CS columns of O (and O' * 1/l) -> registers,
       // release the O columns, then store
+      AQ_PROF(const long long t_e0 = clock64();)
       mbar_wait(&bars[C::B_O_FULL], k & 1);
       tc_fence_after();
+      AQ_PROF(const long long t_e1 = clock64(); prof_ofull += t_e1 - t_e0;)
       const float inv_l = 1.f / l_scale;
       constexpr int DW = D / CS;             // output columns of this thread
       float o[TRAIN ? 2 : 1][DW];
@@ -908,40 +914,29 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars[C::B_O_EMPTY]);
-      if (grow < p.n_q) {
+      AQ_PROF(const long long t_e2 = clock64(); prof_top2 += t_e2 - t_e1;)
+      // stores (rowstore.cuh): in training the P buffers are idle here
+      // (O_FULL: every PV MMA has read them; the next writes are the next
+      // item's pass 2 by these same warps, after the next merge barrier), so
+      // each warp stages its 32 rows there and writes whole row segments
+      constexpr bool STAGE_OUT = TRAIN && C::NSW * 32 * DW * 4 <= C::NP * C::P_BYTES;
+      const int64_t row0 = static_cast<int64_t>(item.qt) * TILE + 32 * (warp & 3);
 #pragma unroll
-        for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
-          void* dst = out ? p.o_hp : p.o;
-          if (dst == nullptr) continue;
-          const int dt = out ? p.o_hp_dt : p.o_dt;
-          const float mul = out ? inv_l * p.ohp_mul : p.o_mul;  // per-tensor scales (1 = reference)
-          const int64_t base = (head * p.n_q + grow) * D + half * DW;
-          if (dt == 0) {
-            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + base);
-#pragma unroll
-            for (int e = 0; e < DW; e += 4)
-              d4[e / 4] = make_float4(o[out][e] * mul, o[out][e + 1] * mul, o[out][e + 2] * mul, o[out][e + 3] * mul);
-          } else {
-            uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(dst) + base);
-#pragma unroll
-            for (int e = 0; e < DW; e += 8) {
-              uint32_t h[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float a = o[out][e + 2 * q] * mul, bb = o[out][e + 2 * q + 1] * mul;
-                if (dt == 1) {
-                  const __nv_bfloat162 v = __floats2bfloat162_rn(a, bb);
-                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
-                } else {
-                  const __half2 v = __floats2half2_rn(a, bb);
-                  h[q] = *reinterpret_cast<const uint32_t*>(&v);
-                }
-              }
-              d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
-            }
-          }
+      for (int out = 0; out < (TRAIN ? 2 : 1); ++out) {
+        void* dst = out ? p.o_hp : p.o;
+        if (dst == nullptr) continue;
+        const int dt = out ? p.o_hp_dt : p.o_dt;
+        const float mul = out ? inv_l * p.ohp_mul : p.o_mul;  // per-tensor scales (1 = reference)
+        const int es = dt == 0 ? 4 : 2;
+        if constexpr (STAGE_OUT) {
+          warp_store_rows<DW>(smem + C::P0 + warp * 32 * DW * 4, lane, o[out], mul, dt,
+                              reinterpret_cast<uint8_t*>(dst) + ((head * p.n_q + row0) * D + half * DW) * es,
+                              static_cast<int64_t>(D) * es, static_cast<int>(p.n_q - row0 < 32 ? p.n_q - row0 : 32));
+        } else if (grow < p.n_q) {
+          store_row<DW>(reinterpret_cast<uint8_t*>(dst) + ((head * p.n_q + grow) * D + half * DW) * es, o[out], mul, dt);
         }
       }
+      AQ_PROF(prof_epi += clock64() - t_e1; t_item = clock64();)
     }
 #undef AQ_ACQUIRE_S
 #ifdef AQ_FWD_PROFILE
@@ -949,7 +944,6 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       atomicAdd(&g_prof[0], static_cast<unsigned long long>(p1_wait));
       atomicAdd(&g_prof[1], static_cast<unsigned long long>(p1_ld));
       atomicAdd(&g_prof[2], static_cast<unsigned long long>(prof_p1));
-      atomicAdd(&g_prof[3], static_cast<unsigned long long>(prof_wait - p1_wait));
       atomicAdd(&g_prof[4], static_cast<unsigned long long>(prof_ld - p1_ld));
       atomicAdd(&g_prof[5], static_cast<unsigned long long>(prof_p2m));
       atomicAdd(&g_prof[6], static_cast<unsigned long long>(prof_pw));
@@ -958,6 +952,11 @@ __global__ void __launch_bounds__(Cfg<D, TRAIN, CS, SAGE, PLAIN, MX>::NUM_THREAD
       atomicAdd(&g_prof[9], static_cast<unsigned long long>(clock64() - prof_start));
       atomicAdd(&g_prof[10], static_cast<unsigned long long>(tiles));
       atomicAdd(&g_prof[11], 1ull);
+      atomicAdd(&g_prof[12], static_cast<unsigned long long>(prof_merge));
+      atomicAdd(&g_prof[13], static_cast<unsigned long long>(prof_ofull));
+      atomicAdd(&g_prof[14], static_cast<unsigned long long>(prof_epi));
+      atomicAdd(&g_prof[15], static_cast<unsigned long long>(prof_top));
+      atomicAdd(&g_prof[3], static_cast<unsigned long long>(prof_top2));
     }
 #else
     (void)prof;

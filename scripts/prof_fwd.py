@@ -20,9 +20,15 @@ torch.cuda.synchronize()
 fn(buf, 0)
 v = list(buf)
 tiles = v[10]
-names = ["p1 S wait", "p1 TMEM ld", "p1 math", "p2 S wait", "p2 TMEM ld", "p2 exp", "p2 P_EMPTY wait", "p2 quant+st",
+# S wait / TMEM ld: both passes (all items but the last one's pass 2), see the kernel
+names = ["S wait", "TMEM ld", "p1 math", "epi: TMEM ld", "-", "p2 exp", "p2 P_EMPTY wait", "p2 quant+st",
          "p2 fence+arrive", "total"]
 print("per warp-tile cycles (averaged over warps):")
 for i, n in enumerate(names):
+    if n != "-":
+        print(f"  {n:18s} {v[i] / tiles:9.1f}")
+for i, n in zip(range(12, 16), ["merge (m, l)", "O_FULL wait", "epilogue ld+st", "next item"]):
     print(f"  {n:18s} {v[i] / tiles:9.1f}")
+acc = sum(v[i] for i in (0, 1, 2, 5, 6, 7, 8, 12, 13, 14, 15))  # [3] is inside [14]
+print(f"  {'unaccounted':18s} {(v[9] - acc) / tiles:9.1f}")
 print("warps", v[11], "tiles", tiles)
