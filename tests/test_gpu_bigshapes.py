@@ -123,6 +123,20 @@ def test_dynamic_item_queue_covers_every_item(shape, monkeypatch):
     assert torch.equal(o_d, oi_d) and torch.equal(l_d, li_d)
 
 
+@pytest.mark.parametrize("shape,d,causal", [((8, 32, 4096), 128, True), ((2, 5, 1100), 128, True),
+                                             ((1, 7, 3000), 64, True), ((2, 3, 2100), 128, False),
+                                             ((1, 4, 1000), 64, False)])
+def test_split_pass_training_forward_matches_k4(shape, d, causal, monkeypatch):
+    """The training forward runs on the split-pass kernel K10 (attn_fwd_qat.cu); K4
+    (AQ_FWD_QAT=0) is the single-stream kernel with the same arithmetic: O, O' and
+    L must agree bit for bit (ragged tails, d = 64, both item orders)."""
+    q, k, v = _inputs(*shape, d=d, seed=7)
+    o10, l10, ohp10, _ = aq.attn_forward(q, k, v, causal=causal, train=True)
+    monkeypatch.setenv("AQ_FWD_QAT", "0")
+    o4, l4, ohp4, _ = aq.attn_forward(q, k, v, causal=causal, train=True)
+    assert torch.equal(o10, o4) and torch.equal(l10, l4) and torch.equal(ohp10, ohp4)
+
+
 @pytest.mark.parametrize("causal", [True, False])
 def test_c4_training_fwd_bwd_full_heads(causal):
     """C4: B8 H32 N4096 d128, fwd + bwd through the autograd Function; two heads
