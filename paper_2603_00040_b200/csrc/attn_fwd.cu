@@ -1057,7 +1057,7 @@ cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
     if (!p.causal || !env_int("AQ_FWDI_DYN", 1) || q_tiles < env_int("AQ_FWDI_DYN_MIN_QT", 256)) p.item_ctr = nullptr;
     return launch_attn_fwd_infer(p, st);
   }
-  // training: the split-pass kernel K10 (attn_fwd_qat.cu; AQ_FWD_QAT=0 keeps
+  // training: the split-pass kernel K11 (attn_fwd_qat.cu; AQ_FWD_QAT=0 keeps
   // K4), on the dynamic banded item order for causal rows from 8 query tiles
   // (C4: 2.07 -> 1.78 ms against its static order, 1 K keys 1.43 -> 1.37, 2 K
   // 2.32 -> 2.07; K4 on its best order: 2.11 / 1.51 / 2.39 ms)

@@ -1,4 +1,4 @@
-// K10: NVFP4 training forward, split-pass (sm_100a).
+// K11: NVFP4 training forward, split-pass (sm_100a).
 //
 // flash_forward_training (attnqat/flash.py:176-246): O = P^F V^F, O' = P V^F
 // and L for each 128-row query tile, on K5's two-stream structure

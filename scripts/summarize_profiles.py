@@ -101,10 +101,16 @@ for rep in ("attn_fwd_c2", "attn_fwd_c3", "attn_fwd_train_c4", "attn_bwd_c4", "a
     with open(os.path.join(DST, f"{TAG}_ncu_{rep}.txt"), "w") as fh:
         fh.write("\n".join(txt) + "\n")
 
-# bench.py reads profiles/ncu_summary.json for roofline.traffic (config -> dominant kernel)
-bench_map = {"c2": summary["attn_fwd_c2"][0], "c4": summary["attn_bwd_c4"][0]}
-if "attn_fwd_c3" in summary:
-    bench_map["c3"] = summary["attn_fwd_c3"][0]
-with open(os.path.join(DST, "ncu_summary.json"), "w") as fh:
-    json.dump({"round": TAG, **bench_map, "all": summary}, fh, indent=1)
+# bench.py reads profiles/ncu_summary.json for roofline.traffic (config -> dominant kernel);
+# a partial capture updates the existing entries
+jpath = os.path.join(DST, "ncu_summary.json")
+prev = json.load(open(jpath)) if os.path.exists(jpath) else {}
+bench_map = {c: prev[c] for c in ("c2", "c3", "c4") if c in prev}
+for cfg, rep in (("c2", "attn_fwd_c2"), ("c3", "attn_fwd_c3"), ("c4", "attn_bwd_c4")):
+    if rep in summary:
+        bench_map[cfg] = summary[rep][0]
+allmap = dict(prev.get("all", {}))
+allmap.update(summary)
+with open(jpath, "w") as fh:
+    json.dump({"round": TAG, **bench_map, "all": allmap}, fh, indent=1)
 print("wrote", sorted(os.listdir(DST)))

@@ -127,7 +127,7 @@ def test_dynamic_item_queue_covers_every_item(shape, monkeypatch):
                                              ((1, 7, 3000), 64, True), ((2, 3, 2100), 128, False),
                                              ((1, 4, 1000), 64, False)])
 def test_split_pass_training_forward_matches_k4(shape, d, causal, monkeypatch):
-    """The training forward runs on the split-pass kernel K10 (attn_fwd_qat.cu); K4
+    """The training forward runs on the split-pass kernel K11 (attn_fwd_qat.cu); K4
     (AQ_FWD_QAT=0) is the single-stream kernel with the same arithmetic: O, O' and
     L must agree bit for bit (ragged tails, d = 64, both item orders)."""
     q, k, v = _inputs(*shape, d=d, seed=7)
