@@ -48,9 +48,22 @@
 #ifndef AQ_QAT_REGB
 #define AQ_QAT_REGB 56
 #endif
+// how many S_B tiles MMA B may issue ahead of the PV MMAs
+#ifndef AQ_QAT_SLEAD
+#define AQ_QAT_SLEAD 1
+#endif
 
 namespace aq {
 namespace fwdq {
+
+// Tuning aid (-DAQ_FWDQ_PROFILE, enabled by AQ_FWD_DEBUG bit 32): cycle sums of
+// the softmax groups' waits, from lane 0 of every warp (aq_debug_fwdq_profile).
+__device__ unsigned long long g_qprof[16];
+#ifdef AQ_FWDQ_PROFILE
+#define AQ_QPROF(...) __VA_ARGS__
+#else
+#define AQ_QPROF(...)
+#endif
 
 template <int D>
 struct Cfg {
@@ -66,7 +79,9 @@ struct Cfg {
   static constexpr int REG_P = 40, REG_B = AQ_QAT_REGB,
                        REG_A = ((POOL - 128 * REG_P - 32 * NSWB * REG_B) / (32 * NSW)) / 8 * 8;
   static_assert(128 * REG_P + 32 * NSWB * REG_B + 32 * NSW * REG_A <= POOL, "register pool");
-  static constexpr int NQ = 2, NSA = 2, NSB = 2, NP = 2;  // Q slots, ring depths, P buffers
+  // Q slots, ring depths (A: K; B: K and V separately, so B's next K tile does
+  // not wait for a 41 KB V stage to drain), P buffers
+  static constexpr int NQ = 2, NSA = 2, NSBK = 2, NSB = 2, NP = 2;
   // TMEM: S_A (half tiles) 64, S_B 128, O 128, O' 128, scale factors 64
   static constexpr uint32_t T_SA = 0, T_SB = 64, T_O = 192, T_OP = 320;
   static constexpr uint32_t T_QSF = 448, T_KSFA = T_QSF + 8 * NQ, T_KSFB = T_KSFA + 8, T_PSF = T_KSFB + 8,
@@ -75,15 +90,16 @@ struct Cfg {
   static constexpr int QC_BYTES = TILE * D / 2, QSF_BYTES = (D / 64) * 512, Q_BYTES = QC_BYTES + QSF_BYTES;
   static constexpr int Q0 = 0;                                         // NQ Q slots
   static constexpr int KA0 = Q0 + NQ * Q_BYTES, KA_BYTES = Q_BYTES;    // ring A: K codes + SF
-  static constexpr int KB0 = KA0 + NSA * KA_BYTES;                     // ring B: K + V^T + SF + V^F
-  static constexpr int KB_V = KA_BYTES, KB_VSF = KB_V + TILE * D / 2, KB_VH = KB_VSF + 1024;
+  static constexpr int KBK0 = KA0 + NSA * KA_BYTES;                    // ring BK: K codes + SF
+  static constexpr int KB0 = KBK0 + NSBK * KA_BYTES;                   // ring BV: V^T + SF + V^F
+  static constexpr int KB_V = 0, KB_VSF = KB_V + TILE * D / 2, KB_VH = KB_VSF + 1024;
   static constexpr int KB_BYTES = KB_VH + TILE * D * 2;
   static constexpr int P0 = KB0 + NSB * KB_BYTES;                      // P^F codes + SF + P^ fp16
   static constexpr int PB_SF = TILE * TILE / 2, PB_H = PB_SF + 1024, P_BYTES = PB_H + TILE * TILE * 2;
   static constexpr int ML = P0 + NP * P_BYTES;                         // pass-1 (m, l) partials [CS][2][TILE]
   static constexpr int LB = ML + CS * 2 * TILE * 4;                    // (L, l) handoff [NQ][2][TILE]
   static constexpr int BARS = LB + NQ * 2 * TILE * 4;
-  static constexpr int NUM_BARS = 40;
+  static constexpr int NUM_BARS = 48;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
   static constexpr int NIQ = 4;                                        // dynamic-schedule item ring
   static constexpr int IQ = TMEM_SLOT + 16;
@@ -95,7 +111,8 @@ struct Cfg {
                        B_O_EMPTY = B_O_FULL + 1, B_SA_FULL = B_O_EMPTY + 1, B_SA_EMPTY = B_SA_FULL + 2,
                        B_SB_FULL = B_SA_EMPTY + 2, B_SB_EMPTY = B_SB_FULL + 1, B_KA_FULL = B_SB_EMPTY + 1,
                        B_KA_EMPTY = B_KA_FULL + NSA, B_KB_FULL = B_KA_EMPTY + NSA, B_KB_EMPTY = B_KB_FULL + NSB,
-                       B_P_FULL = B_KB_EMPTY + NSB, B_P_EMPTY = B_P_FULL + NP, B_QSF = B_P_EMPTY + NP,
+                       B_KBK_FULL = B_KB_EMPTY + NSB, B_KBK_EMPTY = B_KBK_FULL + NSBK,
+                       B_P_FULL = B_KBK_EMPTY + NSBK, B_P_EMPTY = B_P_FULL + NP, B_QSF = B_P_EMPTY + NP,
                        B_IQ_FULL = B_QSF + NQ, B_IQ_EMPTY = B_IQ_FULL + NIQ, B_END = B_IQ_EMPTY + NIQ;
   static_assert(B_END <= NUM_BARS, "barriers");
 };
@@ -182,6 +199,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
     for (int s = 0; s < C::NSA; ++s) {
       mbar_init(&bars[C::B_KA_FULL + s], 1);
       mbar_init(&bars[C::B_KA_EMPTY + s], 1);
+    }
+    for (int s = 0; s < C::NSBK; ++s) {
+      mbar_init(&bars[C::B_KBK_FULL + s], 1);
+      mbar_init(&bars[C::B_KBK_EMPTY + s], 1);
     }
     for (int s = 0; s < C::NSB; ++s) {
       mbar_init(&bars[C::B_KB_FULL + s], 1);
@@ -277,6 +298,18 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
       for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
         const Item item = work_item(p, w, q_tiles, k_tiles);
         for (int j = 0; j < item.nt; ++j, ++it) {
+          const int64_t kidx0 = item.head * k_tiles + j;
+          // K of this tile (S_B) first: its ring drains as soon as the S MMA completes
+          const int sk = it % C::NSBK;
+          if (it >= C::NSBK) mbar_wait(&bars[C::B_KBK_EMPTY + sk], ((it / C::NSBK) - 1) & 1);
+          if (elect_one()) {
+            uint64_t* fb = &bars[C::B_KBK_FULL + sk];
+            uint8_t* kb = smem + C::KBK0 + sk * C::KA_BYTES;
+            mbar_expect_tx(fb, C::KA_BYTES);
+            bulk_g2s(kb, p.k_codes + kidx0 * fp4_tile_bytes(D), C::QC_BYTES, fb);
+            bulk_g2s(kb + C::QC_BYTES, p.k_sf + kidx0 * sf_tile_bytes_qk(D), C::QSF_BYTES, fb);
+          }
+          __syncwarp();
           const int st = it % C::NSB;
           if (it >= C::NSB) mbar_wait(&bars[C::B_KB_EMPTY + st], ((it / C::NSB) - 1) & 1);
           const int64_t kidx = item.head * k_tiles + j;
@@ -284,8 +317,6 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
             uint64_t* fb = &bars[C::B_KB_FULL + st];
             uint8_t* sb = smem + C::KB0 + st * C::KB_BYTES;
             mbar_expect_tx(fb, (p.debug & 4) ? C::KB_VH : C::KB_BYTES);
-            bulk_g2s(sb, p.k_codes + kidx * fp4_tile_bytes(D), C::QC_BYTES, fb);
-            bulk_g2s(sb + C::QC_BYTES, p.k_sf + kidx * sf_tile_bytes_qk(D), C::QSF_BYTES, fb);
             bulk_g2s(sb + C::KB_V, p.v_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, fb);
             bulk_g2s(sb + C::KB_VSF, p.v_sf + kidx * kSfTileBytesV, 1024, fb);
             if (!(p.debug & 4)) bulk_g2s(sb + C::KB_VH, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, fb);
@@ -357,13 +388,13 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           mbar_wait(&bars[C::B_QSF + qs], (k / C::NQ) & 1);
           tc_fence_after();
           for (int ns = 0, np = 0; np < nt;) {
-            if (ns < nt && ns <= np + 1) {
-              const int st = (it + ns) % C::NSB;
-              mbar_wait(&bars[C::B_KB_FULL + st], ((it + ns) / C::NSB) & 1);
+            if (ns < nt && ns <= np + AQ_QAT_SLEAD) {
+              const int sk = (it + ns) % C::NSBK;
+              mbar_wait(&bars[C::B_KBK_FULL + sk], ((it + ns) / C::NSBK) & 1);
               if (su > 0) mbar_wait(&bars[C::B_SB_EMPTY], (su - 1) & 1);  // also: the K SF slot's reader completed
               ++su;
               tc_fence_after();
-              const uint32_t kb = s0 + C::KB0 + st * C::KB_BYTES;
+              const uint32_t kb = s0 + C::KBK0 + sk * C::KA_BYTES;
               if (elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < D / 64; ++ks)
@@ -373,6 +404,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
                   mma_nvf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
                               tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFB + 4 * ks, ks > 0);
                 tc_commit(&bars[C::B_SB_FULL]);
+                tc_commit(&bars[C::B_KBK_EMPTY + sk]);
                 if (ns == nt - 1) tc_commit(&bars[C::B_Q_EMPTY + qs]);  // last read of this Q slot
               }
               __syncwarp();
@@ -383,6 +415,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
             const int pb = pc % C::NP;
             const int st = (it + pj) % C::NSB;
             if (pj == 0 && k > 0) mbar_wait(&bars[C::B_O_EMPTY], (k - 1) & 1);  // previous epilogue read O, O'
+            mbar_wait(&bars[C::B_KB_FULL + st], ((it + pj) / C::NSB) & 1);     // V^T, V^F of this tile landed
             mbar_wait(&bars[C::B_P_FULL + pb], (pc / C::NP) & 1);
             ++pc;
             tc_fence_after();
@@ -424,6 +457,24 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
     float* ml = reinterpret_cast<float*>(smem + C::ML);
     float* lb = reinterpret_cast<float*>(smem + C::LB);
     int su = 0, k = 0;
+    AQ_QPROF(long long qpa[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; const long long qstart_all = clock64();)
+    // per-group wait sums into g_qprof: A [0] S_A, [1] L_EMPTY, [2] total, [3] tiles;
+    // B [8] S_B, [9] L_FULL, [10] P_EMPTY, [11] O_FULL, [13] tiles, [14] total
+    auto qdump = [&](bool ga) {
+      AQ_QPROF(if ((p.debug & 32) && lane == 0) {
+        const long long tot = clock64() - qstart_all;
+        if (ga) {
+          atomicAdd(&g_qprof[0], static_cast<unsigned long long>(qpa[0]));
+          atomicAdd(&g_qprof[1], static_cast<unsigned long long>(qpa[1]));
+          atomicAdd(&g_qprof[2], static_cast<unsigned long long>(tot));
+          atomicAdd(&g_qprof[3], static_cast<unsigned long long>(qpa[3]));
+        } else {
+          for (int e = 4; e < 10; ++e) atomicAdd(&g_qprof[e + 4], static_cast<unsigned long long>(qpa[e]));
+          atomicAdd(&g_qprof[14], static_cast<unsigned long long>(tot));
+        }
+      })
+      (void)ga;
+    };
     if (grp_a) {
       setmaxnreg_inc<C::REG_A>();
       constexpr int CW = C::CW;
@@ -441,7 +492,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
         float m = -INFINITY, l = 0.f;
         for (int jj = 0; jj < nt; ++jj) {
           // this half's 64 keys of the tile, from the shared half-tile buffer
+          AQ_QPROF(long long t0 = clock64();)
           mbar_wait(&bars[C::B_SA_FULL + half], su & 1);
+          AQ_QPROF(qpa[0] += clock64() - t0; qpa[3] += 1;)
           ++su;
           tc_fence_after();
 #pragma unroll
@@ -501,13 +554,16 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
         // rebuilds L2 = fl(L) * log2(e) like K4 and the backward
         const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
         if (half == 0 && grow < p.n_q) p.lse[item.head * p.n_q + grow] = L_nat;
+        AQ_QPROF(long long t1 = clock64();)
         if (k >= C::NQ) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k / C::NQ) - 1) & 1);
+        AQ_QPROF(qpa[1] += clock64() - t1;)
         if (half == 0) {
           lb[(qs * 2 + 0) * TILE + row] = L_nat;
           lb[(qs * 2 + 1) * TILE + row] = lt;
         }
         mbar_arrive(&bars[C::B_L_FULL + qs]);
       }
+      qdump(true);
     } else {
       setmaxnreg_dec<C::REG_B>();
       constexpr int CW = C::CWB;  // 32 keys per thread
@@ -525,7 +581,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
         float L2 = 0.f, l_scale = 0.f;
         // ---------------- pass 2: P, P^F (NVFP4 over 16-key blocks), P^ for O'
         for (int jj = 0; jj < nt; ++jj) {
+          AQ_QPROF(long long t0 = clock64();)
           mbar_wait(&bars[C::B_SB_FULL], su & 1);
+          AQ_QPROF(qpa[4] += clock64() - t0; qpa[9] += 1;)
           ++su;
           tc_fence_after();
           tmem_ld32f(t_lane + C::T_SB + cbase, x);
@@ -533,7 +591,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           tc_fence_before();
           mbar_arrive(&bars[C::B_SB_EMPTY]);
           if (jj == 0) {  // after the first S load, so MMA B can refill the buffer meanwhile
+            AQ_QPROF(long long t1 = clock64();)
             mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
+            AQ_QPROF(qpa[5] += clock64() - t1;)
             L2 = lb[(qs * 2 + 0) * TILE + row] * 1.44269504088896340736f;
             l_scale = lb[(qs * 2 + 1) * TILE + row];  // P^ = exp(S - m) = P * l
             mbar_arrive(&bars[C::B_L_EMPTY + qs]);
@@ -545,7 +605,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
             for (int c = 0; c < CW; ++c) x[c] = (c <= lim) ? x[c] : 0.f;
           }
           const int pb = pc % C::NP;
+          AQ_QPROF(long long t2 = clock64();)
           if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
+          AQ_QPROF(qpa[6] += clock64() - t2;)
           ++pc;
           uint8_t* pbase = smem + C::P0 + pb * C::P_BYTES;
           uint8_t* psf = pbase + C::PB_SF;
@@ -587,7 +649,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           mbar_arrive(&bars[C::B_P_FULL + pb]);
         }
         // ---------------- epilogue: D / 4 columns of O, then of O' * 1/l
+        AQ_QPROF(long long t3 = clock64();)
         mbar_wait(&bars[C::B_O_FULL], k & 1);
+        AQ_QPROF(qpa[7] += clock64() - t3;)
         tc_fence_after();
         constexpr int DW = D / C::CSB;
         const float inv_l = 1.f / l_scale;
@@ -618,6 +682,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           }
         }
       }
+      qdump(false);
     }
   }
 
@@ -649,6 +714,17 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 }
 
 }  // namespace fwdq
+
+// [0] group A S_A wait, [1] A L_EMPTY wait, [2] A total, [3] A tiles (warp-tiles),
+// [8] B S_B wait, [9] B L_FULL wait, [10] B P_EMPTY wait, [11] B O_FULL wait, [13] B tiles, [14] B total
+extern "C" int aq_debug_fwdq_profile(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, fwdq::g_qprof, sizeof(fwdq::g_qprof)) != cudaSuccess) return 5;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(fwdq::g_qprof, z, sizeof(z)) != cudaSuccess) return 5;
+  }
+  return 0;
+}
 
 cudaError_t launch_attn_fwd_qat(const FwdParams& p, cudaStream_t st) {
   if (p.d == 64) return fwdq::launch<64>(p, st);
