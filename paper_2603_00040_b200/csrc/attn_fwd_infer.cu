@@ -54,6 +54,17 @@
 namespace aq {
 namespace fwdi {
 
+// Tuning aid (-DAQ_FWDI_PROFILE, enabled by AQ_FWD_DEBUG bit 32): cycle sums of
+// the softmax groups' waits, from lane 0 of every warp (aq_debug_fwdi_profile):
+// A [0] S wait, [1] L_EMPTY wait, [2] total, [3] tiles;
+// B [8] S wait, [9] L_FULL wait, [10] P_EMPTY wait, [11] O_FULL wait, [13] tiles, [14] total
+__device__ unsigned long long g_iprof[16];
+#ifdef AQ_FWDI_PROFILE
+#define AQ_IPROF(...) __VA_ARGS__
+#else
+#define AQ_IPROF(...)
+#endif
+
 #ifndef AQ_FWDI_CSB
 #define AQ_FWDI_CSB 4
 #endif
@@ -474,6 +485,22 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     const float p_r = p.p_r;  // 1 / t_p (1 = the reference's P^F)
     float x[CW];
     int su = 0, pc = 0, k = 0;
+    AQ_IPROF(long long ipa[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; const long long istart = clock64();)
+    auto idump = [&](bool ga) {
+      AQ_IPROF(if ((p.debug & 32) && lane == 0) {
+        const long long tot = clock64() - istart;
+        if (ga) {
+          atomicAdd(&g_iprof[0], static_cast<unsigned long long>(ipa[0]));
+          atomicAdd(&g_iprof[1], static_cast<unsigned long long>(ipa[1]));
+          atomicAdd(&g_iprof[2], static_cast<unsigned long long>(tot));
+          atomicAdd(&g_iprof[3], static_cast<unsigned long long>(ipa[3]));
+        } else {
+          for (int e = 4; e < 10; ++e) atomicAdd(&g_iprof[e + 4], static_cast<unsigned long long>(ipa[e]));
+          atomicAdd(&g_iprof[14], static_cast<unsigned long long>(tot));
+        }
+      })
+      (void)ga;
+    };
     int chk_wait = 0, chk_pen = 0;  // early-out back-off (warp-uniform)
     const bool early_out = EARLY && (p.debug & 64) == 0;  // AQ_FWD_DEBUG bit 64 disables it (A/B timing)
     float* ml = reinterpret_cast<float*>(smem + C::ML);
@@ -493,7 +520,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           // bit-identical between the two forward kernels.
           float m = -INFINITY, l = 0.f;
           for (int jj = 0; jj < nt; ++jj) {
+            AQ_IPROF(long long t0 = clock64();)
             mbar_wait(&bars[C::B_SA_FULL], su & 1);
+            AQ_IPROF(ipa[0] += clock64() - t0; ipa[3] += 1;)
             ++su;
             tc_fence_after();
   #pragma unroll
@@ -560,10 +589,13 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           // rebuilds L2 = fl(L) * log2(e) exactly like the backward does
           const float L_nat = (mt + __log2f(lt)) * 0.69314718055994530942f;
           if (half == 0 && grow < p.n_q) p.lse[item.head * p.n_q + grow] = L_nat;
+          AQ_IPROF(long long t1 = clock64();)
           if (k >= C::NQ) mbar_wait(&bars[C::B_L_EMPTY + qs], ((k / C::NQ) - 1) & 1);
+          AQ_IPROF(ipa[1] += clock64() - t1;)
           if (half == 0) lb[qs * TILE + row] = L_nat;
           mbar_arrive(&bars[C::B_L_FULL + qs]);
       }
+      idump(true);
     } else {
       if constexpr (C::REALLOC) setmaxnreg_dec<C::REG_B>();
       for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
@@ -577,12 +609,16 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
           constexpr int CW = C::CWB;
           const int half = gw >> 2;  // column split of this thread (pass 2)
           const int cbase = half * CW;
+          AQ_IPROF(long long t1 = clock64();)
           mbar_wait(&bars[C::B_L_FULL + qs], (k / C::NQ) & 1);
+          AQ_IPROF(ipa[5] += clock64() - t1;)
           const float L2 = lb[qs * TILE + row] * 1.44269504088896340736f;
           mbar_arrive(&bars[C::B_L_EMPTY + qs]);
           const float thr = p_skip_thr(L2 + p.p_lshift, sl2);  // blocks of P * p_r below 2^-11
           for (int jj = 0; jj < nt; ++jj) {
+            AQ_IPROF(long long t0 = clock64();)
             mbar_wait(&bars[C::B_SB_FULL], su & 1);
+            AQ_IPROF(ipa[4] += clock64() - t0; ipa[9] += 1;)
             ++su;
             tc_fence_after();
   #pragma unroll
@@ -595,7 +631,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             // stores form one straight-line block per 32 keys that the scheduler can
             // interleave (MUFU work of one group overlaps ALU work of the previous)
             const int pb = pc % C::NP;
+            AQ_IPROF(long long t2 = clock64();)
             if (pc >= C::NP) mbar_wait(&bars[C::B_P_EMPTY + pb], ((pc / C::NP) - 1) & 1);
+            AQ_IPROF(ipa[6] += clock64() - t2;)
             ++pc;
             uint8_t* pcodes = smem + C::P0 + pb * C::P_BYTES;
             uint8_t* psf = pcodes + C::PB_SF;
@@ -704,7 +742,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             mbar_arrive(&bars[C::B_P_FULL + pb]);
           }
           // epilogue: O rows -> registers, release O, store
+          AQ_IPROF(long long t3 = clock64();)
           mbar_wait(&bars[C::B_O_FULL], k & 1);
+          AQ_IPROF(ipa[7] += clock64() - t3;)
           tc_fence_after();
           constexpr int DW = D / C::CSB;
           float o[DW];
@@ -750,6 +790,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
             }
           }
       }
+      idump(false);
     }
   }
 
@@ -789,6 +830,15 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
 }
 
 }  // namespace fwdi
+
+extern "C" int aq_debug_fwdi_profile(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, fwdi::g_iprof, sizeof(fwdi::g_iprof)) != cudaSuccess) return 5;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(fwdi::g_iprof, z, sizeof(z)) != cudaSuccess) return 5;
+  }
+  return 0;
+}
 
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st) {
   if (p.d == 64) return fwdi::launch<64>(p, st);

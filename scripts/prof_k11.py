@@ -1,5 +1,6 @@
-"""Wait breakdown of the split-pass training forward's softmax groups (K11,
-built with -DAQ_FWDQ_PROFILE, AQ_FWD_DEBUG=32). GPU.
+"""Wait breakdown of the split-pass forwards' softmax groups: K11 (training,
+built with -DAQ_FWDQ_PROFILE) or, with AQ_PROF_INFER=1, K5 (inference,
+-DAQ_FWDI_PROFILE); AQ_FWD_DEBUG=32. GPU.
     python scripts/prof_k11.py [B H N d causal]"""
 import ctypes
 import os
@@ -12,17 +13,18 @@ import paper_2603_00040_b200 as aq  # noqa: E402
 from paper_2603_00040_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
-fn = lib.aq_debug_fwdq_profile
+infer = os.environ.get("AQ_PROF_INFER", "0") == "1"
+fn = lib.aq_debug_fwdi_profile if infer else lib.aq_debug_fwdq_profile
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 a = sys.argv[1:]
 B, H, N, d = (int(x) for x in a[:4]) if len(a) >= 4 else (8, 32, 4096, 128)
 causal = (a[4] != "0") if len(a) > 4 else True
 q, k, v = (torch.randn(B, H, N, d, device="cuda").bfloat16() for _ in range(3))
-o, lse, _, ws = aq.attn_forward(q, k, v, causal=causal, train=True)
+o, lse, _, ws = aq.attn_forward(q, k, v, causal=causal, train=not infer)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 16)()
 fn(buf, 1)
-aq.attn_forward(q, k, v, causal=causal, train=True, workspace=ws, operands_staged=True)
+aq.attn_forward(q, k, v, causal=causal, train=not infer, workspace=ws, operands_staged=True)
 torch.cuda.synchronize()
 fn(buf, 0)
 v = list(buf)
