@@ -1051,10 +1051,10 @@ cudaError_t launch_attn_fwd(const FwdParams& p_in, cudaStream_t st) {
   // inference: the split-pass kernel (attn_fwd_infer.cu); AQ_FWD_INFER=0 keeps
   // it on this kernel (tuning comparisons)
   if (!p.train && env_int("AQ_FWD_INFER", 1)) {
-    // K5 reads less per tile (no V^F) and is not L2-bound: the dynamic order
-    // pays only for very long causal rows (32 K: 18.3 -> 17.6 ms; 8 K: 1 %
-    // slower, so the snake-ordered static schedule stays below 256 query tiles)
-    if (!p.causal || !env_int("AQ_FWDI_DYN", 1) || q_tiles < env_int("AQ_FWDI_DYN_MIN_QT", 256)) p.item_ctr = nullptr;
+    // K5 keeps its static snake order: it reads no V^F and is not L2-bound; a
+    // dynamic queue cost it 1 % at C2 and 4 % at C3 (ring reads, registers)
+    // for 4 % at 32 K causal
+    p.item_ctr = nullptr;
     return launch_attn_fwd_infer(p, st);
   }
   // training: the split-pass kernel K11 (attn_fwd_qat.cu; AQ_FWD_QAT=0 keeps

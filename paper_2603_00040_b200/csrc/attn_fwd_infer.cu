@@ -119,9 +119,7 @@ struct Cfg {
   static constexpr int BARS = LB + NQ * TILE * 4;
   static constexpr int NUM_BARS = 48;
   static constexpr int TMEM_SLOT = BARS + NUM_BARS * 8;
-  static constexpr int NIQ = 4;                     // dynamic-schedule item ring
-  static constexpr int IQ = TMEM_SLOT + 16;
-  static constexpr int USED = IQ + NIQ * 8;
+  static constexpr int USED = TMEM_SLOT + 16;
   static constexpr int TOTAL = USED > 120 * 1024 ? USED : 120 * 1024;
   // barriers
   static constexpr int B_Q_FULL = 0, B_Q_EMPTY = NQ, B_L_FULL = 2 * NQ, B_L_EMPTY = 3 * NQ, B_QSF = 4 * NQ,
@@ -129,7 +127,7 @@ struct Cfg {
                        B_SA_EMPTY = B_SA_FULL + 1, B_SB_FULL = B_SA_EMPTY + 1, B_SB_EMPTY = B_SB_FULL + 1,
                        B_KA_FULL = B_SB_EMPTY + 1, B_KA_EMPTY = B_KA_FULL + NSA, B_KB_FULL = B_KA_EMPTY + NSA,
                        B_KB_EMPTY = B_KB_FULL + NSB, B_P_FULL = B_KB_EMPTY + NSB, B_P_EMPTY = B_P_FULL + NP,
-                       B_IQ_FULL = B_P_EMPTY + NP, B_IQ_EMPTY = B_IQ_FULL + NIQ, B_END = B_IQ_EMPTY + NIQ;
+                       B_END = B_P_EMPTY + NP;
   static_assert(B_END <= NUM_BARS, "barriers");
   static_assert(USED <= 227 * 1024, "shared memory");
   static_assert(T_VSF + 8 * NSB <= 512, "TMEM columns");
@@ -143,27 +141,6 @@ struct Item {
 // Same item order as attn_fwd.cu: causal rows longest first across heads.
 __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w, int q_tiles, int k_tiles) {
   Item it;
-  if (p.causal && p.item_ctr) {
-    // dynamic schedule (K4's banded order, attn_fwd.cu work_item): bands of
-    // item_band query tiles longest first, head-major inside a band
-    const int64_t band = min(p.item_band, q_tiles), full = q_tiles / band;
-    int64_t b, r, bs;
-    if (w < full * band * p.heads) {
-      b = w / (band * p.heads);
-      r = w % (band * p.heads);
-      bs = band;
-    } else {
-      b = full;
-      r = w - full * band * p.heads;
-      bs = q_tiles - full * band;
-    }
-    it.head = r / bs;
-    it.qt = q_tiles - 1 - static_cast<int>(b * band + r % bs);
-    const int64_t last =
-        static_cast<int64_t>(min(it.qt * TILE + TILE - 1, static_cast<int>(p.n_q) - 1)) + (p.n_k - p.n_q);
-    it.nt = min(k_tiles, static_cast<int>(last / TILE) + 1);
-    return it;
-  }
   if (AQ_FWDI_SNAKE && p.causal) {
     // boustrophedon over the persistent CTAs: CTA c takes the c-th item of even
     // rounds and the (G-1-c)-th of odd full rounds, so every CTA's sum of
@@ -230,10 +207,6 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       mbar_init(&bars[C::B_P_FULL + s], GRPB);
       mbar_init(&bars[C::B_P_EMPTY + s], 1);
     }
-    for (int s = 0; s < C::NIQ; ++s) {
-      mbar_init(&bars[C::B_IQ_FULL + s], 1);
-      mbar_init(&bars[C::B_IQ_EMPTY + s], C::MMA_B);  // every warp but producer A
-    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -248,24 +221,6 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   constexpr uint32_t id_s = idesc_nvf4(128, 128);
   constexpr uint32_t id_pv = idesc_nvf4(128, D);
 
-  // Work items: static (blockIdx.x + k * gridDim.x) or, with p.item_ctr
-  // (causal), claimed by producer A from a global counter and published
-  // through an NIQ-slot ring that every other warp reads (as in K4). -1 = done.
-  const bool dyn = p.item_ctr != nullptr;
-  int64_t* iq = reinterpret_cast<int64_t*>(smem + C::IQ);
-  auto next_item = [&](int kk) -> int64_t {
-    if (!dyn) {
-      const int64_t w = blockIdx.x + static_cast<int64_t>(kk) * gridDim.x;
-      return w < n_items ? w : -1;
-    }
-    const int s = kk % C::NIQ;
-    mbar_wait(&bars[C::B_IQ_FULL + s], (kk / C::NIQ) & 1);
-    const int64_t w = iq[s];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&bars[C::B_IQ_EMPTY + s]);
-    return w;
-  };
-
   if (warp >= C::PROD_A) {
   // producer / MMA warpgroup: few registers (setmaxnreg inside each role branch,
   // so the limit applies to that branch only)
@@ -273,25 +228,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   if (warp == C::PROD_A) {
     // ------------------------------------------------------------ producer A: Q + K for pass 1
     int it = 0, k = 0;
-    int claim = 0;  // lane 0: the next claimed item (dynamic)
-    if (dyn && lane == 0) claim = static_cast<int>(gridDim.x) + atomicAdd(p.item_ctr, 1);
-    for (;; ++k) {
-      int64_t w;
-      if (!dyn) {
-        w = blockIdx.x + static_cast<int64_t>(k) * gridDim.x;
-        if (w >= n_items) break;
-      } else {
-        w = k == 0 ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(__shfl_sync(~0u, claim, 0));
-        if (k > 0 && lane == 0 && w < n_items) claim = static_cast<int>(gridDim.x) + atomicAdd(p.item_ctr, 1);
-        const int s = k % C::NIQ;
-        if (k >= C::NIQ) mbar_wait(&bars[C::B_IQ_EMPTY + s], ((k / C::NIQ) - 1) & 1);
-        if (lane == 0) {
-          iq[s] = w < n_items ? w : -1;
-          mbar_arrive(&bars[C::B_IQ_FULL + s]);
-        }
-        __syncwarp();
-        if (w >= n_items) break;
-      }
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const Item item = work_item(p, w, q_tiles, k_tiles);
       const int qs = k % C::NQ;
       if (k >= C::NQ) mbar_wait(&bars[C::B_Q_EMPTY + qs], ((k / C::NQ) - 1) & 1);
@@ -319,8 +256,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     }
   } else if (warp == C::PROD_B) {
     // ------------------------------------------------------------ producer B: K + V for pass 2
-    int it = 0, k = 0;
-    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item item = work_item(p, w, q_tiles, k_tiles);
       for (int j = 0; j < item.nt; ++j, ++it) {
         const int st = it % C::NSB;
@@ -341,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   } else if (warp == C::MMA_A) {
     // ------------------------------------------------------------ MMA A: pass-1 S tiles
     int it = 0, k = 0, su = 0;
-    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
       const int qs = k % C::NQ;
       const uint32_t qb = s0 + C::Q0 + qs * C::Q_BYTES;
@@ -388,7 +325,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
   } else if (warp == C::MMA_B) {
     // ------------------------------------------------------------ MMA B: pass-2 S tiles + PV
     int it = 0, k = 0, su = 0, pc = 0;
-    for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
       const int nt = work_item(p, w, q_tiles, k_tiles).nt;
       const int qs = k % C::NQ;
       const uint32_t qb = s0 + C::Q0 + qs * C::Q_BYTES;
@@ -507,7 +444,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
     float* lb = reinterpret_cast<float*>(smem + C::LB);
     if (grp_a) {
       if constexpr (C::REALLOC) setmaxnreg_inc<C::REG_A>();
-      for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
         const Item item = work_item(p, w, q_tiles, k_tiles);
         const int nt = item.nt;
         const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
@@ -598,7 +535,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_infer_kernel(
       idump(true);
     } else {
       if constexpr (C::REALLOC) setmaxnreg_dec<C::REG_B>();
-      for (int64_t w = next_item(k); w >= 0; w = next_item(++k)) {
+      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
         const Item item = work_item(p, w, q_tiles, k_tiles);
         const int nt = item.nt;
         const int64_t grow = static_cast<int64_t>(item.qt) * TILE + row;
@@ -821,10 +758,6 @@ cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = p.heads * ceil_div(p.n_q, TILE);
   const int grid = static_cast<int>(items < sms ? items : sms);
-  if (p.item_ctr) {
-    e = cudaMemsetAsync(p.item_ctr, 0, sizeof(int), st);
-    if (e != cudaSuccess) return e;
-  }
   kern<<<grid, C::NUM_THREADS, C::TOTAL, st>>>(p);
   return cudaGetLastError();
 }

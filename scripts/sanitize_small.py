@@ -17,8 +17,9 @@ for n, d, causal in ((200, 64, True), (77, 128, False)):
     aq.attn_forward(q.detach(), k.detach(), v.detach(), causal=causal, train=False)
     cache = aq.kv4_quantize(k.detach(), v.detach())
     aq.attn_forward_kv4(q.detach(), cache, causal=causal)
-for n, d in ((1100, 128), (1030, 64)):  # the training forward's dynamic item queue (>= 8 causal query tiles)
-    q, k, v, do = (torch.randn(1, 1, n, d, generator=g, device="cuda").bfloat16() for _ in range(4))
+for n, d in ((1100, 128), (1030, 64)):  # the training forward's dynamic item queue (>= 8 causal query tiles,
+    # more items than CTAs so the queue hands out claims)
+    q, k, v, do = (torch.randn(1, 24, n, d, generator=g, device="cuda").bfloat16() for _ in range(4))
     aq.attn_qat(q.requires_grad_(), k.requires_grad_(), v.requires_grad_(), causal=True).backward(do)
 for n, d, causal, b_q, b_k, tl in ((200, 64, True, 40, 200, True), (77, 128, False, 77, 77, True),
                                    (77, 128, True, 77, 77, False), (256, 64, True, 16, 128, True),

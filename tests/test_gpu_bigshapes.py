@@ -108,9 +108,10 @@ def test_c3_early_out_is_exact():
 
 @pytest.mark.parametrize("shape", [(8, 32, 4096), (1, 3, 32768)])
 def test_dynamic_item_queue_covers_every_item(shape, monkeypatch):
-    """Causal rows of >= 32 query tiles run K4 on the dynamic item queue (>= 256
-    for K5): every (head, query tile) must be computed exactly once, so O / O' / L
-    equal the static schedule's bit for bit, and K4's O equals K5's."""
+    """Causal rows of >= 8 query tiles run the training forward (K11) on the
+    dynamic item queue: every (head, query tile) must be computed exactly once, so
+    O / O' / L equal the static schedule's bit for bit, and equal the inference
+    kernel's (K5, static order) O and L."""
     q, k, v = _inputs(*shape, seed=5)
     o_d, l_d, ohp_d, _ = aq.attn_forward(q, k, v, causal=True, train=True)
     oi_d, li_d, _, _ = aq.attn_forward(q, k, v, causal=True, train=False)
