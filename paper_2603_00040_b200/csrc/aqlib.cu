@@ -534,6 +534,7 @@ int aq_attn_fwd_mx(const AqFwdArgs* a, void* stream) {
   p.causal = a->causal;
   p.train = a->train;
   p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(a->d)));
+  p.item_ctr = reinterpret_cast<int*>(ws + w.sched);
   return cuda_status(launch_attn_fwd_mx(p, st));
 }
 

@@ -104,6 +104,7 @@ cudaError_t launch_attn_fwd(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_infer_mx(const FwdParams& p, cudaStream_t st);
 cudaError_t launch_attn_fwd_qat(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_attn_fwd_qat_mx(const FwdParams& p, cudaStream_t st);
 // K4 with the sage3 score terms; p.train selects two-level P (O written from
 // the f16 accumulator into p.o_hp) vs plain NVFP4 P (O into p.o)
 cudaError_t launch_attn_fwd_sage(const FwdParams& p, cudaStream_t st);

@@ -1024,10 +1024,21 @@ extern "C" int aq_debug_fwd_profile(unsigned long long* out, int reset) {
 cudaError_t launch_attn_fwd_mx(const FwdParams& p, cudaStream_t st) {
   // inference: the split-pass kernel; AQ_FWD_INFER=0 keeps it on K4 (comparisons)
   if (!p.train && env_int("AQ_FWD_INFER", 1)) return launch_attn_fwd_infer_mx(p, st);
-  if (p.d == 64) return p.train ? fwd::launch<64, true, 2, false, false, true>(p, st)
-                                : fwd::launch<64, false, 2, false, false, true>(p, st);
-  if (p.d == 128) return p.train ? fwd::launch<128, true, 2, false, false, true>(p, st)
-                                 : fwd::launch<128, false, 2, false, false, true>(p, st);
+  // training: the split-pass kernel K11's MX instance (AQ_FWD_QAT=0 keeps K4's),
+  // on the same item order as the NVFP4 training forward
+  if (p.train && env_int("AQ_FWD_QAT", 1)) {
+    FwdParams q = p;
+    if (!q.causal || !env_int("AQ_FWD_DYN", 1) || ceil_div(q.n_q, TILE) < env_int("AQ_FWDQ_DYN_MIN_QT", 8))
+      q.item_ctr = nullptr;
+    q.item_band = std::max(1, env_int("AQ_FWD_BAND", 8));
+    return launch_attn_fwd_qat_mx(q, st);
+  }
+  FwdParams q = p;
+  q.item_ctr = nullptr;  // K4's MX instance keeps its static order
+  if (q.d == 64) return q.train ? fwd::launch<64, true, 2, false, false, true>(q, st)
+                                : fwd::launch<64, false, 2, false, false, true>(q, st);
+  if (q.d == 128) return q.train ? fwd::launch<128, true, 2, false, false, true>(q, st)
+                                 : fwd::launch<128, false, 2, false, false, true>(q, st);
   return cudaErrorInvalidValue;
 }
 

@@ -24,6 +24,7 @@
 // (CS = 2), p_from_s / quantize_p16_s, P^ = fp16(P * l), O' MMA order and
 // epilogue scaling -- so O, O' and L are bit-identical to K4, and O, L to K5.
 //
+// MXFP4: the same pipeline on kind::mxf4 (the MX template flag).
 // Item order: K5's static snake, or (p.item_ctr, causal) K4's dynamic banded
 // queue, claimed by producer A and published through a shared-memory ring.
 // AQ_FWD_DEBUG bits (timing experiments only): 1 skips the O' MMAs, 2 the P^
@@ -166,7 +167,10 @@ __device__ __forceinline__ Item work_item(const FwdParams& p, int64_t w64, int q
   return it;
 }
 
-template <int D>
+// MX: the MXFP4 instance (codec.py:123-203): S and PV on kind::mxf4 block32
+// with one scale-factor image per 128 K (IDs 0 / 2 per K = 64 step), P in
+// 32-key UE8M0 blocks -- K4's MX instance on this pipeline.
+template <int D, bool MX = false>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(const FwdParams p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           mbar_wait(&bars[C::B_Q_FULL + qs], (k / C::NQ) & 1);
           tc_fence_after();
           if (elect_one()) {  // Q scale factors in TMEM, for MMA B too
-            for (int ks = 0; ks < D / 64; ++ks)
+            for (int ks = 0; ks < (MX ? 1 : D / 64); ++ks)
               tmem_cp_32x128_x4(tmem + C::T_QSF + 8 * qs + 4 * ks, desc_at(t_sf, qb + C::QC_BYTES + ks * 512));
             tc_commit(&bars[C::B_QSF + qs]);
           }
@@ -362,13 +366,21 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
               if (elect_one()) {
                 if (h == 0) {  // the slot's previous reader (half 1 of the last tile) has completed
 #pragma unroll
-                  for (int ks = 0; ks < D / 64; ++ks)
+                  for (int ks = 0; ks < (MX ? 1 : D / 64); ++ks)
                     tmem_cp_32x128_x4(tmem + C::T_KSFA + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
                 }
 #pragma unroll
-                for (int ks = 0; ks < D / 64; ++ks)
-                  mma_nvf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096 + h * 1024),
-                              id_h, tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFA + 4 * ks + 2 * h, ks > 0);
+                for (int ks = 0; ks < D / 64; ++ks) {
+                  if constexpr (MX) {
+                    const uint32_t sid = 2u * ks;
+                    mma_mxf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096 + h * 1024),
+                                idesc_mxf4(128, 64, sid), (tmem + C::T_QSF + 8 * qs) | (sid << 30),
+                                (tmem + C::T_KSFA + 2 * h) | (sid << 30), ks > 0);
+                  } else {
+                    mma_nvf4_ss(tmem + C::T_SA, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096 + h * 1024),
+                                id_h, tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFA + 4 * ks + 2 * h, ks > 0);
+                  }
+                }
                 tc_commit(&bars[C::B_SA_FULL + h]);
                 if (h == 1) tc_commit(&bars[C::B_KA_EMPTY + st]);
               }
@@ -397,12 +409,20 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
               const uint32_t kb = s0 + C::KBK0 + sk * C::KA_BYTES;
               if (elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < D / 64; ++ks)
+                for (int ks = 0; ks < (MX ? 1 : D / 64); ++ks)
                   tmem_cp_32x128_x4(tmem + C::T_KSFB + 4 * ks, desc_at(t_sf, kb + C::QC_BYTES + ks * 512));
 #pragma unroll
-                for (int ks = 0; ks < D / 64; ++ks)
-                  mma_nvf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
-                              tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFB + 4 * ks, ks > 0);
+                for (int ks = 0; ks < D / 64; ++ks) {
+                  if constexpr (MX) {
+                    const uint32_t sid = 2u * ks;
+                    mma_mxf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096),
+                                idesc_mxf4(128, 128, sid), (tmem + C::T_QSF + 8 * qs) | (sid << 30),
+                                (tmem + C::T_KSFB) | (sid << 30), ks > 0);
+                  } else {
+                    mma_nvf4_ss(tmem + C::T_SB, desc_at(t_k, qb + ks * 4096), desc_at(t_k, kb + ks * 4096), id_s,
+                                tmem + C::T_QSF + 8 * qs + 4 * ks, tmem + C::T_KSFB + 4 * ks, ks > 0);
+                  }
+                }
                 tc_commit(&bars[C::B_SB_FULL]);
                 tc_commit(&bars[C::B_KBK_EMPTY + sk]);
                 if (ns == nt - 1) tc_commit(&bars[C::B_Q_EMPTY + qs]);  // last read of this Q slot
@@ -423,15 +443,24 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
             const uint32_t pbase = s0 + C::P0 + pb * C::P_BYTES;
             if (elect_one()) {
 #pragma unroll
-              for (int ks = 0; ks < 2; ++ks) {
+              for (int ks = 0; ks < (MX ? 1 : 2); ++ks) {
                 tmem_cp_32x128_x4(tmem + C::T_PSF + 8 * pb + 4 * ks, desc_at(t_sf, pbase + C::PB_SF + ks * 512));
                 tmem_cp_32x128_x4(tmem + C::T_VSF + 8 * st + 4 * ks, desc_at(t_sf, sb + C::KB_VSF + ks * 512));
               }
 #pragma unroll
-              for (int ks = 0; ks < 2; ++ks)
-                mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096), desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)),
-                            id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks, tmem + C::T_VSF + 8 * st + 4 * ks,
-                            (pj > 0 || ks > 0));
+              for (int ks = 0; ks < 2; ++ks) {
+                if constexpr (MX) {
+                  const uint32_t sid = 2u * ks;
+                  mma_mxf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096),
+                              desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)), idesc_mxf4(128, D, sid),
+                              (tmem + C::T_PSF + 8 * pb) | (sid << 30), (tmem + C::T_VSF + 8 * st) | (sid << 30),
+                              (pj > 0 || ks > 0));
+                } else {
+                  mma_nvf4_ss(tmem + C::T_O, desc_at(t_k, pbase + ks * 4096),
+                              desc_at(t_v, sb + C::KB_V + ks * 2 * (D * 16)), id_pv, tmem + C::T_PSF + 8 * pb + 4 * ks,
+                              tmem + C::T_VSF + 8 * st + 4 * ks, (pj > 0 || ks > 0));
+                }
+              }
 #pragma unroll
               for (int ks = 0; ks < ((p.debug & 1) ? 0 : TILE / 16); ++ks)
                 mma_f16_ss(tmem + C::T_OP, desc_at(t_ph, pbase + C::PB_H + ks * 4096),
@@ -611,12 +640,19 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
           ++pc;
           uint8_t* pbase = smem + C::P0 + pb * C::P_BYTES;
           uint8_t* psf = pbase + C::PB_SF;
-          const PBlock qa = quantize_p16_s(x, p.p_r);
-          const PBlock qb = quantize_p16_s(x + 16, p.p_r);
-          *reinterpret_cast<uint4*>(pbase + t8x32_off(row, cbase, TILE)) =
-              make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
-          *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) =
-              static_cast<uint16_t>(qa.scale | (qb.scale << 8));
+          if constexpr (MX) {  // one 32-key UE8M0 block
+            uint32_t cd[4], sc;
+            quantize_p32_mx(x, cd, sc);
+            *reinterpret_cast<uint4*>(pbase + t8x32_off(row, cbase, TILE)) = make_uint4(cd[0], cd[1], cd[2], cd[3]);
+            psf[sf512_off(row, cbase / 32)] = static_cast<uint8_t>(sc);
+          } else {
+            const PBlock qa = quantize_p16_s(x, p.p_r);
+            const PBlock qb = quantize_p16_s(x + 16, p.p_r);
+            *reinterpret_cast<uint4*>(pbase + t8x32_off(row, cbase, TILE)) =
+                make_uint4(qa.codes[0], qa.codes[1], qb.codes[0], qb.codes[1]);
+            *reinterpret_cast<uint16_t*>(psf + sf512_off(row, cbase / 16)) =
+                static_cast<uint16_t>(qa.scale | (qb.scale << 8));
+          }
           uint8_t* ph = pbase + C::PB_H;
 #pragma unroll
           for (int c8 = 0; c8 < ((p.debug & 2) ? 0 : CW / 8); ++c8) {
@@ -630,7 +666,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
             }
             *reinterpret_cast<uint4*>(ph + t8x8_off(row, cbase + c8 * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
           }
-          if (p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
+          if (!MX && p.pf_codes != nullptr && grow < p.n_q) {  // instrument: this row's P^F of the tile
             const int64_t n16 = ceil_div(p.n_k, 16);
             const int64_t c0 = static_cast<int64_t>(jj) * TILE + cbase;
             uint8_t* dc = p.pf_codes + (item.head * p.n_q + grow) * (n16 * 8);
@@ -694,10 +730,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_fwd_qat_kernel(co
   }
 }
 
-template <int D>
+template <int D, bool MX = false>
 cudaError_t launch(const FwdParams& p, cudaStream_t st) {
   using C = Cfg<D>;
-  auto kern = attn_fwd_qat_kernel<D>;
+  auto kern = attn_fwd_qat_kernel<D, MX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -729,6 +765,12 @@ extern "C" int aq_debug_fwdq_profile(unsigned long long* out, int reset) {
 cudaError_t launch_attn_fwd_qat(const FwdParams& p, cudaStream_t st) {
   if (p.d == 64) return fwdq::launch<64>(p, st);
   if (p.d == 128) return fwdq::launch<128>(p, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_attn_fwd_qat_mx(const FwdParams& p, cudaStream_t st) {
+  if (p.d == 64) return fwdq::launch<64, true>(p, st);
+  if (p.d == 128) return fwdq::launch<128, true>(p, st);
   return cudaErrorInvalidValue;
 }
 

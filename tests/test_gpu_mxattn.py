@@ -66,3 +66,17 @@ def test_mx_autograd_matches_functional():
     dq, dk, dv = aq.attn_backward(q.detach(), k.detach(), v.detach(), d_o, o2, o_hp, lse, causal=True, mx=True)
     assert torch.equal(o, o2)
     assert torch.equal(q.grad, dq) and torch.equal(k.grad, dk) and torch.equal(v.grad, dv)
+
+
+@pytest.mark.parametrize("shape,d,causal", [((2, 5, 1100), 128, True), ((1, 3, 700), 64, True),
+                                             ((2, 3, 900), 128, False)])
+def test_mx_split_pass_training_forward_matches_k4(shape, d, causal, monkeypatch):
+    """The MXFP4 training forward runs on the split-pass kernel K11's MX instance;
+    K4's MX instance (AQ_FWD_QAT=0) has the same arithmetic: O, O' and L agree bit
+    for bit (ragged tails, d = 64, the dynamic item queue from 8 causal query tiles)."""
+    g = torch.Generator(device="cuda").manual_seed(33)
+    q, k, v = (torch.randn(*shape, d, generator=g, device="cuda").bfloat16() for _ in range(3))
+    o11, l11, ohp11 = aq.attn_forward_mx(q, k, v, causal=causal, train=True)
+    monkeypatch.setenv("AQ_FWD_QAT", "0")
+    o4, l4, ohp4 = aq.attn_forward_mx(q, k, v, causal=causal, train=True)
+    assert torch.equal(o11, o4) and torch.equal(l11, l4) and torch.equal(ohp11, ohp4)
