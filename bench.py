@@ -461,6 +461,17 @@ def run_attention(args, name, cfg, rank, world, local, main_line=False):
                 "step_frac_of_fp4_peak": value / world / peaks["nvfp4"],
                 "step_frac_of_mixed_ceiling": value / world / (1.17 * peaks["bf16"]),
                 "traffic": _traffic_from_profiles(name)}
+        # the training forward (K11, split-pass) beside it: FP4 S / PV plus the f16 O' MMA
+        fms = time_device(torch, lambda: aq.attn_forward(q, k, v, causal=causal, train=True, workspace=wsf,
+                                                       operands_staged=True, keep_for_bwd=True, out=o_f,
+                                                       lse_out=lse_f, o_hp_out=ohp_f),
+                          reps, 2, st, barrier)
+        ffl = flops_rank / 3.5
+        roof["forward"] = {"kernel": f"attn_fwd_qat_kernel<{d}>", "kernel_ms": fms,
+                           "achieved": ffl / (fms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                           "frac_of_fp4_peak": ffl / (fms * 1e-3) / 1e12 / peaks["nvfp4"],
+                           "kernel_share_of_step": fms / ms,
+                           "traffic": _traffic_from_profiles("train_fwd_" + name)}
 
     rec = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",

@@ -105,8 +105,9 @@ for rep in ("attn_fwd_c2", "attn_fwd_c3", "attn_fwd_train_c4", "attn_bwd_c4", "a
 # a partial capture updates the existing entries
 jpath = os.path.join(DST, "ncu_summary.json")
 prev = json.load(open(jpath)) if os.path.exists(jpath) else {}
-bench_map = {c: prev[c] for c in ("c2", "c3", "c4") if c in prev}
-for cfg, rep in (("c2", "attn_fwd_c2"), ("c3", "attn_fwd_c3"), ("c4", "attn_bwd_c4")):
+bench_map = {c: prev[c] for c in ("c2", "c3", "c4", "train_fwd_c4") if c in prev}
+for cfg, rep in (("c2", "attn_fwd_c2"), ("c3", "attn_fwd_c3"), ("c4", "attn_bwd_c4"),
+                 ("train_fwd_c4", "attn_fwd_train_c4")):
     if rep in summary:
         bench_map[cfg] = summary[rep][0]
 allmap = dict(prev.get("all", {}))
