@@ -13,12 +13,13 @@
 //
 // Step 1 (HBM-bound byte shuffle): both operands are re-laid into 128-row
 // MMA tiles (T8x32 codes + SF512 scale images, layouts.cuh), K zero-padded
-// to a multiple of 128 (zero codes and zero scales contribute exactly 0).
+// to a multiple of BK (zero codes and zero scales contribute exactly 0).
 // Step 2: persistent GEMM, one CTA per SM, 128 x 128 output tiles, K in
-// 128-wide slabs through a 6-stage TMA-bulk ring:
-//   warp 0   producer: 1-D bulk copies of the A / B slabs (18 KB per stage)
-//   warp 1   MMA issuer: per slab, tcgen05.cp of the 4 scale images into
-//            TMEM, then 2 x M128 N128 K64 block-scaled MMAs; commits release
+// 256-wide slabs through a 5-stage TMA-bulk ring (128-wide slabs in 11
+// stages were 5-8 % slower: one commit / barrier round trip per 2 MMAs):
+//   warp 0   producer: 1-D bulk copies of the A / B slabs (36 KB per stage)
+//   warp 1   MMA issuer: per slab, tcgen05.cp of the 8 scale images into
+//            TMEM, then 4 x M128 N128 K64 block-scaled MMAs; commits release
 //            the stage and, after the last slab, publish the accumulator
 //   warps 2-5 epilogue: TMEM -> registers -> C; two accumulator buffers
 //            in TMEM so the epilogue of tile t overlaps the MMAs of tile t+1
@@ -32,21 +33,30 @@
 namespace aq {
 namespace gemm {
 
-constexpr int BM = 128, BN = 128, BK = 128;  // output tile, K slab
-#ifndef AQ_FP4MM_STAGES
-#define AQ_FP4MM_STAGES 11
+#ifndef AQ_FP4MM_BK
+#define AQ_FP4MM_BK 256
 #endif
-constexpr int NST = AQ_FP4MM_STAGES;           // ring stages (bytes in flight per SM = NST x 18 KB)
-constexpr int CODE_SLAB = TILE * BK / 2;       // 8 KB: 4 K-chunks of a 128-row T8x32 tile
-constexpr int SF_SLAB = (BK / 64) * 512;       // 1 KB: 2 SF512 images
+constexpr int BM = 128, BN = 128, BK = AQ_FP4MM_BK;  // output tile, K slab
+// AQ_FP4MM_DIAG (timing diagnostics only, wrong results): 1 = no operand loads,
+// 2 = no scale copies / MMAs, 3 = no scale copies, 4 = no C stores
+#ifndef AQ_FP4MM_DIAG
+#define AQ_FP4MM_DIAG 0
+#endif
+#ifndef AQ_FP4MM_STAGES
+#define AQ_FP4MM_STAGES 5
+#endif
+constexpr int NST = AQ_FP4MM_STAGES;           // ring stages (bytes in flight per SM = NST x 36 KB)
+constexpr int CODE_SLAB = TILE * BK / 2;       // BK/32 K-chunks of a 128-row T8x32 tile
+constexpr int SF_SLAB = (BK / 64) * 512;       // BK/64 SF512 images
+constexpr int SF_COLS = 8 * (BK / 64);         // TMEM columns of one stage's scales (A then B)
 constexpr int STAGE = 2 * (CODE_SLAB + SF_SLAB);
 constexpr int BAR0 = NST * STAGE;
 constexpr int NUM_BARS = 2 * NST + 4;
 constexpr int SMEM = BAR0 + NUM_BARS * 8 + 16;
 constexpr int NUM_THREADS = 32 * 6;
-constexpr uint32_t T_ACC = 0, T_SF = 256;      // acc buffers [0,128), [128,256); SF 16 cols per stage
+constexpr uint32_t T_ACC = 0, T_SF = 256;      // acc buffers [0,128), [128,256); SF_COLS per stage
 static_assert(SMEM <= 227 * 1024, "shared memory");
-static_assert(T_SF + 16 * NST <= 512, "TMEM columns");
+static_assert(T_SF + SF_COLS * NST <= 512, "TMEM columns");
 
 // MX = MXFP4 operands (UE8M0 scale per 32 codes, codec.py:123-166): the same
 // code tiles; the SF512 images then hold 4 scales per 128 K (one image per slab).
@@ -131,13 +141,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams 
         if (it >= NST) mbar_wait(&empty[st], ((it / NST) - 1) & 1);
         if (elect_one()) {
           uint8_t* dst = smem + st * STAGE;
-          constexpr int SFB = MX ? 512 : SF_SLAB;  // scale bytes per operand per slab
+          constexpr int SFB = MX ? SF_SLAB / 2 : SF_SLAB;  // scale bytes per operand per slab
+#if AQ_FP4MM_DIAG == 1
+          mbar_arrive(&full[st]);
+          if (false) {
+#else
+          {
+#endif
           mbar_expect_tx(&full[st], 2 * (CODE_SLAB + SFB));
           bulk_g2s(dst, p.a_codes + tm * (TILE * p.kp / 2) + s * CODE_SLAB, CODE_SLAB, &full[st]);
           bulk_g2s(dst + CODE_SLAB, p.a_sf + tm * (p.kp / 64) * 512 + s * SFB, SFB, &full[st]);
           bulk_g2s(dst + CODE_SLAB + SF_SLAB, p.b_codes + tn * (TILE * p.kp / 2) + s * CODE_SLAB, CODE_SLAB,
                    &full[st]);
           bulk_g2s(dst + 2 * CODE_SLAB + SF_SLAB, p.b_sf + tn * (p.kp / 64) * 512 + s * SFB, SFB, &full[st]);
+          }
         }
         __syncwarp();
       }
@@ -161,25 +178,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams 
         const uint32_t base = s0 + st * STAGE;
         const uint32_t a_c = base, a_s = base + CODE_SLAB, b_c = base + CODE_SLAB + SF_SLAB,
                        b_s = base + 2 * CODE_SLAB + SF_SLAB;
-        const uint32_t sfa = tmem + T_SF + 16 * st, sfb = sfa + 8;
+        const uint32_t sfa = tmem + T_SF + SF_COLS * st, sfb = sfa + SF_COLS / 2;
         if (elect_one()) {
+#if AQ_FP4MM_DIAG == 2
+          if (false) {
+#else
           if constexpr (MX) {
-            // one image per slab: scales of K blocks 0-3 (32 wide); K step ks
-            // starts at byte 2 ks of each row's 32-bit scale cell
-            tmem_cp_32x128_x4(sfa, desc_at(t_sf, a_s));
-            tmem_cp_32x128_x4(sfb, desc_at(t_sf, b_s));
+#endif
+            // one image per 128 K: scales of K blocks 0-3 (32 wide); K step ks
+            // starts at byte 2 (ks % 2) of each row's 32-bit scale cell
+#pragma unroll
+            for (int h = 0; h < BK / 128; ++h) {
+              tmem_cp_32x128_x4(sfa + 4 * h, desc_at(t_sf, a_s + 512 * h));
+              tmem_cp_32x128_x4(sfb + 4 * h, desc_at(t_sf, b_s + 512 * h));
+            }
 #pragma unroll
             for (int ks = 0; ks < BK / 64; ++ks) {
-              const uint32_t sid = 2u * ks;
+              const uint32_t sid = 2u * (ks & 1);
+              const uint32_t h4 = 4u * (ks >> 1);
               mma_mxf4_ss(acc, desc_at(t_code, a_c + ks * 4096), desc_at(t_code, b_c + ks * 4096),
-                          idesc_mxf4(BM, BN, sid), sfa | (sid << 30), sfb | (sid << 30), (s > 0 || ks > 0));
+                          idesc_mxf4(BM, BN, sid), (sfa + h4) | (sid << 30), (sfb + h4) | (sid << 30),
+                          (s > 0 || ks > 0));
             }
           } else {
+#if AQ_FP4MM_DIAG == 2
+            if (false)
+#endif
 #pragma unroll
             for (int ks = 0; ks < BK / 64; ++ks) {
+#if AQ_FP4MM_DIAG == 3
+              if (s < 2)
+#endif
               tmem_cp_32x128_x4(sfa + 4 * ks, desc_at(t_sf, a_s + ks * 512));
+#if AQ_FP4MM_DIAG == 3
+              if (s < 2)
+#endif
               tmem_cp_32x128_x4(sfb + 4 * ks, desc_at(t_sf, b_s + ks * 512));
             }
+#if AQ_FP4MM_DIAG == 2
+            if (false)
+#endif
 #pragma unroll
             for (int ks = 0; ks < BK / 64; ++ks)
               mma_nvf4_ss(acc, desc_at(t_code, a_c + ks * 4096), desc_at(t_code, b_c + ks * 4096), id, sfa + 4 * ks,
@@ -213,7 +251,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) fp4mm_kernel(const GemmParams 
           tc_fence_before();
           mbar_arrive(&acc_empty[ab]);
         }
-        if (row < p.M) {
+        if (AQ_FP4MM_DIAG != 4 && row < p.M) {
           float* dst = p.c + row * p.ldc + col0 + c;
           if (col0 + c + 32 <= p.N && (p.ldc % 4) == 0) {
 #pragma unroll
