@@ -254,6 +254,10 @@ int aq_debug_fwd_profile(unsigned long long* out, int reset);
 /* Cycle counters of the backward compute warps (library built with
  * -DAQ_BWD_PROFILE; tuning aid). out: 16 counters. */
 int aq_debug_bwd_profile(unsigned long long* out, int reset);
+/* Per-CTA timeline of the last backward launch, 5 values per CTA (globaltimer ns
+ * of entry / first S tile / tile loop done / exit, then smid | is_kv << 16);
+ * only in -DAQ_BWD_PROFILE builds, otherwise returns AQ_E_CUDA. Measurement only. */
+int aq_debug_bwd_timeline(unsigned long long* out, int ctas);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,7 @@ PROTOTYPES = {
     "aq_probe_mma_flops": (ctypes.c_double, [c_int, c_int, c_int]),
     "aq_debug_fwd_profile": (c_int, [ctypes.POINTER(ctypes.c_ulonglong), c_int]),
     "aq_debug_bwd_profile": (c_int, [ctypes.POINTER(ctypes.c_ulonglong), c_int]),
+    "aq_debug_bwd_timeline": (c_int, [ctypes.POINTER(ctypes.c_ulonglong), c_int]),
 }
 
 _lib = None

@@ -40,6 +40,21 @@ namespace bwd {
 // of every compute warp; [0..7] KV role, [8..13] Q role, [14] KV tiles, [15] Q tiles.
 __device__ unsigned long long g_bprof[16];
 #ifdef AQ_BWD_PROFILE
+// per-CTA timeline (globaltimer ns): [0] entry, [1] first S in registers
+// (compute warp 0), [2] tile loop done, [3] exit, [4] smid | role << 16 | tiles << 32
+constexpr int kTimelineCtas = 32768;
+__device__ unsigned long long g_btl[kTimelineCtas][5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int64_t tl_cta() { return static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x; }
+#define AQ_TL(slot) do { if (threadIdx.x == 0 && tl_cta() < kTimelineCtas) g_btl[tl_cta()][slot] = gtimer(); } while (0)
+#else
+#define AQ_TL(slot) do { } while (0)
+#endif
+#ifdef AQ_BWD_PROFILE
 #define AQ_BPROF(...) __VA_ARGS__
 #else
 #define AQ_BPROF(...)
@@ -56,7 +71,15 @@ struct Cfg {
   static constexpr int NUM_THREADS = 32 * (NCW + 2);
   static constexpr int PRODUCER = NCW, MMA = NCW + 1;
 };
-constexpr int HALF = TILE / 2;               // dP half width of the KV kernel
+constexpr int HALF = TILE / 2;               // dP half width of the KV kernel (AQ_BWD_DPFULL=0)
+// AQ_BWD_DPFULL=1: the KV role computes dP_i as one N=128 product into the S
+// columns once S_i is in registers (S_{i+1} follows once dP_i is), instead of
+// two N=64 halves in a 64-column buffer. With operands streaming from shared
+// memory an N=64 bf16 MMA costs as long as an N=128 one (~49 vs ~50 ns per K16
+// step, scripts/probe_mma.py), so the halves doubled dP's tensor time.
+#ifndef AQ_BWD_DPFULL
+#define AQ_BWD_DPFULL 1
+#endif
 
 // N consecutive fp32 columns of this warp's TMEM lanes
 template <int N>
@@ -174,10 +197,12 @@ enum KvBar {
   KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE, KV_B_V
 };
 
-// Schedule per query tile i (MMA warp, in issue order):
-//   dP_i half 0 | S_{i+1} | dP_i half 1 | dV_i (once P^F_i is in SMEM) | dK_i (once dS_i is)
-// so S_{i+1} runs while the compute warps are still on tile i, and the Q
+// Schedule per query tile i (MMA warp, in issue order), AQ_BWD_DPFULL=1:
+//   dP_i (N=128, into S's columns once S_i is read) | S_{i+1} (once dP_i is read) |
+//   dV_i (once P^F_i is in SMEM) | dK_i (once dS_i is)
+// so dP_i runs under the P / P^F computation and S_{i+1} under dS_i; the Q
 // codes / dO / Q^F rings are released by the MMA that last reads them.
+// AQ_BWD_DPFULL=0 (round 1): dP_i half 0 | S_{i+1} | dP_i half 1 | dV_i | dK_i.
 template <int D, bool MX, bool PLAIN>
 __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head) {
   using L = KvSmem<D, PLAIN>;
@@ -210,7 +235,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       mbar_init(&bars[KV_B_DO_FULL + s], 1);
       mbar_init(&bars[KV_B_DO_EMPTY + s], 1);
       mbar_init(&bars[KV_B_DP_FULL + s], 1);
-      mbar_init(&bars[KV_B_DP_EMPTY + s], 32 * NCW / 2);
+      mbar_init(&bars[KV_B_DP_EMPTY + s], AQ_BWD_DPFULL ? 32 * NCW : 32 * NCW / 2);
     }
     mbar_init(&bars[KV_B_QH_FULL], 1);
     mbar_init(&bars[KV_B_QH_EMPTY], 1);
@@ -308,7 +333,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     // 16-bit operand format: bf16, or the PLAIN instance's p.plain_fmt (0 = fp16)
     const uint32_t f16f = PLAIN ? static_cast<uint32_t>(p.plain_fmt) : 1u;
     const uint32_t id_s16 = idesc_f16(128, 128, f16f, 0, 0);  // PLAIN: Q (K-major) x K (K-major)
-    const uint32_t id_dp = idesc_f16(128, HALF, f16f, 0, 0);  // dO (K-major) x V^F half (K-major)
+    const uint32_t id_dp = idesc_f16(128, AQ_BWD_DPFULL ? TILE : HALF, f16f, 0, 0);  // dO (K-major) x V^F (half)
     const uint32_t id_kv = idesc_f16(128, D, f16f, 1, 1);     // P^F^T / dS^T (MN) x dO / Q^F (MN)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);        // FP4 codes, K-major T8x32
     constexpr uint64_t t_sf = desc_template(0, 128);
@@ -321,7 +346,8 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       const int s = i & 1;
       const uint32_t qc = s0 + L::QC0 + s * L::QC_BYTES;
       mbar_wait(&bars[KV_B_QC_FULL + s], (i >> 1) & 1);
-      if (i > 0) mbar_wait(&bars[KV_B_S_EMPTY], (i - 1) & 1);
+      // DPFULL: the caller has waited for dP_{i-1} to be read (it shares S's columns)
+      if (!AQ_BWD_DPFULL && i > 0) mbar_wait(&bars[KV_B_S_EMPTY], (i - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         // S = Q K^T (FP4, same instruction sequence as the forward)
@@ -353,8 +379,8 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < D / 16; ++ks)
-          mma_f16_ss(tmem + KV_T_DP, desc_at(t_kmaj, do_h + ks * 4096), desc_at(t_kmaj, v_h + h * 1024 + ks * 4096),
-                     id_dp, ks > 0);
+          mma_f16_ss(tmem + (AQ_BWD_DPFULL ? KV_T_S : KV_T_DP), desc_at(t_kmaj, do_h + ks * 4096),
+                     desc_at(t_kmaj, v_h + h * 1024 + ks * 4096), id_dp, ks > 0);
         tc_commit(&bars[KV_B_DP_FULL + h]);
       }
       __syncwarp();
@@ -373,12 +399,24 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       const uint32_t do_h = s0 + L::DO_H0 + s * TILE * D * 2;
       // dP = dO V^F^T, one 64-key half at a time, with S_{i+1} in between
       mbar_wait(&bars[KV_B_DO_FULL + s], (ii / NDO) & 1);
+#if AQ_BWD_DPFULL
+      // dP_i (N = 128) into S's columns once every compute warp holds S_i; S_{i+1}
+      // once every compute warp holds dP_i
+      if (ii == 0) mbar_wait(&bars[KV_B_V], 0);
+      mbar_wait(&bars[KV_B_S_EMPTY], ph);
+      issue_dp(ii, 0, do_h);
+      if (ii + 1 < ni) {
+        mbar_wait(&bars[KV_B_DP_EMPTY], ph);
+        issue_s(ii + 1);
+      }
+#else
       if (ii > 0) mbar_wait(&bars[KV_B_DP_EMPTY + 1], ph ^ 1);
       else mbar_wait(&bars[KV_B_V], 0);
       issue_dp(ii, 0, do_h);
       if (ii + 1 < ni) issue_s(ii + 1);
       mbar_wait(&bars[KV_B_DP_EMPTY + 0], ph);
       issue_dp(ii, 1, do_h);
+#endif
       // dV += P^F^T dO
       mbar_wait(&bars[KV_B_PF_FULL], ph);
       tc_fence_after();
@@ -411,7 +449,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     const int row = 32 * (warp & 3) + lane;
     const int kg = warp >> 2;
     const int kb = kg * KPT;      // first key (in tile) of this thread
-    const int dph = kb / HALF;    // dP half holding those keys
+    const int dph = AQ_BWD_DPFULL ? 0 : kb / HALF;  // dP half holding those keys
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
     const bool f16 = PLAIN && p.plain_fmt == 0;  // fp16 operand tiles (PLAIN fp16 mode)
@@ -440,6 +478,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       float pr[KPT];
       AQ_BPROF(tq_ = clock64();)
       mbar_wait(&bars[KV_B_S_FULL], ph);
+      if (ii == 0) AQ_TL(1);
       tc_fence_after();
       tmem_load_f<KPT>(t_lane + KV_T_S + kb, pr);
       tc_fence_before();
@@ -537,7 +576,7 @@ if (PLAIN || !(MX && p.fq_p)) {
       mbar_wait(&bars[KV_B_DP_FULL + dph], ph);
       tc_fence_after();
       float dp[KPT];
-      tmem_load_f<KPT>(t_lane + KV_T_DP + kb % HALF, dp);
+      tmem_load_f<KPT>(t_lane + (AQ_BWD_DPFULL ? KV_T_S + kb : KV_T_DP + kb % HALF), dp);
       tc_fence_before();
       mbar_arrive(&bars[KV_B_DP_EMPTY + dph]);
       AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
@@ -549,6 +588,7 @@ if (PLAIN || !(MX && p.fq_p)) {
       AQ_BPROF(tn_ = clock64(); pr_[6] += tn_ - tq_; tq_ = tn_;)
     }
     AQ_BPROF(if (lane == 0) { for (int e = 0; e < 7; ++e) atomicAdd(&g_bprof[e], pr_[e]); atomicAdd(&g_bprof[14], static_cast<unsigned long long>(ni)); })
+    AQ_TL(2);
     // epilogue: dK, dV rows (thread = key row, D/NKG columns)
     if (ni > 0) {
       mbar_wait(&bars[KV_B_DONE], 0);
@@ -820,6 +860,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       float pr[KPT];
       AQ_BPROF(tq_ = clock64();)
       mbar_wait(&bars[Q_B_S_FULL], ph);
+      if (j == 0) AQ_TL(1);
       tc_fence_after();
       tmem_load_f<KPT>(t_lane + Q_T_S + kb, pr);
       tc_fence_before();
@@ -846,6 +887,7 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
       AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
     }
     AQ_BPROF(if (lane == 0) { for (int e = 0; e < 5; ++e) atomicAdd(&g_bprof[8 + e], pr_[e]); atomicAdd(&g_bprof[15], static_cast<unsigned long long>(nt)); })
+    AQ_TL(2);
     // epilogue: dQ rows (thread = query row, D/NKG columns), written once in the output dtype
     if (nt > 0) {
       mbar_wait(&bars[Q_B_DONE], 0);
@@ -894,8 +936,17 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const 
   } else {
     qt = q_tiles - 1 - (r - m);
   }
+  AQ_TL(0);
   if (kv >= 0) bwd_kv_tile<D, MX, PLAIN>(p, smem, kv, head);
   else bwd_q_tile<D, MX, PLAIN>(p, smem, qt, head);
+#ifdef AQ_BWD_PROFILE
+  if (threadIdx.x == 0 && tl_cta() < kTimelineCtas) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_btl[tl_cta()][3] = gtimer();
+    g_btl[tl_cta()][4] = smid | (static_cast<unsigned long long>(kv >= 0) << 16);
+  }
+#endif
 }
 
 // K6: D = rowsum(dO . O_ref) (fp32) and dO -> bf16 T8x8 tiles (pad rows zero).
@@ -1003,6 +1054,18 @@ cudaError_t launch_attn_bwd(const BwdParams& p, cudaStream_t st) {
   if (p.d == 64) return bwd::launch<64>(p, st);
   if (p.d == 128) return bwd::launch<128>(p, st);
   return cudaErrorInvalidValue;
+}
+
+// per-CTA timeline of the last profiled launch (-DAQ_BWD_PROFILE builds; else returns 5)
+extern "C" int aq_debug_bwd_timeline(unsigned long long* out, int ctas) {
+#ifdef AQ_BWD_PROFILE
+  if (ctas > bwd::kTimelineCtas) ctas = bwd::kTimelineCtas;
+  return cudaMemcpyFromSymbol(out, bwd::g_btl, sizeof(unsigned long long) * 5 * ctas) == cudaSuccess ? 0 : 5;
+#else
+  (void)out;
+  (void)ctas;
+  return 5;
+#endif
 }
 
 extern "C" int aq_debug_bwd_profile(unsigned long long* out, int reset) {

@@ -16,15 +16,25 @@ namespace aq {
 namespace probe {
 
 constexpr int M = 128, N = 256;
+constexpr int kProbeSmemBig = 13 * 1024 + 8 * 12 * 1024;  // SF + 8 operand buffers (A 4 KB + B 8 KB)
 
 __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int kind, int rounds) {
   // A: 128 x 64 fp4 (4 KB) or 128 x 16 bf16 (4 KB); B: 256 rows (8 KB); SF 2 x 512 B
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
-  __shared__ __align__(8) uint64_t bar;
-  for (int i = threadIdx.x; i < (12 * 1024 + 1024) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  __shared__ __align__(8) uint64_t bar, bar_end;
+  // kinds >= 5 stream operands from NB distinct buffers (no operand reuse) filled
+  // with random codes (scales 0x38 = 1.0); kinds < 5 reuse one zero-filled tile
+  const bool rnd = kind >= 5;
+  for (int i = threadIdx.x; i < (rnd ? kProbeSmemBig : 13 * 1024) / 4; i += blockDim.x) {
+    uint32_t x = rnd ? (static_cast<uint32_t>(i) * 2654435761u) ^ 0x5bd1e995u : 0u;
+    reinterpret_cast<uint32_t*>(smem)[i] = x;
+  }
+  if (rnd)
+    for (int i = threadIdx.x; i < 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem + 12 * 1024)[i] = 0x38383838u;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar_end, 1);
     fence_mbar_init();
   }
   if (threadIdx.x < 32) tmem_alloc(&slot, 512);
@@ -61,7 +71,33 @@ __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int kind, int rounds) 
         mbar_wait(&bar, r & 1);
       }
     }
-    if (kind != 4) {
+    else if (kind >= 9) {  // 9/10/11: bf16 N128/N256/N64, 12: nvf4 N64; streaming random operands
+      const int n = kind == 10 ? 256 : (kind == 9 ? 128 : 64);
+      const uint32_t ob = smem_u32(smem + 13 * 1024);
+      const uint32_t idf = idesc_f16(M, n, 1, 0, 0), id4 = idesc_nvf4(M, n);
+      for (int r = 0; r < rounds; ++r) {
+        const uint32_t o = ob + (r & 7) * 12 * 1024;
+        if (kind == 12)
+          mma_nvf4_ss(tmem, smem_desc(o, 2048, 128), smem_desc(o + 4096, 4096, 128), id4, tmem + 256, tmem + 264, r > 0);
+        else
+          mma_f16_ss(tmem, smem_desc(o, 2048, 128), smem_desc(o + 4096, 4096, 128), idf, r > 0);
+      }
+    }
+    else if (kind >= 5) {  // 5: N128, 6: N256, 7: N128 + commit per 2 MMAs, 8: N256 one buffer (random)
+      const int n = (kind == 6 || kind == 8) ? 256 : 128;
+      const uint32_t id = idesc_nvf4(M, n);
+      const uint32_t ob = smem_u32(smem + 13 * 1024);
+      for (int r = 0; r < rounds; ++r) {
+        const uint32_t o = kind == 8 ? ob : ob + (r & 7) * 12 * 1024;
+        mma_nvf4_ss(tmem + ((kind == 7) ? 128 * (r & 1) : 0), smem_desc(o, 2048, 128), smem_desc(o + 4096, 4096, 128), id,
+                    tmem + 256, tmem + 264, r > 0);
+        if (kind == 7 && (r & 1)) tc_commit(&bar);
+      }
+    }
+    if (kind == 7) {
+      tc_commit(&bar_end);
+      mbar_wait(&bar_end, 0);
+    } else if (kind != 4) {
       tc_commit(&bar);
       mbar_wait(&bar, 0);
     }
@@ -81,13 +117,15 @@ extern "C" {
 
 /* FLOPs executed by one aq_probe_mma_peak launch. kind 0 = NVFP4 (K=64), 1 = bf16 (K=16). */
 double aq_probe_mma_flops(int kind, int ctas, int rounds) {
-  const double k = (kind == 1) ? 16.0 : 64.0;
-  const double n = (kind >= 2) ? 128.0 : aq::probe::N;
+  const double k = (kind == 1 || (kind >= 9 && kind <= 11)) ? 16.0 : 64.0;
+  const double n = (kind == 0 || kind == 1 || kind == 6 || kind == 8 || kind == 10) ? 256.0
+                   : (kind == 11 || kind == 12) ? 64.0 : 128.0;
   return 2.0 * aq::probe::M * n * k * static_cast<double>(ctas) * rounds;
 }
 
 int aq_probe_mma_peak(int kind, int ctas, int rounds, void* stream) {
-  const int smem = 13 * 1024;
+  const int smem = kind >= 5 ? aq::probe::kProbeSmemBig : 13 * 1024;
+  if (kind >= 5) cudaFuncSetAttribute(aq::probe::mma_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   aq::probe::mma_peak_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(kind, rounds);
   return cudaGetLastError() == cudaSuccess ? AQ_OK : AQ_E_CUDA;
 }
