@@ -9,7 +9,7 @@ import paper_2603_00040_b200 as aq  # noqa: E402
 
 torch.manual_seed(0)
 for spec in (aq.NVFP4, aq.MXFP4):
-    for M, N, K in ((256, 384, 512), (200, 130, 992), (1024, 1024, 4096)):
+    for M, N, K in ((256, 384, 512), (200, 130, 992), (1024, 1024, 4096), (300, 700, 1056), (128, 256, 64), (129, 257, 2048)):
         a, b = torch.randn(M, K, device="cuda"), torch.randn(N, K, device="cuda")
         qa, qb = aq.quantize(a, spec), aq.quantize(b, spec)
         c = aq.fp4mm(qa, qb)

@@ -16,7 +16,9 @@ def _qt(x):
     return aq.QuantTensor(x.shape[0], x.shape[1], aq.NVFP4, codes, scales), codes, scales
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (37, 200, 48), (256, 384, 1024), (300, 129, 272), (1, 1, 16)])
+# N >= 256 runs the 128 x 256 kernel (staged epilogue for K <= 8192, direct beyond)
+@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (37, 200, 48), (256, 384, 1024), (300, 129, 272), (1, 1, 16),
+                                   (129, 700, 528), (260, 512, 256), (64, 256, 8448)])
 def test_fp4mm_matches_oracle(M, N, K):
     rng = np.random.default_rng(M * 7 + N + K)
     a = rng.standard_normal((M, K)) * 10.0 ** rng.uniform(-2, 2, (M, 1))
@@ -59,7 +61,8 @@ def test_matmul():
         aq.matmul(a, b[:3])
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (37, 200, 96), (256, 384, 1024), (300, 129, 288), (1, 1, 32)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 128), (37, 200, 96), (256, 384, 1024), (300, 129, 288), (1, 1, 32),
+                                   (129, 700, 544), (64, 256, 8448)])
 def test_fp4mm_mxfp4_matches_dequantized_product(M, N, K):
     # MXFP4 QuantTensors (UE8M0 per 32, codec.py:123-166) on kind::mxf4 block32:
     # exact block products, fp32 accumulation
