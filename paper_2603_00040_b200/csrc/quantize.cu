@@ -346,22 +346,39 @@ __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfl
                                                                   int fqh_dt, uint8_t* __restrict__ fqh2_t,
                                                                   int fqh2_dt, float inv_ts, int* __restrict__ nonfinite) {
   constexpr int SLAB = 64, PITCH = D + 8;  // tokens per CTA step; padded row (16-bit elements)
-  __shared__ __align__(16) __nv_bfloat16 slab[SLAB][PITCH];
+  // the slab (64 contiguous token rows, 16 KB at D = 128) arrives by one 1-D bulk
+  // copy, double-buffered so the next slab's load overlaps this slab's work (the
+  // column-pair reads below touch one row per instruction: no padding needed)
+  // (dynamic shared memory: with the f16 stage it exceeds the 48 KB static limit)
+  extern __shared__ __align__(128) uint8_t qc_smem[];
+  auto slab = reinterpret_cast<__nv_bfloat16(*)[SLAB][D]>(qc_smem);                        // [2][SLAB][D]
+  auto bar = reinterpret_cast<uint64_t*>(qc_smem + 2 * SLAB * D * 2);                       // [2]
   // training: the dequantized values, as f16 pairs, for the T8x8 operand tiles
-  __shared__ __align__(16) __half slab_h[FQH ? SLAB : 1][FQH ? PITCH : 8];
+  auto slab_h = reinterpret_cast<__half(*)[PITCH]>(qc_smem + 2 * SLAB * D * 2 + 16);        // [SLAB][PITCH]
+  constexpr uint32_t SLAB_BYTES = SLAB * D * 2;
+  constexpr int CV = D / 8;  // 16-byte vectors per token row
   const int64_t tiles = n / TILE;
   const int64_t nslabs = heads * tiles * (TILE / SLAB);
-  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
-    const int64_t tok0 = sidx * SLAB;  // flat token index over all heads (tiles never straddle heads)
-    __syncthreads();
-    constexpr int CV = D / 8;           // 16-byte vectors per token row
-#pragma unroll
-    for (int k = 0; k < SLAB * CV / 128; ++k) {
-      const int i = threadIdx.x + k * 128;
-      const int tt = i / CV, c = (i % CV) * 8;
-      *reinterpret_cast<uint4*>(&slab[tt][c]) = *reinterpret_cast<const uint4*>(x + (tok0 + tt) * D + c);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    if (blockIdx.x < nslabs) {
+      mbar_expect_tx(&bar[0], SLAB_BYTES);
+      bulk_g2s(&slab[0][0][0], x + static_cast<int64_t>(blockIdx.x) * SLAB * D, SLAB_BYTES, &bar[0]);
     }
-    __syncthreads();
+  }
+  int it = 0;
+  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x, ++it) {
+    const int64_t tok0 = sidx * SLAB;  // flat token index over all heads (tiles never straddle heads)
+    const int buf = it & 1;
+    __syncthreads();  // every thread is done with slab[buf ^ 1] (previous slab) and slab_h
+    if (threadIdx.x == 0 && sidx + gridDim.x < nslabs) {
+      fence_async_smem();
+      mbar_expect_tx(&bar[buf ^ 1], SLAB_BYTES);
+      bulk_g2s(&slab[buf ^ 1][0][0], x + (sidx + gridDim.x) * SLAB * D, SLAB_BYTES, &bar[buf ^ 1]);
+    }
+    mbar_wait(&bar[buf], (it >> 1) & 1);
     const int64_t tile = tok0 / TILE;
     const int kt0 = static_cast<int>(tok0 % TILE);
     for (int wi = threadIdx.x; wi < (D / 2) * (SLAB / 32); wi += blockDim.x) {
@@ -370,7 +387,7 @@ __global__ void __launch_bounds__(128) quantize_cols_tiled_kernel(const __nv_bfl
       float v0[32], v1[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(&slab[g32 * 32 + j][2 * cp]);
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(&slab[buf][g32 * 32 + j][2 * cp]);
         v0[j] = __uint_as_float(w << 16);
         v1[j] = __uint_as_float(w & 0xFFFF0000u);
       }
@@ -731,12 +748,18 @@ cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
         quantize_cols_slab_kernel<64><<<static_cast<int>(gs), 64, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, a.inv_ts, a.nonfinite);
       return cudaGetLastError();
     }
+    // dynamic smem: two bf16 slabs, the barriers, the f16 stage (training)
+    const int sm = static_cast<int>(2 * 64 * a.cols * 2 + 16 + (fqh ? 64 * (a.cols + 8) * 2 : 0));
     if (a.cols == 128) {
-      if (fqh) quantize_cols_tiled_kernel<128, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
-      else quantize_cols_tiled_kernel<128, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
+      if (fqh) {
+        cudaFuncSetAttribute(quantize_cols_tiled_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        quantize_cols_tiled_kernel<128, true><<<gg, 128, sm, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
+      } else {
+        quantize_cols_tiled_kernel<128, false><<<gg, 128, sm, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
+      }
     } else {
-      if (fqh) quantize_cols_tiled_kernel<64, true><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
-      else quantize_cols_tiled_kernel<64, false><<<gg, 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
+      if (fqh) quantize_cols_tiled_kernel<64, true><<<gg, 128, sm, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, h1, a.fqh_dt, h2, a.fqh2_dt, a.inv_ts, a.nonfinite);
+      else quantize_cols_tiled_kernel<64, false><<<gg, 128, sm, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, nullptr, 0, a.inv_ts, a.nonfinite);
     }
     return cudaGetLastError();
   }
