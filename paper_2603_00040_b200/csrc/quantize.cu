@@ -694,26 +694,39 @@ __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat
                                                                int64_t n, uint8_t* __restrict__ codes_t,
                                                                uint8_t* __restrict__ sf_t, float inv_ts,
                                                                int* __restrict__ nonfinite) {
-  constexpr int PITCH = D + 8;
-  __shared__ __align__(16) __nv_bfloat16 slab[32][PITCH];
+  // 32 contiguous token rows per slab, double-buffered 1-D bulk copies (the
+  // column reads touch one row per instruction: no padding needed)
+  __shared__ __align__(128) __nv_bfloat16 slab[2][32][D];
+  __shared__ __align__(8) uint64_t bar[2];
+  constexpr uint32_t SLAB_BYTES = 32 * D * 2;
   const int64_t nslabs = heads * (n / 32);
   const int c = threadIdx.x;
-  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x) {
-    const int64_t tok0 = sidx * 32;  // flat token index (n % 128 == 0: slabs never straddle heads)
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = threadIdx.x + k * D;
-      const int tt = i / (D / 8), cc = (i % (D / 8)) * 8;
-      *reinterpret_cast<uint4*>(&slab[tt][cc]) = *reinterpret_cast<const uint4*>(x + (tok0 + tt) * D + cc);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    if (blockIdx.x < nslabs) {
+      mbar_expect_tx(&bar[0], SLAB_BYTES);
+      bulk_g2s(&slab[0][0][0], x + static_cast<int64_t>(blockIdx.x) * 32 * D, SLAB_BYTES, &bar[0]);
     }
-    __syncthreads();
+  }
+  int it = 0;
+  for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x, ++it) {
+    const int64_t tok0 = sidx * 32;  // flat token index (n % 128 == 0: slabs never straddle heads)
+    const int buf = it & 1;
+    __syncthreads();  // every thread is done with slab[buf ^ 1]
+    if (threadIdx.x == 0 && sidx + gridDim.x < nslabs) {
+      fence_async_smem();
+      mbar_expect_tx(&bar[buf ^ 1], SLAB_BYTES);
+      bulk_g2s(&slab[buf ^ 1][0][0], x + (sidx + gridDim.x) * 32 * D, SLAB_BYTES, &bar[buf ^ 1]);
+    }
+    mbar_wait(&bar[buf], (it >> 1) & 1);
     Block16 q[2];
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       float v[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __bfloat162float(slab[16 * b + j][c]);
+      for (int j = 0; j < 16; ++j) v[j] = __bfloat162float(slab[buf][16 * b + j][c]);
       scale16(v, inv_ts);
       quantize_block16<false, true>(v, q[b]);
     }
