@@ -194,7 +194,7 @@ constexpr uint32_t KV_T_S = 0, KV_T_DK = 128, KV_T_DV = 256, KV_T_DP = 384, KV_T
 enum KvBar {
   KV_B_K = 0, KV_B_QC_FULL = 1, KV_B_QC_EMPTY = 3, KV_B_DO_FULL = 5, KV_B_DO_EMPTY = 7, KV_B_QH_FULL = 9,
   KV_B_QH_EMPTY, KV_B_S_FULL, KV_B_S_EMPTY, KV_B_DP_FULL, KV_B_DP_EMPTY = KV_B_DP_FULL + 2,
-  KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE, KV_B_V
+  KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE, KV_B_V, KV_B_DV_DONE
 };
 
 // Schedule per query tile i (MMA warp, in issue order), AQ_BWD_DPFULL=1:
@@ -246,6 +246,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     mbar_init(&bars[KV_B_DS_FULL], 32 * NCW);
     mbar_init(&bars[KV_B_DS_FREE], 1);
     mbar_init(&bars[KV_B_DONE], 1);
+    mbar_init(&bars[KV_B_DV_DONE], 1);
     fence_mbar_init();
     // the stationary K / V^F tiles and the first query tile are requested
     // before the CTA-wide sync, so their latency overlaps TMEM allocation.
@@ -426,6 +427,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
                      (ii > 0 || ks > 0));
         tc_commit(&bars[KV_B_PF_FREE]);
         tc_commit(&bars[KV_B_DO_EMPTY + s]);
+        if (ii == ni - 1) tc_commit(&bars[KV_B_DV_DONE]);  // dV final: its epilogue overlaps the last dK
       }
       __syncwarp();
       // dK += dS^T Q^F (PLAIN: Q from its ring slot, already waited for by S_i)
@@ -589,15 +591,17 @@ if (PLAIN || !(MX && p.fq_p)) {
     }
     AQ_BPROF(if (lane == 0) { for (int e = 0; e < 7; ++e) atomicAdd(&g_bprof[e], pr_[e]); atomicAdd(&g_bprof[14], static_cast<unsigned long long>(ni)); })
     AQ_TL(2);
-    // epilogue: dK, dV rows (thread = key row, D/NKG columns)
-    if (ni > 0) {
-      mbar_wait(&bars[KV_B_DONE], 0);
-      tc_fence_after();
-    }
+    // epilogue: dV rows as soon as the last dV MMA is done (while the last dK
+    // MMA runs), then dK rows (thread = key row, D/NKG columns)
     const int64_t key = k0 + row;
     constexpr int DH = D / NKG;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
+    for (int w2 = 0; w2 < 2; ++w2) {
+      const int which = 1 - w2;
+      if (ni > 0) {
+        mbar_wait(&bars[which ? KV_B_DV_DONE : KV_B_DONE], 0);
+        tc_fence_after();
+      }
       float g[DH];
       if (ni > 0) {
         tmem_load_f<DH>(t_lane + (which ? KV_T_DV : KV_T_DK) + kg * DH, g);
