@@ -71,14 +71,17 @@ struct Cfg {
   static constexpr int NUM_THREADS = 32 * (NCW + 2);
   static constexpr int PRODUCER = NCW, MMA = NCW + 1;
 };
-constexpr int HALF = TILE / 2;               // dP half width of the KV kernel (AQ_BWD_DPFULL=0)
-// AQ_BWD_DPFULL=1: the KV role computes dP_i as one N=128 product into the S
-// columns once S_i is in registers (S_{i+1} follows once dP_i is), instead of
-// two N=64 halves in a 64-column buffer. With operands streaming from shared
-// memory an N=64 bf16 MMA costs as long as an N=128 one (~49 vs ~50 ns per K16
-// step, scripts/probe_mma.py), so the halves doubled dP's tensor time.
-#ifndef AQ_BWD_DPFULL
-#define AQ_BWD_DPFULL 1
+// The KV role computes dP_i as one N=128 product into the S columns once S_i
+// is in registers (S_{i+1} follows once dP_i is). Until round 2 it ran two N=64
+// halves in a 64-column buffer; with operands streaming from shared memory an
+// N=64 bf16 MMA costs as long as an N=128 one (~49 vs ~50 ns per K16 step,
+// scripts/probe_mma.py), so the halves doubled dP's tensor time.
+// AQ_BWD_PAIR=1: a KV CTA runs two key tiles of its head (see bwd_kv_tile).
+// Measured at C4 it is 5 % slower (3.62 -> 3.82 ms): the paired CTAs' tile
+// loops ran ~5 % slower per tile and the item switch was not hidden, so the
+// default launch keeps one key tile per CTA (the item loop then runs once).
+#ifndef AQ_BWD_PAIR
+#define AQ_BWD_PAIR 0
 #endif
 
 // N consecutive fp32 columns of this warp's TMEM lanes
@@ -188,8 +191,8 @@ struct KvSmem {
   static_assert(TOTAL <= 227 * 1024, "shared memory");
 };
 
-// TMEM: S [0,128); dK [128,128+D); dV [256,256+D); dP (one 64-key half) [384,448); SF 448+
-constexpr uint32_t KV_T_S = 0, KV_T_DK = 128, KV_T_DV = 256, KV_T_DP = 384, KV_T_QSF = 448, KV_T_KSF = 464;
+// TMEM: S and dP (one after the other) [0,128); dK [128,128+D); dV [256,256+D); SF 448+
+constexpr uint32_t KV_T_S = 0, KV_T_DK = 128, KV_T_DV = 256, KV_T_QSF = 448, KV_T_KSF = 464;
 
 enum KvBar {
   KV_B_K = 0, KV_B_QC_FULL = 1, KV_B_QC_EMPTY = 3, KV_B_DO_FULL = 5, KV_B_DO_EMPTY = 7, KV_B_QH_FULL = 9,
@@ -197,14 +200,18 @@ enum KvBar {
   KV_B_PF_FULL = KV_B_DP_EMPTY + 2, KV_B_PF_FREE, KV_B_DS_FULL, KV_B_DS_FREE, KV_B_DONE, KV_B_V, KV_B_DV_DONE
 };
 
-// Schedule per query tile i (MMA warp, in issue order), AQ_BWD_DPFULL=1:
+// Schedule per query tile i (MMA warp, in issue order):
 //   dP_i (N=128, into S's columns once S_i is read) | S_{i+1} (once dP_i is read) |
 //   dV_i (once P^F_i is in SMEM) | dK_i (once dS_i is)
 // so dP_i runs under the P / P^F computation and S_{i+1} under dS_i; the Q
 // codes / dO / Q^F rings are released by the MMA that last reads them.
-// AQ_BWD_DPFULL=0 (round 1): dP_i half 0 | S_{i+1} | dP_i half 1 | dV_i | dK_i.
+// A CTA may run a second key tile kt2 of the same head after kt (kt2 >= 0):
+// every ring and barrier phase continues across the two items (g = tile count
+// of the CTA); the second item's K / V are loaded once the first item's MMAs
+// are done, and its first S / dP run while the compute warps store the first
+// item's dK / dV, so the second item pays no launch gap and no ramp.
 template <int D, bool MX, bool PLAIN>
-__device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head) {
+__device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, int kt, int64_t head, int kt2 = -1) {
   using L = KvSmem<D, PLAIN>;
   constexpr int NDO = L::NDO;
   constexpr int NCW = Cfg<D>::NCW, NKG = Cfg<D>::NKG, KPT = Cfg<D>::KPT;
@@ -213,19 +220,27 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::TMEM_SLOT);
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int k0 = kt * TILE;
   const int q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
   const int k_tiles = static_cast<int>(ceil_div(p.n_k, TILE));
   const int64_t offset = p.n_k - p.n_q;
-  // first query tile with any visible key of this key tile (flash.py:127-128, 366-368)
-  int i_begin = 0;
-  if (p.causal) {
-    const int64_t need = k0 - offset - (TILE - 1);  // q0 >= need
-    i_begin = need > 0 ? static_cast<int>(ceil_div(need, TILE)) : 0;
-  }
-  const int ni = q_tiles > i_begin ? q_tiles - i_begin : 0;
-
-  const int64_t kidx = head * k_tiles + kt;
+  const int nit = kt2 >= 0 ? 2 : 1;
+  // first query tile with any visible key of key tile t (flash.py:127-128, 366-368)
+  auto first_q = [&](int t) {
+    if (!p.causal) return 0;
+    const int64_t need = static_cast<int64_t>(t) * TILE - offset - (TILE - 1);  // q0 >= need
+    return need > 0 ? static_cast<int>(ceil_div(need, TILE)) : 0;
+  };
+  // per-item state (item 0 here; every role switches to item 1 in its own loop)
+  int k0 = kt * TILE, i_begin = first_q(kt);
+  int ni = q_tiles > i_begin ? q_tiles - i_begin : 0;
+  int64_t kidx = head * k_tiles + kt;
+  auto set_item = [&](int it) {
+    const int t = it ? kt2 : kt;
+    k0 = t * TILE;
+    i_begin = first_q(t);
+    ni = q_tiles > i_begin ? q_tiles - i_begin : 0;
+    kidx = head * k_tiles + t;
+  };
   if (threadIdx.x == 32 * PRODUCER) {
     mbar_init(&bars[KV_B_K], 1);
     mbar_init(&bars[KV_B_V], 1);
@@ -235,7 +250,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       mbar_init(&bars[KV_B_DO_FULL + s], 1);
       mbar_init(&bars[KV_B_DO_EMPTY + s], 1);
       mbar_init(&bars[KV_B_DP_FULL + s], 1);
-      mbar_init(&bars[KV_B_DP_EMPTY + s], AQ_BWD_DPFULL ? 32 * NCW : 32 * NCW / 2);
+      mbar_init(&bars[KV_B_DP_EMPTY + s], 32 * NCW);
     }
     mbar_init(&bars[KV_B_QH_FULL], 1);
     mbar_init(&bars[KV_B_QH_EMPTY], 1);
@@ -287,10 +302,9 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
   if (warp == PRODUCER) {
     // ------------------------------------------------------------ producer
     // (K, V^F and query tile 0 were requested before the CTA-wide sync)
-    auto load_qc = [&](int t) {
+    auto load_qc = [&](int t, int64_t qidx) {  // t: ring position (tile count of the CTA)
       const int s = t & 1;
       if (t >= 2) mbar_wait(&bars[KV_B_QC_EMPTY + s], ((t >> 1) - 1) & 1);
-      const int64_t qidx = head * q_tiles + i_begin + t;
       if (elect_one()) {
         uint8_t* dst = smem + L::QC0 + s * L::QC_BYTES;
         mbar_expect_tx(&bars[KV_B_QC_FULL + s], L::QC_BYTES);
@@ -303,10 +317,9 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       }
       __syncwarp();
     };
-    auto load_do = [&](int t) {
+    auto load_do = [&](int t, int64_t qidx) {
       const int s = t % NDO;
       if (t >= NDO) mbar_wait(&bars[KV_B_DO_EMPTY + s], ((t / NDO) - 1) & 1);
-      const int64_t qidx = head * q_tiles + i_begin + t;
       if (elect_one()) {
         mbar_expect_tx(&bars[KV_B_DO_FULL + s], TILE * D * 2);
         bulk_g2s(smem + L::DO_H0 + s * TILE * D * 2, p.do_h + qidx * h_tile_bytes(D), TILE * D * 2,
@@ -314,19 +327,47 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       }
       __syncwarp();
     };
-    for (int t = 0; t < ni; ++t) {
-      if (t + 1 < ni) {
-        load_qc(t + 1);
-        load_do(t + 1);
+    int g = 0;
+    for (int it = 0; it < nit; ++it) {
+      if (it > 0) {
+        set_item(it);
+        // K / V^F of this item replace the previous item's once all its MMAs are done
+        mbar_wait(&bars[KV_B_DONE], (it - 1) & 1);
+        if (elect_one()) {
+          if (PLAIN) {
+            mbar_expect_tx(&bars[KV_B_K], TILE * D * 2);
+            bulk_g2s(smem + L::K_CODES, p.k_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_K]);
+          } else {
+            mbar_expect_tx(&bars[KV_B_K], TILE * D / 2 + (D / 64) * 512);
+            bulk_g2s(smem + L::K_CODES, p.k_codes + kidx * fp4_tile_bytes(D), TILE * D / 2, &bars[KV_B_K]);
+            bulk_g2s(smem + L::K_SF, p.k_sf + kidx * sf_tile_bytes_qk(D), (D / 64) * 512, &bars[KV_B_K]);
+          }
+          mbar_expect_tx(&bars[KV_B_V], TILE * D * 2);
+          bulk_g2s(smem + L::V_H, p.v_h + kidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_V]);
+        }
+        __syncwarp();
       }
-      if (PLAIN) continue;  // the Q ring slot is the dK operand too
-      if (t > 0) mbar_wait(&bars[KV_B_QH_EMPTY], (t - 1) & 1);
-      const int64_t qidx = head * q_tiles + i_begin + t;
-      if (elect_one()) {
-        mbar_expect_tx(&bars[KV_B_QH_FULL], TILE * D * 2);
-        bulk_g2s(smem + L::Q_H, p.q_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_QH_FULL]);
+      for (int t = 0; t < ni; ++t, ++g) {
+        // the next query tile: this item's, or the next item's first (the rings run on)
+        if (t + 1 < ni) {
+          load_qc(g + 1, head * q_tiles + i_begin + t + 1);
+          load_do(g + 1, head * q_tiles + i_begin + t + 1);
+        } else if (it + 1 < nit) {
+          const int ib = first_q(kt2);
+          if (ib < q_tiles) {
+            load_qc(g + 1, head * q_tiles + ib);
+            load_do(g + 1, head * q_tiles + ib);
+          }
+        }
+        if (PLAIN) continue;  // the Q ring slot is the dK operand too
+        if (g > 0) mbar_wait(&bars[KV_B_QH_EMPTY], (g - 1) & 1);
+        const int64_t qidx = head * q_tiles + i_begin + t;
+        if (elect_one()) {
+          mbar_expect_tx(&bars[KV_B_QH_FULL], TILE * D * 2);
+          bulk_g2s(smem + L::Q_H, p.q_h + qidx * h_tile_bytes(D), TILE * D * 2, &bars[KV_B_QH_FULL]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp == MMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -334,7 +375,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
     // 16-bit operand format: bf16, or the PLAIN instance's p.plain_fmt (0 = fp16)
     const uint32_t f16f = PLAIN ? static_cast<uint32_t>(p.plain_fmt) : 1u;
     const uint32_t id_s16 = idesc_f16(128, 128, f16f, 0, 0);  // PLAIN: Q (K-major) x K (K-major)
-    const uint32_t id_dp = idesc_f16(128, AQ_BWD_DPFULL ? TILE : HALF, f16f, 0, 0);  // dO (K-major) x V^F (half)
+    const uint32_t id_dp = idesc_f16(128, TILE, f16f, 0, 0);  // dO (K-major) x V^F (K-major)
     const uint32_t id_kv = idesc_f16(128, D, f16f, 1, 1);     // P^F^T / dS^T (MN) x dO / Q^F (MN)
     constexpr uint64_t t_fp4 = desc_template(2048, 128);        // FP4 codes, K-major T8x32
     constexpr uint64_t t_sf = desc_template(0, 128);
@@ -347,8 +388,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       const int s = i & 1;
       const uint32_t qc = s0 + L::QC0 + s * L::QC_BYTES;
       mbar_wait(&bars[KV_B_QC_FULL + s], (i >> 1) & 1);
-      // DPFULL: the caller has waited for dP_{i-1} to be read (it shares S's columns)
-      if (!AQ_BWD_DPFULL && i > 0) mbar_wait(&bars[KV_B_S_EMPTY], (i - 1) & 1);
+      // the caller has waited for dP_{i-1} to be read (it shares S's columns)
       tc_fence_after();
       if (elect_one()) {
         // S = Q K^T (FP4, same instruction sequence as the forward)
@@ -380,78 +420,77 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       tc_fence_after();
       if (elect_one()) {
         for (int ks = 0; ks < D / 16; ++ks)
-          mma_f16_ss(tmem + (AQ_BWD_DPFULL ? KV_T_S : KV_T_DP), desc_at(t_kmaj, do_h + ks * 4096),
-                     desc_at(t_kmaj, v_h + h * 1024 + ks * 4096), id_dp, ks > 0);
+          mma_f16_ss(tmem + KV_T_S, desc_at(t_kmaj, do_h + ks * 4096), desc_at(t_kmaj, v_h + h * 1024 + ks * 4096),
+                     id_dp, ks > 0);
         tc_commit(&bars[KV_B_DP_FULL + h]);
       }
       __syncwarp();
     };
-    mbar_wait(&bars[KV_B_K], 0);
-    tc_fence_after();
-    if (!PLAIN && elect_one()) {
-      for (int ks = 0; ks < D / 64; ++ks)
-        tmem_cp_32x128_x4(tmem + KV_T_KSF + 4 * ks, desc_at(t_sf, s0 + L::K_SF + ks * 512));
-    }
-    __syncwarp();
-    if (ni > 0) issue_s(0);
-    for (int ii = 0; ii < ni; ++ii) {
-      const uint32_t ph = ii & 1;
-      const int s = ii % NDO;
-      const uint32_t do_h = s0 + L::DO_H0 + s * TILE * D * 2;
-      // dP = dO V^F^T, one 64-key half at a time, with S_{i+1} in between
-      mbar_wait(&bars[KV_B_DO_FULL + s], (ii / NDO) & 1);
-#if AQ_BWD_DPFULL
-      // dP_i (N = 128) into S's columns once every compute warp holds S_i; S_{i+1}
-      // once every compute warp holds dP_i
-      if (ii == 0) mbar_wait(&bars[KV_B_V], 0);
-      mbar_wait(&bars[KV_B_S_EMPTY], ph);
-      issue_dp(ii, 0, do_h);
-      if (ii + 1 < ni) {
-        mbar_wait(&bars[KV_B_DP_EMPTY], ph);
-        issue_s(ii + 1);
-      }
-#else
-      if (ii > 0) mbar_wait(&bars[KV_B_DP_EMPTY + 1], ph ^ 1);
-      else mbar_wait(&bars[KV_B_V], 0);
-      issue_dp(ii, 0, do_h);
-      if (ii + 1 < ni) issue_s(ii + 1);
-      mbar_wait(&bars[KV_B_DP_EMPTY + 0], ph);
-      issue_dp(ii, 1, do_h);
-#endif
-      // dV += P^F^T dO
-      mbar_wait(&bars[KV_B_PF_FULL], ph);
+    int g = 0;  // tile count of the CTA: ring slots and barrier phases run on across items
+    for (int it = 0; it < nit; ++it) {
+      if (it > 0) set_item(it);
+      mbar_wait(&bars[KV_B_K], it & 1);
+      // S's columns: the previous item's last dP has been read (S_0 overwrites them)
+      if (g > 0) mbar_wait(&bars[KV_B_DP_EMPTY], (g - 1) & 1);
       tc_fence_after();
-      if (elect_one()) {
-        for (int ks = 0; ks < TILE / 16; ++ks)
-          mma_f16_ss(tmem + KV_T_DV, desc_at(t_mn, p_h + ks * 256), desc_at(t_mn, do_h + ks * 256), id_kv,
-                     (ii > 0 || ks > 0));
-        tc_commit(&bars[KV_B_PF_FREE]);
-        tc_commit(&bars[KV_B_DO_EMPTY + s]);
-        if (ii == ni - 1) tc_commit(&bars[KV_B_DV_DONE]);  // dV final: its epilogue overlaps the last dK
+      if (!PLAIN && elect_one()) {  // after the previous item's S MMAs in the pipe
+        for (int ks = 0; ks < D / 64; ++ks)
+          tmem_cp_32x128_x4(tmem + KV_T_KSF + 4 * ks, desc_at(t_sf, s0 + L::K_SF + ks * 512));
       }
       __syncwarp();
-      // dK += dS^T Q^F (PLAIN: Q from its ring slot, already waited for by S_i)
-      mbar_wait(&bars[KV_B_DS_FULL], ph);
-      if (!PLAIN) mbar_wait(&bars[KV_B_QH_FULL], ph);
-      tc_fence_after();
+      if (ni > 0) issue_s(g);
+      for (int ii = 0; ii < ni; ++ii, ++g) {
+        const uint32_t ph = g & 1;
+        const int s = g % NDO;
+        const uint32_t do_h = s0 + L::DO_H0 + s * TILE * D * 2;
+        mbar_wait(&bars[KV_B_DO_FULL + s], (g / NDO) & 1);
+        // dP_i (N = 128) into S's columns once every compute warp holds S_i; S_{i+1}
+        // once every compute warp holds dP_i
+        if (ii == 0) mbar_wait(&bars[KV_B_V], it & 1);
+        mbar_wait(&bars[KV_B_S_EMPTY], ph);
+        issue_dp(g, 0, do_h);
+        if (ii + 1 < ni) {
+          mbar_wait(&bars[KV_B_DP_EMPTY], ph);
+          issue_s(g + 1);
+        }
+        // dV += P^F^T dO (the item's first dV overwrites: the compute warps read the
+        // previous item's dV before they produced this P^F)
+        mbar_wait(&bars[KV_B_PF_FULL], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int ks = 0; ks < TILE / 16; ++ks)
+            mma_f16_ss(tmem + KV_T_DV, desc_at(t_mn, p_h + ks * 256), desc_at(t_mn, do_h + ks * 256), id_kv,
+                       (ii > 0 || ks > 0));
+          tc_commit(&bars[KV_B_PF_FREE]);
+          tc_commit(&bars[KV_B_DO_EMPTY + s]);
+          if (ii == ni - 1) tc_commit(&bars[KV_B_DV_DONE]);  // dV final: its epilogue overlaps the last dK
+        }
+        __syncwarp();
+        // dK += dS^T Q^F (PLAIN: Q from its ring slot, already waited for by S_i)
+        mbar_wait(&bars[KV_B_DS_FULL], ph);
+        if (!PLAIN) mbar_wait(&bars[KV_B_QH_FULL], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t qf = PLAIN ? s0 + L::QC0 + (g & 1) * L::QC_BYTES : q_h;
+          for (int ks = 0; ks < TILE / 16; ++ks)
+            mma_f16_ss(tmem + KV_T_DK, desc_at(t_mn, ds_h + ks * 256), desc_at(t_mn, qf + ks * 256), id_kv,
+                       (ii > 0 || ks > 0));
+          tc_commit(&bars[KV_B_DS_FREE]);
+          tc_commit(&bars[PLAIN ? KV_B_QC_EMPTY + (g & 1) : KV_B_QH_EMPTY]);
+        }
+        __syncwarp();
+      }
       if (elect_one()) {
-        const uint32_t qf = PLAIN ? s0 + L::QC0 + (ii & 1) * L::QC_BYTES : q_h;
-        for (int ks = 0; ks < TILE / 16; ++ks)
-          mma_f16_ss(tmem + KV_T_DK, desc_at(t_mn, ds_h + ks * 256), desc_at(t_mn, qf + ks * 256), id_kv,
-                     (ii > 0 || ks > 0));
-        tc_commit(&bars[KV_B_DS_FREE]);
-        tc_commit(&bars[PLAIN ? KV_B_QC_EMPTY + (ii & 1) : KV_B_QH_EMPTY]);
+        if (ni == 0) tc_commit(&bars[KV_B_DV_DONE]);  // one DV_DONE / DONE phase per item
+        tc_commit(&bars[KV_B_DONE]);
       }
       __syncwarp();
     }
-    if (elect_one()) tc_commit(&bars[KV_B_DONE]);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ compute warps
     const int row = 32 * (warp & 3) + lane;
     const int kg = warp >> 2;
     const int kb = kg * KPT;      // first key (in tile) of this thread
-    const int dph = AQ_BWD_DPFULL ? 0 : kb / HALF;  // dP half holding those keys
     const uint32_t t_lane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
     const bool f16 = PLAIN && p.plain_fmt == 0;  // fp16 operand tiles (PLAIN fp16 mode)
@@ -465,10 +504,13 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       l2 = (t < ni && qq < p.n_q) ? p.lse[head * p.n_q + qq] : 0.f;
       dq = t < ni ? p.delta[head * (q_tiles * TILE) + qq] : 0.f;
     };
+    int g = 0;  // tile count of the CTA (barrier phases run on across items)
+    for (int it = 0; it < nit; ++it) {
+    if (it > 0) set_item(it);
     float L_next, D_next;
     row_stats(0, L_next, D_next);
-    for (int ii = 0; ii < ni; ++ii) {
-      const uint32_t ph = ii & 1;
+    for (int ii = 0; ii < ni; ++ii, ++g) {
+      const uint32_t ph = g & 1;
       const int64_t q = static_cast<int64_t>(i_begin + ii) * TILE + row;
       const bool qvalid = q < p.n_q;
       const float L2 = L_next * 1.44269504088896340736f;
@@ -480,7 +522,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
       float pr[KPT];
       AQ_BPROF(tq_ = clock64();)
       mbar_wait(&bars[KV_B_S_FULL], ph);
-      if (ii == 0) AQ_TL(1);
+      if (ii == 0 && it == 0) AQ_TL(1);
       tc_fence_after();
       tmem_load_f<KPT>(t_lane + KV_T_S + kb, pr);
       tc_fence_before();
@@ -493,7 +535,7 @@ __device__ __forceinline__ void bwd_kv_tile(const BwdParams& p, uint8_t* smem, i
         for (int c = 0; c < KPT; ++c) pr[c] = (c <= lim) ? pr[c] : 0.f;
       }
       AQ_BPROF(tn_ = clock64(); pr_[1] += tn_ - tq_; tq_ = tn_;)
-      if (ii > 0) mbar_wait(&bars[KV_B_PF_FREE], (ii - 1) & 1);
+      if (g > 0) mbar_wait(&bars[KV_B_PF_FREE], (g - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[2] += tn_ - tq_; tq_ = tn_;)
       // P^F (or P) -> bf16 [query][key] T8x8
       if (!PLAIN && MX && p.fq_p) {  // MXFP4 P^F: 32-key UE8M0 blocks, dequantized exactly to bf16
@@ -575,43 +617,45 @@ if (PLAIN || !(MX && p.fq_p)) {
       mbar_arrive(&bars[KV_B_PF_FULL]);
       AQ_BPROF(tn_ = clock64(); pr_[3] += tn_ - tq_; tq_ = tn_;)
       // dS = (dP - D) . P / sqrt(d) -> bf16
-      mbar_wait(&bars[KV_B_DP_FULL + dph], ph);
+      mbar_wait(&bars[KV_B_DP_FULL], ph);
       tc_fence_after();
       float dp[KPT];
-      tmem_load_f<KPT>(t_lane + (AQ_BWD_DPFULL ? KV_T_S + kb : KV_T_DP + kb % HALF), dp);
+      tmem_load_f<KPT>(t_lane + KV_T_S + kb, dp);
       tc_fence_before();
-      mbar_arrive(&bars[KV_B_DP_EMPTY + dph]);
+      mbar_arrive(&bars[KV_B_DP_EMPTY]);
       AQ_BPROF(tn_ = clock64(); pr_[4] += tn_ - tq_; tq_ = tn_;)
-      if (ii > 0) mbar_wait(&bars[KV_B_DS_FREE], (ii - 1) & 1);
+      if (g > 0) mbar_wait(&bars[KV_B_DS_FREE], (g - 1) & 1);
       AQ_BPROF(tn_ = clock64(); pr_[5] += tn_ - tq_; tq_ = tn_;)
       store_ds<KPT>(ds_h, row, kb, dp, pr, Dq, p.inv_sqrt_d, f16);
       fence_async_smem();
       mbar_arrive(&bars[KV_B_DS_FULL]);
       AQ_BPROF(tn_ = clock64(); pr_[6] += tn_ - tq_; tq_ = tn_;)
     }
-    AQ_BPROF(if (lane == 0) { for (int e = 0; e < 7; ++e) atomicAdd(&g_bprof[e], pr_[e]); atomicAdd(&g_bprof[14], static_cast<unsigned long long>(ni)); })
+    AQ_BPROF(if (lane == 0) { for (int e = 0; e < 7; ++e) { atomicAdd(&g_bprof[e], pr_[e]); pr_[e] = 0; } atomicAdd(&g_bprof[14], static_cast<unsigned long long>(ni)); })
     AQ_TL(2);
     // epilogue: dV rows as soon as the last dV MMA is done (while the last dK
-    // MMA runs), then dK rows (thread = key row, D/NKG columns)
+    // MMA runs), then dK rows (thread = key row, D/NKG columns); the next
+    // item's S / dP run meanwhile
     const int64_t key = k0 + row;
     constexpr int DH = D / NKG;
 #pragma unroll
     for (int w2 = 0; w2 < 2; ++w2) {
       const int which = 1 - w2;
       if (ni > 0) {
-        mbar_wait(&bars[which ? KV_B_DV_DONE : KV_B_DONE], 0);
+        mbar_wait(&bars[which ? KV_B_DV_DONE : KV_B_DONE], it & 1);
         tc_fence_after();
       }
-      float g[DH];
+      float gr[DH];
       if (ni > 0) {
-        tmem_load_f<DH>(t_lane + (which ? KV_T_DV : KV_T_DK) + kg * DH, g);
+        tmem_load_f<DH>(t_lane + (which ? KV_T_DV : KV_T_DK) + kg * DH, gr);
       } else {
 #pragma unroll
-        for (int e = 0; e < DH; ++e) g[e] = 0.f;  // no visible query: zero gradient
+        for (int e = 0; e < DH; ++e) gr[e] = 0.f;  // no visible query: zero gradient
       }
       if (key < p.n_k)
-        store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + kg * DH, p.g_dt, g, which ? p.dv_mul : p.dk_mul);
+        store_run<DH>(which ? p.dv : p.dk, (head * p.n_k + key) * D + kg * DH, p.g_dt, gr, which ? p.dv_mul : p.dk_mul);
     }
+    }  // items
   }
 
   tc_fence_before();
@@ -925,11 +969,33 @@ __device__ __forceinline__ void bwd_q_tile(const BwdParams& p, uint8_t* smem, in
 // MX: the MXFP4 instance (S recomputed on kind::mxf4 block32, P^F in 32-key
 // UE8M0 blocks dequantized exactly to bf16; everything else is shared).
 // PLAIN: quantized=False (16-bit S recompute, P unquantized; flash.py:344-349).
+// KV items pair up when the key and query tilings match and the tile count is even
+__host__ __device__ __forceinline__ bool pair_kv(const BwdParams& p, int kv_tiles, int q_tiles) {
+  return AQ_BWD_PAIR && kv_tiles == q_tiles && p.n_q == p.n_k && (kv_tiles & 1) == 0;
+}
+
 template <int D, bool MX, bool PLAIN = false>
 __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1) attn_bwd_kernel(const BwdParams p, int kv_tiles, int q_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int64_t head = blockIdx.y;
   const int r = blockIdx.x;
+  if (pair_kv(p, kv_tiles, q_tiles)) {
+    // KV CTAs run key tiles (c, T-1-c): T+1 query tiles each under causal masking
+    // (T non-causal); order KV pair 0, Q tile T-1, KV pair 1, Q tile T-2, ...
+    const int h = kv_tiles / 2;
+    AQ_TL(0);
+    if (r < 2 * h && (r & 1) == 0) bwd_kv_tile<D, MX, PLAIN>(p, smem, r >> 1, head, kv_tiles - 1 - (r >> 1));
+    else bwd_q_tile<D, MX, PLAIN>(p, smem, q_tiles - 1 - (r < 2 * h ? (r >> 1) : r - h), head);
+#ifdef AQ_BWD_PROFILE
+    if (threadIdx.x == 0 && tl_cta() < kTimelineCtas) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      g_btl[tl_cta()][3] = gtimer();
+      g_btl[tl_cta()][4] = smid | (static_cast<unsigned long long>(r < 2 * h && (r & 1) == 0) << 16);
+    }
+#endif
+    return;
+  }
   const int m = min(kv_tiles, q_tiles);
   int kv = -1, qt = -1;
   if (r < 2 * m) {
@@ -1041,7 +1107,8 @@ cudaError_t launch(const BwdParams& p, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int kv_tiles = static_cast<int>(ceil_div(p.n_k, TILE)), q_tiles = static_cast<int>(ceil_div(p.n_q, TILE));
-  kern<<<dim3(static_cast<unsigned>(kv_tiles + q_tiles), static_cast<unsigned>(p.heads)), Cfg<D>::NUM_THREADS, smem, st>>>(
+  const int gx = pair_kv(p, kv_tiles, q_tiles) ? kv_tiles / 2 + q_tiles : kv_tiles + q_tiles;
+  kern<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(p.heads)), Cfg<D>::NUM_THREADS, smem, st>>>(
       p, kv_tiles, q_tiles);
   return cudaGetLastError();
 }

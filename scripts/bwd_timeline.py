@@ -24,7 +24,8 @@ for _ in range(3):
     aq.attn_backward(q, k, v, do, o, ohp, lse, causal=True, fwd_workspace=ws)
 torch.cuda.synchronize()
 heads = B * H
-ctas = heads * 2 * ((N + 127) // 128)
+T = (N + 127) // 128
+ctas = heads * (T // 2 + T) if (T % 2 == 0 and os.environ.get("AQ_TL_PAIRED", "1") == "1") else heads * 2 * T
 buf = (ctypes.c_ulonglong * (5 * ctas))()
 assert lib.aq_debug_bwd_timeline(buf, ctas) == 0, "not a -DAQ_BWD_PROFILE build"
 a = np.frombuffer(buf, dtype=np.uint64).reshape(ctas, 5).astype(np.int64)
