@@ -1043,13 +1043,35 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const void* d_o, int do_dt
     const int64_t tile = h * q_tiles + q / TILE;
     uint8_t* tdst = do_h + tile * h_tile_bytes(D);
     float acc = 0.f;
+    // bf16 dO and O_ref (the autograd path): all of this lane's 16-byte loads are
+    // issued before any tile store, so they are in flight together (the stores
+    // could alias the inputs as far as the compiler knows)
+    const bool bf = do_dt == 1 && o_dt == 1;
+    uint4 gw[NCG / 4], ow[NCG / 4];
+    if (bf && valid) {
+#pragma unroll
+      for (int i = 0; i < NCG / 4; ++i) {
+        const int64_t base = base_row + (cg + 4 * i) * 8;
+        gw[i] = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(d_o) + base);
+        ow[i] = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(o_ref) + base);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < NCG / 4; ++i) {
       const int c8 = cg + 4 * i;
       float g[8], o[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) g[e] = o[e] = 0.f;
-      if (valid) {
+      if (valid && bf) {
+        const uint32_t gg[4] = {gw[i].x, gw[i].y, gw[i].z, gw[i].w}, oo[4] = {ow[i].x, ow[i].y, ow[i].z, ow[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          g[2 * e] = __uint_as_float(gg[e] << 16);
+          g[2 * e + 1] = __uint_as_float(gg[e] & 0xFFFF0000u);
+          o[2 * e] = __uint_as_float(oo[e] << 16);
+          o[2 * e + 1] = __uint_as_float(oo[e] & 0xFFFF0000u);
+        }
+      } else if (valid) {
         const int64_t base = base_row + c8 * 8;
         if (do_dt == 1) {
           const uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(d_o) + base);
