@@ -248,22 +248,39 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(RowsArgs a) {
 // output-pointer branches, no reference-layout or fake-quant stores: one
 // thread = 32 columns (two blocks) of one row, one 16-byte code store and one
 // 2-byte scale store.
+// n = rows per head; a ragged last tile (n % 128 != 0, e.g. C3's N = 32760) is
+// zero-padded exactly as the general kernel pads it (zero blocks through the
+// same quantizer, no non-finite check).
 template <int D, bool FQH, bool F32 = false>
-__global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __restrict__ xv, int64_t rows,
-                                                                  uint8_t* __restrict__ codes_t,
+__global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __restrict__ xv, int64_t heads,
+                                                                  int64_t n, uint8_t* __restrict__ codes_t,
                                                                   uint8_t* __restrict__ sf_t,
                                                                   uint8_t* __restrict__ fqh_t, int fqh_dt,
                                                                   float inv_ts, int* __restrict__ nonfinite) {
   constexpr int NPAIR = D / 32;
-  const int64_t total = rows * NPAIR;
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t total = heads * n_pad * NPAIR;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int bp = static_cast<int>(t & (NPAIR - 1));
-    const int64_t row = t / NPAIR;
-    const int64_t tile = row / TILE;
-    const int rr = static_cast<int>(row % TILE);
+    const int64_t rowp = t / NPAIR;  // padded row over all heads (tiles of consecutive heads are consecutive)
+    const int64_t tile = rowp / TILE;
+    const int rr = static_cast<int>(rowp % TILE);
+    int64_t row = rowp;              // source row
+    bool real = true;
+    if (n_pad != n) {
+      const int64_t h = rowp / n_pad, r = rowp % n_pad;
+      real = r < n;
+      row = h * n + r;
+    }
     Block16 q[2];
-    if constexpr (F32) {  // fp32 input (the sage3 centred operands)
+    if (!real) {
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      quantize_block16<FQH, true>(v, q[0]);
+      q[1] = q[0];
+    } else if constexpr (F32) {  // fp32 input (the sage3 centred operands)
       const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(xv) + row * D + bp * 32);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(256) quantize_rows_tiled_kernel(const void* __
       }
     }
     // NaN / Inf input (codec.py:313-314): flag it for the host to raise InvalidValue
-    if (nonfinite != nullptr && !(q[0].finite && q[1].finite)) atomicOr(nonfinite, 1);
+    if (real && nonfinite != nullptr && !(q[0].finite && q[1].finite)) atomicOr(nonfinite, 1);
     if (FQH) {
       // the 16-bit fake-quantized operand tile the backward reuses (T8x8)
       uint8_t* base = fqh_t + tile * h_tile_bytes(D);
@@ -648,26 +665,24 @@ cudaError_t launch_tile16(const void* x, int x_dt, int64_t heads, int64_t n, int
 cudaError_t launch_quantize_rows(const RowsArgs& a, cudaStream_t st) {
   const int64_t n_pad = (a.codes_t || a.sf_t || a.fqh_t) ? ceil_div(a.n, TILE) * TILE : a.n;
   const bool fast = (a.x_dt == kBF16 || a.x_dt == kF32) && a.codes_t && a.sf_t && !a.fq && !a.codes_ref &&
-                    !a.scales_ref && a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    !a.scales_ref && a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
   if (fast && a.x_dt == kF32 && !a.fqh_t) {
-    const int64_t rows = a.heads * a.n;
-    const int g = grid_for(rows * (a.cols / 32));
-    if (a.cols == 128) quantize_rows_tiled_kernel<128, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
-    else quantize_rows_tiled_kernel<64, false, true><<<g, 256, 0, st>>>(a.x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
+    const int g = grid_for(a.heads * n_pad * (a.cols / 32));
+    if (a.cols == 128) quantize_rows_tiled_kernel<128, false, true><<<g, 256, 0, st>>>(a.x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
+    else quantize_rows_tiled_kernel<64, false, true><<<g, 256, 0, st>>>(a.x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     return cudaGetLastError();
   }
   if (fast && a.x_dt == kBF16) {
-    const int64_t rows = a.heads * a.n;
-    const int g = grid_for(rows * (a.cols / 32));
+    const int g = grid_for(a.heads * n_pad * (a.cols / 32));
     const auto* x = a.x;
     uint8_t* fqh = static_cast<uint8_t*>(a.fqh_t);
     if (a.cols == 128) {
-      if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
-      else quantize_rows_tiled_kernel<128, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
+      if (fqh) quantize_rows_tiled_kernel<128, true><<<g, 256, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
+      else quantize_rows_tiled_kernel<128, false><<<g, 256, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     } else {
-      if (fqh) quantize_rows_tiled_kernel<64, true><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
-      else quantize_rows_tiled_kernel<64, false><<<g, 256, 0, st>>>(x, rows, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
+      if (fqh) quantize_rows_tiled_kernel<64, true><<<g, 256, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, fqh, a.fqh_dt, a.inv_ts, a.nonfinite);
+      else quantize_rows_tiled_kernel<64, false><<<g, 256, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, nullptr, 0, a.inv_ts, a.nonfinite);
     }
     return cudaGetLastError();
   }
