@@ -710,32 +710,51 @@ __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat
                                                                uint8_t* __restrict__ sf_t, float inv_ts,
                                                                int* __restrict__ nonfinite) {
   // 32 contiguous token rows per slab, double-buffered 1-D bulk copies (the
-  // column reads touch one row per instruction: no padding needed)
+  // column reads touch one row per instruction: no padding needed). A ragged
+  // head (n % 128 != 0, e.g. C3's N = 32760) is zero-padded to whole tiles, as
+  // quantize_padded pads V^T (codec.py:359-381): the slab's rows past n are
+  // zeroed in shared memory and quantized like the general kernel does.
   __shared__ __align__(128) __nv_bfloat16 slab[2][32][D];
   __shared__ __align__(8) uint64_t bar[2];
-  constexpr uint32_t SLAB_BYTES = 32 * D * 2;
-  const int64_t nslabs = heads * (n / 32);
+  const int64_t n_pad = ceil_div(n, TILE) * TILE;
+  const int64_t spp = n_pad / 32;  // slabs per head
+  const int64_t nslabs = heads * spp;
   const int c = threadIdx.x;
+  auto valid_rows = [&](int64_t sidx) {
+    const int64_t left = n - (sidx % spp) * 32;
+    return static_cast<int>(left < 0 ? 0 : (left < 32 ? left : 32));
+  };
+  auto issue = [&](int64_t sidx, int b) {  // thread 0
+    const int valid = valid_rows(sidx);
+    if (valid > 0) {
+      mbar_expect_tx(&bar[b], static_cast<uint32_t>(valid) * D * 2);
+      bulk_g2s(&slab[b][0][0], x + ((sidx / spp) * n + (sidx % spp) * 32) * D, static_cast<uint32_t>(valid) * D * 2,
+               &bar[b]);
+    } else {
+      mbar_arrive(&bar[b]);
+    }
+  };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
-    if (blockIdx.x < nslabs) {
-      mbar_expect_tx(&bar[0], SLAB_BYTES);
-      bulk_g2s(&slab[0][0][0], x + static_cast<int64_t>(blockIdx.x) * 32 * D, SLAB_BYTES, &bar[0]);
-    }
+    if (blockIdx.x < nslabs) issue(blockIdx.x, 0);
   }
   int it = 0;
   for (int64_t sidx = blockIdx.x; sidx < nslabs; sidx += gridDim.x, ++it) {
-    const int64_t tok0 = sidx * 32;  // flat token index (n % 128 == 0: slabs never straddle heads)
+    const int64_t tok0 = sidx * 32;  // flat padded token index (n_pad % 128 == 0: slabs never straddle heads)
     const int buf = it & 1;
     __syncthreads();  // every thread is done with slab[buf ^ 1]
     if (threadIdx.x == 0 && sidx + gridDim.x < nslabs) {
       fence_async_smem();
-      mbar_expect_tx(&bar[buf ^ 1], SLAB_BYTES);
-      bulk_g2s(&slab[buf ^ 1][0][0], x + (sidx + gridDim.x) * 32 * D, SLAB_BYTES, &bar[buf ^ 1]);
+      issue(sidx + gridDim.x, buf ^ 1);
     }
     mbar_wait(&bar[buf], (it >> 1) & 1);
+    const int valid = valid_rows(sidx);  // uniform over the CTA
+    if (valid < 32) {
+      for (int r = valid; r < 32; ++r) slab[buf][r][c] = __float2bfloat16_rn(0.f);
+      __syncthreads();
+    }
     Block16 q[2];
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
@@ -756,19 +775,21 @@ __global__ void __launch_bounds__(D) quantize_cols_slab_kernel(const __nv_bfloat
 }
 
 cudaError_t launch_quantize_cols(const RowsArgs& a, cudaStream_t st) {
+  // fast paths: bf16, contiguous heads, MMA tile outputs only; the inference
+  // (slab) kernel also takes a ragged last tile, the training kernel whole tiles
   const bool fast = a.x_dt == kBF16 && a.codes_t && a.sf_t && !a.fq && !a.codes_ref && !a.scales_ref &&
-                    a.n % TILE == 0 && a.ld == a.cols && a.hs == a.n * a.cols &&
+                    a.ld == a.cols && a.hs == a.n * a.cols &&
                     (a.cols == 64 || a.cols == 128) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
-  if (fast) {
+  const bool fqh = a.fqh_t || a.fqh2_t;
+  if (fast && (!fqh || a.n % TILE == 0)) {
     int64_t g = a.heads * (a.n / 64);
     if (g > 148 * 64) g = 148 * 64;
     const auto* x = static_cast<const __nv_bfloat16*>(a.x);
-    const bool fqh = a.fqh_t || a.fqh2_t;
     auto* h1 = static_cast<uint8_t*>(a.fqh_t);
     auto* h2 = static_cast<uint8_t*>(a.fqh2_t);
     const int gg = static_cast<int>(g);
     if (!fqh) {
-      int64_t gs = a.heads * (a.n / 32);
+      int64_t gs = a.heads * (ceil_div(a.n, TILE) * TILE / 32);
       if (gs > 148 * 16) gs = 148 * 16;
       if (a.cols == 128)
         quantize_cols_slab_kernel<128><<<static_cast<int>(gs), 128, 0, st>>>(x, a.heads, a.n, a.codes_t, a.sf_t, a.inv_ts, a.nonfinite);
